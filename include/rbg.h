@@ -1,0 +1,182 @@
+/*
+ * rbg.h -- C ABI of the B200-native RB-greedy / pivoted-QR hot path (arXiv 1805.06124).
+ *
+ * The library computes, on one or more B200 GPUs, the reduced-basis greedy of
+ * Algorithm 3, which Proposition 5.5 shows is
+ * modified Gram-Schmidt with column pivoting (Algorithm 2), using the
+ * residual recurrence of Sec. 6.1.2 and Hoffmann's iterated MGS with
+ * kappa = 2 for each new basis vector:
+ *
+ *   r2_j = ||s_j||_w^2                                             (sweep 0)
+ *   repeat:  (J, m) = argmax_j r2_j (ties: lowest global index)   (pivot search)
+ *            err_k = sqrt(max(m, 0)); stop if err_k < tol, k = k_max, or all selected
+ *            q_{k+1} = IMGS(s_J) against q_1..q_k; stop RANK if degenerate
+ *            R(k+1, j) = <q_{k+1}, s_j>_w and r2_j -= |R(k+1, j)|^2 for every column
+ *
+ * with <x, y>_w = sum_i w_i conj(x_i) y_i.  Every floating-point result follows the
+ * canonical arithmetic contract of DESIGN.md (lane counts L_S = 32 for the sweep and
+ * L_I = 2048 for IMGS), so results are bit-reproducible and independent of the number of
+ * GPUs the columns are sharded over.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns rbg_status; none aborts, throws or exits.  On failure a
+ *    thread-local message is available from rbg_last_error().
+ *  - Matrices are column-major.  A complex element is two doubles (re, im) interleaved.
+ *    S is N x M with column j at S + j*ld elements; ld >= N.
+ *  - Ownership: the library owns the context and every buffer it allocates; outputs are
+ *    copied into caller-owned buffers.  A borrowed device S (rbg_desc.borrow = 1) must
+ *    stay alive and unmodified until rbg_destroy.
+ *  - All GPU work is enqueued on one CUDA stream (rbg_desc.stream, or a stream the library
+ *    creates).  Getters synchronise that stream.
+ */
+#ifndef RBG_H
+#define RBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rbg_ctx rbg_ctx;  /* opaque, owned by the library */
+
+typedef enum { RBG_REAL_F64 = 1, RBG_COMPLEX_F64 = 2 } rbg_dtype;
+
+typedef enum {
+    RBG_OK = 0,
+    RBG_EINVAL = 1,      /* bad argument (sizes, tol, weights, null pointer, alignment) */
+    RBG_ENONFINITE = 2,  /* S holds NaN/Inf; message gives the first (row, col)         */
+    RBG_ENOMEM = 3,      /* device or host allocation failed                           */
+    RBG_ECUDA = 4,       /* CUDA runtime error                                         */
+    RBG_ENCCL = 5,       /* NCCL missing or failed                                     */
+    RBG_ESTATE = 6       /* call not valid in the context's current state              */
+} rbg_status;
+
+/* Why the greedy stopped.  Stop reasons are results, not errors. */
+typedef enum {
+    RBG_STOP_NONE = 0,          /* still running (or not started)                         */
+    RBG_STOP_TOL = 1,           /* err_k < tol (Algorithm 3 loop test)      */
+    RBG_STOP_KMAX = 2,          /* k = k_max basis vectors                                */
+    RBG_STOP_RANK = 3,          /* IMGS found the pivot numerically in span(Q) (R7, R17)   */
+    RBG_STOP_ALL_SELECTED = 4   /* every column already selected                          */
+} rbg_stop;
+
+typedef enum { RBG_MEM_HOST = 0, RBG_MEM_DEVICE = 1 } rbg_mem;
+
+/* Column-sharded execution: NONE = one GPU owns all columns;
+ * NCCL = ncclAllGather of {maxloc record, candidate column} per iteration;
+ * EXTERNAL = the caller moves the exchange buffers itself between rbg_iter_local and
+ * rbg_iter_finish (used to run the sharded path on one GPU in tests). */
+typedef enum { RBG_COMM_NONE = 0, RBG_COMM_NCCL = 1, RBG_COMM_EXTERNAL = 2 } rbg_comm;
+
+typedef struct rbg_desc {
+    const void *S;        /* N x M_loc snapshot block, column-major                      */
+    rbg_mem S_mem;        /* where S lives                                               */
+    int64_t N;            /* rows (grid points), >= 1                                    */
+    int64_t M;            /* columns on this rank (M_loc), >= 1                          */
+    int64_t ld;           /* column stride in elements, >= N (0 => N)                    */
+    int borrow;           /* device S only: 1 = use in place (16-B aligned columns; real
+                             dtype needs even ld), 0 = copy                              */
+    const double *w;      /* N positive finite weights, NULL => all ones                 */
+    rbg_mem w_mem;
+    rbg_dtype dtype;
+    double tol;           /* >= 0; stop when err_k < tol                                 */
+    int64_t k_max;        /* 1 <= k_max <= min(N, M_global)                              */
+    void *stream;         /* cudaStream_t to enqueue on; NULL => library-owned stream    */
+    int device;           /* CUDA ordinal; -1 => current device                          */
+    int check_finite;     /* 1 (default) => scan S for NaN/Inf at create                 */
+    rbg_comm comm;
+    int rank, world;      /* this rank and the number of ranks (world = 1 unless sharded) */
+    int64_t col_offset;   /* global index of local column 0                              */
+    int64_t M_global;     /* total columns over all ranks (0 => M)                       */
+    uint8_t nccl_id[128]; /* ncclUniqueId from rbg_get_unique_id on rank 0 (comm = NCCL) */
+} rbg_desc;
+
+typedef struct rbg_stats {
+    int64_t k;              /* basis vectors built                                      */
+    int64_t sweeps;         /* coefficient sweeps timed (excluding sweep 0)              */
+    double t_init_ms;       /* sweep 0 (norms)                                          */
+    double t_sweep_ms;      /* sum over sweeps of the fused sweep kernel (T_pivot)       */
+    double t_xchg_ms;       /* sum of exchange time (C_j); 0 on one GPU                  */
+    double t_imgs_ms;       /* sum of pivot decision + IMGS (T_IMGS)                     */
+    double t_total_ms;      /* first event to last event (T_j summed)      */
+} rbg_stats;
+
+/* Fill *d with defaults: ld = 0, borrow = 0, w = NULL, device = -1, check_finite = 1,
+ * comm = NONE, rank = 0, world = 1, col_offset = 0, M_global = 0. */
+void rbg_desc_init(rbg_desc *d);
+
+/* North-star entry point: host S (N x M, ld = N) and host w (NULL => ones).  The matrix
+ * is copied to the current device.  Errors: EINVAL (N < 1, M < 1, k_max outside
+ * [1, min(N, M)], tol < 0 or NaN, w_i <= 0 or non-finite, unknown dtype, NULL S or ctx),
+ * ENONFINITE (first NaN/Inf position in the message), ENOMEM, ECUDA. */
+rbg_status rbg_create(rbg_ctx **ctx, const void *S, int64_t N, int64_t M, const double *w,
+                      double tol, int64_t k_max, rbg_dtype dtype);
+
+/* Extended create (memory space, borrowing, stream, device, sharding). */
+rbg_status rbg_create_ex(rbg_ctx **ctx, const rbg_desc *desc);
+
+/* ncclGetUniqueId (rank 0 calls it; the caller broadcasts the 128 bytes).  ENCCL if
+ * libnccl.so.2 cannot be loaded. */
+rbg_status rbg_get_unique_id(uint8_t out[128]);
+
+/* Run the greedy to its stop reason (blocking).  ESTATE for comm = EXTERNAL. */
+rbg_status rbg_run(rbg_ctx *ctx);
+
+/* Enqueue up to n more iterations without synchronising (the first call also enqueues
+ * sweep 0).  Iterations after the stop decision are no-ops on the device. */
+rbg_status rbg_step(rbg_ctx *ctx, int64_t n);
+
+/* Per-phase CUDA-event timing of subsequent iterations (0 = off, the default). */
+rbg_status rbg_set_timing(rbg_ctx *ctx, int on);
+
+/* Capture iterations into CUDA graphs of `batch` iterations (0 = plain launches). */
+rbg_status rbg_set_graph_batch(rbg_ctx *ctx, int batch);
+
+/* Synchronise the context's stream. */
+rbg_status rbg_sync(rbg_ctx *ctx);
+
+/* k = basis size, M_loc = local columns, why = stop reason (NONE while running). */
+rbg_status rbg_result_info(rbg_ctx *ctx, int64_t *k, int64_t *M_loc, rbg_stop *why);
+
+/* Outputs (replicated on every rank unless noted).  Host buffers unless on_device. */
+rbg_status rbg_get_pivots(rbg_ctx *ctx, int64_t *out);        /* k global column ids   */
+rbg_status rbg_get_errors(rbg_ctx *ctx, double *out);         /* k+1: err_0 .. err_k   */
+rbg_status rbg_get_nu(rbg_ctx *ctx, int32_t *out);            /* k IMGS sweep counts   */
+rbg_status rbg_get_rdiag(rbg_ctx *ctx, double *out);          /* k IMGS norms R(i,i)   */
+/* Q: N x k column-major, column i at out + i*ldq elements (ldq >= N).                   */
+rbg_status rbg_get_basis(rbg_ctx *ctx, void *out, int64_t ldq, int on_device);
+/* R: k x M_loc ROW-major, R(i, j) = <q_i, s_j>_w at out + i*ldr + j elements
+ * (ldr >= M_loc); column-sharded over ranks.                                            */
+rbg_status rbg_get_R(rbg_ctx *ctx, void *out, int64_t ldr, int on_device);
+/* r2: M_loc squared residuals after the last sweep (selected columns = -inf).           */
+rbg_status rbg_get_r2(rbg_ctx *ctx, double *out, int on_device);
+rbg_status rbg_get_stats(rbg_ctx *ctx, rbg_stats *out);
+/* Per-iteration phase times (timing mode): n entries each, any pointer may be NULL.     */
+rbg_status rbg_get_timings(rbg_ctx *ctx, double *sweep_ms, double *xchg_ms, double *imgs_ms,
+                           int64_t n);
+
+/* Sharded path driven by the caller (comm = EXTERNAL).  One iteration is
+ *   rbg_iter_local (sweep + maxloc + pack the local candidate into the send buffer),
+ *   the caller's all-gather of send buffers into every rank's receive buffer
+ *   (rank p's bytes at recv + p * bytes), then rbg_iter_finish (pivot decision + IMGS). */
+rbg_status rbg_iter_local(rbg_ctx *ctx);
+rbg_status rbg_iter_finish(rbg_ctx *ctx);
+rbg_status rbg_xchg_buffers(rbg_ctx *ctx, void **send, void **recv, size_t *bytes_per_rank);
+/* Convenience for tests: all-gather the send buffers of `world` EXTERNAL contexts on the
+ * same device (device-to-device copies), ctxs[p] holding rank p. */
+rbg_status rbg_emulate_allgather(rbg_ctx **ctxs, int world);
+
+/* Lane counts of the canonical arithmetic contract this build implements. */
+void rbg_lanes(int *L_S, int *L_I);
+const char *rbg_version(void);
+const char *rbg_last_error(void);
+
+/* NULL-safe; frees everything the library allocated for ctx. */
+void rbg_destroy(rbg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBG_H */

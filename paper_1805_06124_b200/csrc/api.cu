@@ -1,0 +1,700 @@
+// api.cu -- the C ABI (include/rbg.h): argument checking, device memory, the iteration
+// loop (plain launches or CUDA-graph batches), sharded exchange, getters.
+//
+// One iteration of Algorithm 3 is enqueued as three stream-ordered
+// steps with no host synchronisation:
+//     local  : fused sweep with q_{k-1} (sweep 0 = weighted norms) + local maxloc
+//              [+ pack of the local candidate column when sharded]        -> sweep.cu
+//     xchg   : ncclAllGather of one slot per rank (sharded runs only)     -> comm.cpp
+//     finish : global pivot decision, stop test, IMGS of s_J -> q_k        -> imgs.cu
+// The loop state (k, stop flag, maxloc) lives in device memory, so the host only
+// enqueues; steps after the stop decision return immediately on the device.  The cost
+// model T_j = T_pivot + T_IMGS + C_j is measured with CUDA events
+// around the three steps when timing is on.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "kernels.h"
+#include "rbg.h"
+
+using namespace rbg;
+
+namespace {
+
+thread_local std::string g_err;
+
+rbg_status fail(rbg_status s, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(e_ == cudaErrorMemoryAllocation ? RBG_ENOMEM : RBG_ECUDA,             \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define TRY(call)                          \
+    do {                                   \
+        rbg_status s_ = (call);            \
+        if (s_ != RBG_OK) return s_;       \
+    } while (0)
+
+struct PhaseEvents {
+    cudaEvent_t e[4];
+};
+
+}  // namespace
+
+struct rbg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool cplx = true;
+    long long N = 0, M = 0, nvec = 0, ldv = 0, ldq_v = 0;
+    size_t se = 16;  // bytes per element
+    double2 *S = nullptr;
+    bool own_S = false;
+    double *w = nullptr;
+    double2 *Q = nullptr, *WQ = nullptr;
+    double *R = nullptr, *r2 = nullptr;
+    DevState *st = nullptr;
+    double *errors = nullptr, *rdiag = nullptr;
+    long long *piv = nullptr;
+    int *nu = nullptr;
+    Rec *recs = nullptr;
+    unsigned *ticket = nullptr;
+    double tol = 0.0;
+    long long k_max = 0;
+    rbg_comm comm = RBG_COMM_NONE;
+    int rank = 0, world = 1;
+    long long col_offset = 0, M_global = 0;
+    unsigned char *send = nullptr, *recv = nullptr;
+    size_t slot = 0;
+    void *nccl = nullptr;
+    int num_sms = 148;
+    SweepConfig cfg_init{}, cfg_sweep{};
+    bool started = false;
+    bool local_pending = false;  // EXTERNAL: local done, finish not yet
+    long long iters = 0;         // iterations enqueued
+    bool timing = false;
+    std::vector<PhaseEvents> ev;  // per iteration when timing
+    std::vector<long long> ev_iter;
+    int graph_batch = 0;
+    cudaGraphExec_t graph = nullptr;
+};
+
+namespace {
+
+void free_ctx(rbg_ctx *c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    for (auto &p : c->ev)
+        for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
+    if (c->nccl) nccl_destroy(c->nccl);
+    if (c->own_S) cudaFree(c->S);
+    cudaFree(c->w);
+    cudaFree(c->Q);
+    cudaFree(c->WQ);
+    cudaFree(c->R);
+    cudaFree(c->r2);
+    cudaFree(c->st);
+    cudaFree(c->errors);
+    cudaFree(c->rdiag);
+    cudaFree(c->piv);
+    cudaFree(c->nu);
+    cudaFree(c->recs);
+    cudaFree(c->ticket);
+    cudaFree(c->send);
+    cudaFree(c->recv);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+SweepArgs sweep_args(const rbg_ctx *c) {
+    SweepArgs a;
+    a.S = c->S;
+    a.ldv = c->ldv;
+    a.M = c->M;
+    a.N = c->N;
+    a.nvec = c->nvec;
+    a.w = c->w;
+    a.WQ = c->WQ;
+    a.ldq_v = c->ldq_v;
+    a.R = c->R;
+    a.r2 = c->r2;
+    a.st = c->st;
+    a.recs = c->recs;
+    a.ticket = c->ticket;
+    a.col_offset = c->col_offset;
+    a.send = c->world > 1 ? c->send : nullptr;
+    return a;
+}
+
+ImgsArgs imgs_args(const rbg_ctx *c) {
+    ImgsArgs a;
+    a.S = c->S;
+    a.ldv = c->ldv;
+    a.N = c->N;
+    a.nvec = c->nvec;
+    a.w = c->w;
+    a.Q = c->Q;
+    a.WQ = c->WQ;
+    a.ldq_v = c->ldq_v;
+    a.st = c->st;
+    a.errors = c->errors;
+    a.piv = c->piv;
+    a.nu = c->nu;
+    a.rdiag = c->rdiag;
+    a.r2 = c->r2;
+    a.k_max = c->k_max;
+    a.tol = c->tol;
+    a.col_offset = c->col_offset;
+    a.M_loc = c->M;
+    a.world = c->world;
+    a.recv = c->recv;
+    a.slot_bytes = c->slot;
+    return a;
+}
+
+rbg_status enqueue_local(rbg_ctx *c) {
+    const bool init = !c->started;
+    CU(launch_sweep(sweep_args(c), c->cplx, init, init ? c->cfg_init : c->cfg_sweep, c->stream));
+    c->started = true;
+    return RBG_OK;
+}
+
+rbg_status enqueue_xchg(rbg_ctx *c) {
+    if (c->world > 1 && c->comm == RBG_COMM_NCCL) {
+        const char *msg = nullptr;
+        if (nccl_allgather_bytes(c->send, c->recv, c->slot, c->nccl, c->stream, &msg))
+            return fail(RBG_ENCCL, "ncclAllGather: %s", msg ? msg : "?");
+    }
+    return RBG_OK;
+}
+
+rbg_status enqueue_finish(rbg_ctx *c) {
+    CU(launch_imgs(imgs_args(c), c->cplx, c->stream));
+    return RBG_OK;
+}
+
+rbg_status enqueue_iteration(rbg_ctx *c) {
+    PhaseEvents *pe = nullptr;
+    if (c->timing) {
+        PhaseEvents p;
+        for (int i = 0; i < 4; i++) CU(cudaEventCreate(&p.e[i]));
+        c->ev.push_back(p);
+        c->ev_iter.push_back(c->iters);
+        pe = &c->ev.back();
+        CU(cudaEventRecord(pe->e[0], c->stream));
+    }
+    TRY(enqueue_local(c));
+    if (pe) CU(cudaEventRecord(pe->e[1], c->stream));
+    TRY(enqueue_xchg(c));
+    if (pe) CU(cudaEventRecord(pe->e[2], c->stream));
+    TRY(enqueue_finish(c));
+    if (pe) CU(cudaEventRecord(pe->e[3], c->stream));
+    c->iters++;
+    return RBG_OK;
+}
+
+rbg_status build_graph(rbg_ctx *c) {
+    if (c->graph) return RBG_OK;
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rbg_status s = RBG_OK;
+    for (int i = 0; i < c->graph_batch && s == RBG_OK; i++) {
+        s = enqueue_local(c);
+        if (s == RBG_OK) s = enqueue_xchg(c);
+        if (s == RBG_OK) s = enqueue_finish(c);
+    }
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (s != RBG_OK) return s;
+    CU(e);
+    e = cudaGraphInstantiate(&c->graph, g, 0);
+    cudaGraphDestroy(g);
+    CU(e);
+    return RBG_OK;
+}
+
+rbg_status enqueue_n(rbg_ctx *c, long long n) {
+    while (n > 0) {
+        if (!c->started || c->timing || c->graph_batch <= 0 || n < c->graph_batch) {
+            TRY(enqueue_iteration(c));
+            n--;
+            continue;
+        }
+        TRY(build_graph(c));
+        CU(cudaGraphLaunch(c->graph, c->stream));
+        c->iters += c->graph_batch;
+        n -= c->graph_batch;
+    }
+    return RBG_OK;
+}
+
+rbg_status check_ctx(rbg_ctx *c) {
+    if (!c) return fail(RBG_EINVAL, "null context");
+    CU(cudaSetDevice(c->device));
+    return RBG_OK;
+}
+
+rbg_status read_state(rbg_ctx *c, DevState *h) {
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpy(h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void rbg_desc_init(rbg_desc *d) {
+    if (!d) return;
+    std::memset(d, 0, sizeof *d);
+    d->S_mem = RBG_MEM_HOST;
+    d->w_mem = RBG_MEM_HOST;
+    d->dtype = RBG_COMPLEX_F64;
+    d->device = -1;
+    d->check_finite = 1;
+    d->comm = RBG_COMM_NONE;
+    d->world = 1;
+}
+
+const char *rbg_last_error(void) { return g_err.c_str(); }
+
+void rbg_lanes(int *L_S, int *L_I) {
+    if (L_S) *L_S = kLaneSweep;
+    if (L_I) *L_I = kLaneImgs;
+}
+
+const char *rbg_version(void) { return "rbg 0.1 sm_100a L_S=32 L_I=2048 kappa=2 nu_max=5"; }
+
+rbg_status rbg_get_unique_id(uint8_t out[128]) {
+    if (!out) return fail(RBG_EINVAL, "null output");
+    const char *msg = nullptr;
+    if (nccl_get_unique_id(out, &msg)) return fail(RBG_ENCCL, "ncclGetUniqueId: %s", msg ? msg : "?");
+    return RBG_OK;
+}
+
+rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
+    if (!out || !d) return fail(RBG_EINVAL, "null ctx or desc");
+    *out = nullptr;
+    if (!d->S) return fail(RBG_EINVAL, "null S");
+    if (d->dtype != RBG_REAL_F64 && d->dtype != RBG_COMPLEX_F64) return fail(RBG_EINVAL, "unknown dtype %d", (int)d->dtype);
+    if (d->N < 1 || d->M < 1) return fail(RBG_EINVAL, "N=%lld M=%lld must be >= 1", (long long)d->N, (long long)d->M);
+    const long long ld = d->ld ? d->ld : d->N;
+    if (ld < d->N) return fail(RBG_EINVAL, "ld=%lld < N=%lld", ld, (long long)d->N);
+    if (!(d->tol >= 0.0) || std::isinf(d->tol)) return fail(RBG_EINVAL, "tol must be finite and >= 0");
+    const int world = d->world < 1 ? 1 : d->world;
+    if (d->rank < 0 || d->rank >= world) return fail(RBG_EINVAL, "rank %d outside [0, %d)", d->rank, world);
+    const long long Mg = d->M_global ? d->M_global : d->M;
+    if (world == 1 && (d->col_offset != 0 || Mg != d->M))
+        return fail(RBG_EINVAL, "one rank must own all columns");
+    if (d->col_offset < 0 || d->col_offset + d->M > Mg) return fail(RBG_EINVAL, "column range outside M_global");
+    if (d->k_max < 1 || d->k_max > std::min<long long>(d->N, Mg))
+        return fail(RBG_EINVAL, "k_max=%lld outside [1, min(N, M)=%lld]", (long long)d->k_max,
+                    std::min<long long>(d->N, Mg));
+    if (world > 1 && d->comm == RBG_COMM_NONE) return fail(RBG_EINVAL, "world > 1 needs comm NCCL or EXTERNAL");
+    const bool cplx = d->dtype == RBG_COMPLEX_F64;
+    const long long nvec = cplx ? d->N : (d->N + 1) / 2;
+    if (imgs_maxv(nvec) == 0) return fail(RBG_EINVAL, "N=%lld exceeds the IMGS register tile (max %d vectors)", (long long)d->N, 16 * kLaneImgs);
+
+    // weights: validate on the host
+    std::vector<double> wh(d->N, 1.0);
+    if (d->w) {
+        if (d->w_mem == RBG_MEM_DEVICE) {
+            cudaError_t e = cudaMemcpy(wh.data(), d->w, sizeof(double) * d->N, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return fail(RBG_ECUDA, "reading w: %s", cudaGetErrorString(e));
+        } else {
+            std::memcpy(wh.data(), d->w, sizeof(double) * d->N);
+        }
+        for (long long i = 0; i < d->N; i++)
+            if (!(wh[i] > 0.0) || std::isinf(wh[i])) return fail(RBG_EINVAL, "w[%lld]=%g must be positive and finite", i, wh[i]);
+    }
+    // host S: finiteness check in column-major order (first offending (row, col))
+    if (d->S_mem == RBG_MEM_HOST && d->check_finite) {
+        const double *Sh = static_cast<const double *>(d->S);
+        const long long per = cplx ? 2 : 1;
+        for (long long j = 0; j < d->M; j++)
+            for (long long i = 0; i < d->N; i++)
+                for (long long r = 0; r < per; r++)
+                    if (!std::isfinite(Sh[(j * ld + i) * per + r]))
+                        return fail(RBG_ENONFINITE, "non-finite S entry at (row %lld, col %lld)", i, j + d->col_offset);
+    }
+    if (d->S_mem == RBG_MEM_DEVICE && d->borrow) {
+        if (reinterpret_cast<uintptr_t>(d->S) % 16) return fail(RBG_EINVAL, "borrowed S must be 16-byte aligned");
+        if (!cplx && (ld % 2)) return fail(RBG_EINVAL, "borrowed real S needs an even ld");
+    }
+
+    rbg_ctx *c = new rbg_ctx();
+    auto bail = [&](rbg_status s) {
+        std::string keep = g_err;
+        free_ctx(c);
+        g_err = keep;
+        return s;
+    };
+#define CUB(call)                                                                                    \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return bail(fail(e_ == cudaErrorMemoryAllocation ? RBG_ENOMEM : RBG_ECUDA, "%s: %s", #call, \
+                             cudaGetErrorString(e_)));                                               \
+    } while (0)
+
+    if (d->device >= 0) c->device = d->device;
+    else CUB(cudaGetDevice(&c->device));
+    CUB(cudaSetDevice(c->device));
+    CUB(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (d->stream) c->stream = static_cast<cudaStream_t>(d->stream);
+    else {
+        CUB(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    c->cplx = cplx;
+    c->se = cplx ? 16 : 8;
+    c->N = d->N;
+    c->M = d->M;
+    c->nvec = nvec;
+    c->ldq_v = nvec;
+    c->tol = d->tol;
+    c->k_max = d->k_max;
+    c->comm = d->comm;
+    c->rank = d->rank;
+    c->world = world;
+    c->col_offset = d->col_offset;
+    c->M_global = Mg;
+
+    // snapshot matrix
+    const size_t col_bytes = (size_t)d->N * c->se;
+    if (d->S_mem == RBG_MEM_DEVICE && d->borrow) {
+        c->S = const_cast<double2 *>(static_cast<const double2 *>(d->S));
+        c->ldv = cplx ? ld : ld / 2;
+    } else {
+        c->ldv = nvec;
+        const size_t dst_pitch = (size_t)nvec * 16;
+        CUB(cudaMalloc(&c->S, dst_pitch * d->M));
+        c->own_S = true;
+        if (dst_pitch != col_bytes) CUB(cudaMemsetAsync(c->S, 0, dst_pitch * d->M, c->stream));
+        const cudaMemcpyKind kind = d->S_mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        if (dst_pitch == col_bytes && (size_t)ld * c->se == col_bytes)
+            CUB(cudaMemcpyAsync(c->S, d->S, col_bytes * d->M, kind, c->stream));
+        else
+            CUB(cudaMemcpy2DAsync(c->S, dst_pitch, d->S, (size_t)ld * c->se, col_bytes, d->M, kind, c->stream));
+    }
+    if (d->S_mem == RBG_MEM_DEVICE && d->check_finite) {
+        unsigned long long *bad = nullptr, hbad = ~0ull;
+        CUB(cudaMalloc(&bad, sizeof *bad));
+        CUB(cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream));
+        CUB(launch_check_finite(c->S, c->ldv, c->M, c->N, nvec, cplx, bad, c->stream));
+        CUB(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, c->stream));
+        CUB(cudaStreamSynchronize(c->stream));
+        cudaFree(bad);
+        if (hbad != ~0ull)
+            return bail(fail(RBG_ENONFINITE, "non-finite S entry at (row %lld, col %lld)", (long long)(hbad % d->N),
+                             (long long)(hbad / d->N) + d->col_offset));
+    }
+
+    // weights (zero padded), basis, coefficients, state
+    std::vector<double> wpad(2 * nvec + 2, 0.0);
+    std::memcpy(wpad.data(), wh.data(), sizeof(double) * d->N);
+    CUB(cudaMalloc(&c->w, sizeof(double) * wpad.size()));
+    CUB(cudaMemcpyAsync(c->w, wpad.data(), sizeof(double) * wpad.size(), cudaMemcpyHostToDevice, c->stream));
+    const size_t qbytes = (size_t)c->k_max * nvec * 16;
+    CUB(cudaMalloc(&c->Q, qbytes));
+    CUB(cudaMalloc(&c->WQ, qbytes));
+    CUB(cudaMemsetAsync(c->Q, 0, qbytes, c->stream));
+    CUB(cudaMemsetAsync(c->WQ, 0, qbytes, c->stream));
+    CUB(cudaMalloc(&c->R, (size_t)c->k_max * c->M * c->se));
+    CUB(cudaMemsetAsync(c->R, 0, (size_t)c->k_max * c->M * c->se, c->stream));
+    CUB(cudaMalloc(&c->r2, sizeof(double) * c->M));
+    CUB(cudaMalloc(&c->st, sizeof(DevState)));
+    CUB(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
+    CUB(cudaMalloc(&c->errors, sizeof(double) * (c->k_max + 1)));
+    CUB(cudaMemsetAsync(c->errors, 0, sizeof(double) * (c->k_max + 1), c->stream));
+    CUB(cudaMalloc(&c->rdiag, sizeof(double) * c->k_max));
+    CUB(cudaMalloc(&c->piv, sizeof(long long) * c->k_max));
+    CUB(cudaMalloc(&c->nu, sizeof(int) * c->k_max));
+    CUB(cudaMemsetAsync(c->nu, 0, sizeof(int) * c->k_max, c->stream));
+    c->cfg_init = sweep_config(cplx, true, nvec, c->num_sms, c->device);
+    c->cfg_sweep = sweep_config(cplx, false, nvec, c->num_sms, c->device);
+    const int max_grid = std::max(c->cfg_init.grid, c->cfg_sweep.grid);
+    CUB(cudaMalloc(&c->recs, sizeof(Rec) * max_grid));
+    CUB(cudaMalloc(&c->ticket, sizeof(unsigned)));
+    CUB(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
+
+    if (world > 1) {
+        c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;
+        CUB(cudaMalloc(&c->send, c->slot));
+        CUB(cudaMalloc(&c->recv, c->slot * world));
+        CUB(cudaMemsetAsync(c->send, 0, c->slot, c->stream));
+        CUB(cudaMemsetAsync(c->recv, 0, c->slot * world, c->stream));
+        if (d->comm == RBG_COMM_NCCL) {
+            const char *msg = nullptr;
+            if (nccl_init(&c->nccl, world, d->rank, d->nccl_id, &msg))
+                return bail(fail(RBG_ENCCL, "ncclCommInitRank: %s", msg ? msg : "?"));
+        }
+    }
+    CUB(cudaStreamSynchronize(c->stream));
+#undef CUB
+    *out = c;
+    return RBG_OK;
+}
+
+rbg_status rbg_create(rbg_ctx **ctx, const void *S, int64_t N, int64_t M, const double *w, double tol,
+                      int64_t k_max, rbg_dtype dtype) {
+    rbg_desc d;
+    rbg_desc_init(&d);
+    d.S = S;
+    d.N = N;
+    d.M = M;
+    d.w = w;
+    d.tol = tol;
+    d.k_max = k_max;
+    d.dtype = dtype;
+    return rbg_create_ex(ctx, &d);
+}
+
+rbg_status rbg_step(rbg_ctx *c, int64_t n) {
+    TRY(check_ctx(c));
+    if (c->comm == RBG_COMM_EXTERNAL) return fail(RBG_ESTATE, "EXTERNAL contexts use rbg_iter_local/finish");
+    if (n < 0) return fail(RBG_EINVAL, "n < 0");
+    return enqueue_n(c, n);
+}
+
+rbg_status rbg_run(rbg_ctx *c) {
+    TRY(check_ctx(c));
+    if (c->comm == RBG_COMM_EXTERNAL) return fail(RBG_ESTATE, "EXTERNAL contexts use rbg_iter_local/finish");
+    const long long need = c->k_max + 1 - c->iters;
+    if (need > 0) TRY(enqueue_n(c, need));
+    CU(cudaStreamSynchronize(c->stream));
+    return RBG_OK;
+}
+
+rbg_status rbg_set_timing(rbg_ctx *c, int on) {
+    TRY(check_ctx(c));
+    c->timing = on != 0;
+    return RBG_OK;
+}
+
+rbg_status rbg_set_graph_batch(rbg_ctx *c, int batch) {
+    TRY(check_ctx(c));
+    if (batch < 0) return fail(RBG_EINVAL, "batch < 0");
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    c->graph_batch = batch;
+    return RBG_OK;
+}
+
+rbg_status rbg_sync(rbg_ctx *c) {
+    TRY(check_ctx(c));
+    CU(cudaStreamSynchronize(c->stream));
+    return RBG_OK;
+}
+
+rbg_status rbg_result_info(rbg_ctx *c, int64_t *k, int64_t *M_loc, rbg_stop *why) {
+    TRY(check_ctx(c));
+    DevState h;
+    TRY(read_state(c, &h));
+    if (k) *k = h.k;
+    if (M_loc) *M_loc = c->M;
+    if (why) *why = (rbg_stop)h.stop;
+    return RBG_OK;
+}
+
+rbg_status rbg_get_pivots(rbg_ctx *c, int64_t *out) {
+    TRY(check_ctx(c));
+    if (!out) return fail(RBG_EINVAL, "null output");
+    DevState h;
+    TRY(read_state(c, &h));
+    if (h.k) CU(cudaMemcpy(out, c->piv, sizeof(long long) * h.k, cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_errors(rbg_ctx *c, double *out) {
+    TRY(check_ctx(c));
+    if (!out) return fail(RBG_EINVAL, "null output");
+    DevState h;
+    TRY(read_state(c, &h));
+    const long long n = h.stop ? h.k + 1 : h.k;
+    if (n) CU(cudaMemcpy(out, c->errors, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_nu(rbg_ctx *c, int32_t *out) {
+    TRY(check_ctx(c));
+    if (!out) return fail(RBG_EINVAL, "null output");
+    DevState h;
+    TRY(read_state(c, &h));
+    if (h.k) CU(cudaMemcpy(out, c->nu, sizeof(int) * h.k, cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_rdiag(rbg_ctx *c, double *out) {
+    TRY(check_ctx(c));
+    if (!out) return fail(RBG_EINVAL, "null output");
+    DevState h;
+    TRY(read_state(c, &h));
+    if (h.k) CU(cudaMemcpy(out, c->rdiag, sizeof(double) * h.k, cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_basis(rbg_ctx *c, void *out, int64_t ldq, int on_device) {
+    TRY(check_ctx(c));
+    if (!out || ldq < c->N) return fail(RBG_EINVAL, "null output or ldq < N");
+    DevState h;
+    TRY(read_state(c, &h));
+    if (h.k)
+        CU(cudaMemcpy2D(out, (size_t)ldq * c->se, c->Q, (size_t)c->ldq_v * 16, (size_t)c->N * c->se, h.k,
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_R(rbg_ctx *c, void *out, int64_t ldr, int on_device) {
+    TRY(check_ctx(c));
+    if (!out || ldr < c->M) return fail(RBG_EINVAL, "null output or ldr < M_loc");
+    DevState h;
+    TRY(read_state(c, &h));
+    if (h.k)
+        CU(cudaMemcpy2D(out, (size_t)ldr * c->se, c->R, (size_t)c->M * c->se, (size_t)c->M * c->se, h.k,
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_r2(rbg_ctx *c, double *out, int on_device) {
+    TRY(check_ctx(c));
+    if (!out) return fail(RBG_EINVAL, "null output");
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpy(out, c->r2, sizeof(double) * c->M, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+rbg_status rbg_get_timings(rbg_ctx *c, double *sweep_ms, double *xchg_ms, double *imgs_ms, int64_t n) {
+    TRY(check_ctx(c));
+    CU(cudaStreamSynchronize(c->stream));
+    // sweep i uses q_i: the local step of iteration i+1; xchg/imgs i: iteration i
+    for (int64_t i = 0; i < n; i++) {
+        float ms;
+        if (sweep_ms) {
+            sweep_ms[i] = NAN;
+            if ((size_t)(i + 1) < c->ev.size() && c->ev_iter[i + 1] == i + 1) {
+                CU(cudaEventElapsedTime(&ms, c->ev[i + 1].e[0], c->ev[i + 1].e[1]));
+                sweep_ms[i] = ms;
+            }
+        }
+        if ((size_t)i < c->ev.size() && c->ev_iter[i] == i) {
+            if (xchg_ms) {
+                CU(cudaEventElapsedTime(&ms, c->ev[i].e[1], c->ev[i].e[2]));
+                xchg_ms[i] = ms;
+            }
+            if (imgs_ms) {
+                CU(cudaEventElapsedTime(&ms, c->ev[i].e[2], c->ev[i].e[3]));
+                imgs_ms[i] = ms;
+            }
+        } else {
+            if (xchg_ms) xchg_ms[i] = NAN;
+            if (imgs_ms) imgs_ms[i] = NAN;
+        }
+    }
+    return RBG_OK;
+}
+
+rbg_status rbg_get_stats(rbg_ctx *c, rbg_stats *o) {
+    TRY(check_ctx(c));
+    if (!o) return fail(RBG_EINVAL, "null output");
+    DevState h;
+    TRY(read_state(c, &h));
+    std::memset(o, 0, sizeof *o);
+    o->k = h.k;
+    // iterations with events, restricted to those that did work: 0..k
+    const long long last = std::min<long long>(h.k, (long long)c->ev.size() - 1);
+    float ms;
+    bool first = true;
+    cudaEvent_t e_first = nullptr, e_last = nullptr;
+    for (long long t = 0; t <= last; t++) {
+        if (c->ev_iter[t] != t) continue;
+        const PhaseEvents &p = c->ev[t];
+        CU(cudaEventElapsedTime(&ms, p.e[0], p.e[1]));
+        if (t == 0) o->t_init_ms = ms;
+        else {
+            o->t_sweep_ms += ms;
+            o->sweeps++;
+        }
+        CU(cudaEventElapsedTime(&ms, p.e[1], p.e[2]));
+        o->t_xchg_ms += ms;
+        CU(cudaEventElapsedTime(&ms, p.e[2], p.e[3]));
+        o->t_imgs_ms += ms;
+        if (first) {
+            e_first = p.e[0];
+            first = false;
+        }
+        e_last = p.e[3];
+    }
+    if (e_first && e_last) {
+        CU(cudaEventElapsedTime(&ms, e_first, e_last));
+        o->t_total_ms = ms;
+    }
+    return RBG_OK;
+}
+
+rbg_status rbg_iter_local(rbg_ctx *c) {
+    TRY(check_ctx(c));
+    if (c->comm != RBG_COMM_EXTERNAL || c->local_pending) return fail(RBG_ESTATE, "iter_local out of order");
+    TRY(enqueue_local(c));
+    c->local_pending = true;
+    return RBG_OK;
+}
+
+rbg_status rbg_iter_finish(rbg_ctx *c) {
+    TRY(check_ctx(c));
+    if (c->comm != RBG_COMM_EXTERNAL || !c->local_pending) return fail(RBG_ESTATE, "iter_finish out of order");
+    TRY(enqueue_finish(c));
+    c->local_pending = false;
+    c->iters++;
+    return RBG_OK;
+}
+
+rbg_status rbg_xchg_buffers(rbg_ctx *c, void **send, void **recv, size_t *bytes) {
+    TRY(check_ctx(c));
+    if (send) *send = c->send;
+    if (recv) *recv = c->recv;
+    if (bytes) *bytes = c->slot;
+    return RBG_OK;
+}
+
+rbg_status rbg_emulate_allgather(rbg_ctx **ctxs, int world) {
+    if (!ctxs || world < 1) return fail(RBG_EINVAL, "bad context list");
+    for (int p = 0; p < world; p++) {
+        if (!ctxs[p] || ctxs[p]->world != world || ctxs[p]->rank != p || !ctxs[p]->send)
+            return fail(RBG_EINVAL, "context %d is not rank %d of a %d-rank EXTERNAL group", p, p, world);
+        CU(cudaSetDevice(ctxs[p]->device));
+        CU(cudaStreamSynchronize(ctxs[p]->stream));
+    }
+    for (int p = 0; p < world; p++)
+        for (int r = 0; r < world; r++)
+            CU(cudaMemcpy(ctxs[p]->recv + (size_t)r * ctxs[p]->slot, ctxs[r]->send, ctxs[r]->slot,
+                          cudaMemcpyDeviceToDevice));
+    return RBG_OK;
+}
+
+void rbg_destroy(rbg_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    free_ctx(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// common.cuh -- device-side types and PTX helpers shared by the rbg kernels (sm_100a).
+//
+// Arithmetic rule for every kernel in this directory: the canonical arithmetic contract
+// of DESIGN.md.  The library is compiled with --fmad=false, so a*b+c is never fused
+// behind our back; every fused multiply-add is an explicit fma().
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rbg {
+
+constexpr int kLaneSweep = 32;      // L_S: one warp per column
+constexpr int kImgsCtas = 8;        // cluster size of the IMGS kernel
+constexpr int kImgsThreads = 256;   // threads per IMGS CTA
+constexpr int kLaneImgs = kImgsCtas * kImgsThreads;  // L_I = 2048
+constexpr int kNuMax = 5;           // IMGS sweep cap (R7)
+
+constexpr int kStopNone = 0, kStopTol = 1, kStopKmax = 2, kStopRank = 3, kStopAll = 4;
+
+// One maxloc record: 16 bytes, total order (m descending, j ascending).
+struct __align__(16) Rec {
+    double m;
+    long long j;
+};
+
+__device__ __forceinline__ bool rec_better(double m1, long long j1, double m2, long long j2) {
+    return (m1 > m2) || (m1 == m2 && j1 < j2);
+}
+
+// Device-resident loop state (one per context).
+struct DevState {
+    long long k;        // basis vectors built so far
+    int stop;           // rbg_stop
+    int pad;
+    double m_loc;       // local maxloc after the last sweep
+    long long j_loc;    // its GLOBAL column index
+};
+
+// Layout of one rank's slot in the exchange buffer: Rec header then the candidate column
+// (N_pad elements), padded to 16 bytes.
+__host__ __device__ inline size_t xchg_slot_bytes(long long nvec) {
+    return sizeof(Rec) + (size_t)nvec * 16;
+}
+
+// ----------------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// TMA bulk copy global -> shared (non-tensor), completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// L2 evict-first policy for the streamed snapshot matrix (read exactly once per sweep).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// 16-byte streaming load: non-coherent path, no L1 allocation, L2 evict-first.
+__device__ __forceinline__ double2 ld_stream(const double2 *p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
+// Map a local shared address to the same offset in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t map_dsmem(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void st_dsmem_v2(uint32_t addr, double a, double b) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+
+}  // namespace rbg

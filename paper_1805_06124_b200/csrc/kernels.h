@@ -1,0 +1,68 @@
+// kernels.h -- host-visible launch interface of the rbg device kernels (internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace rbg {
+
+// Fused column sweep (a0 init norms / a2 coefficient sweep + residual update + maxloc).
+struct SweepArgs {
+    const double2 *S;      // snapshot block as 16-byte vectors, column j at S + j*ldv
+    long long ldv;         // column stride in vectors
+    long long M;           // local columns
+    long long N;           // rows (elements)
+    long long nvec;        // vectors per column: complex N, real ceil(N/2)
+    const double *w;       // weights, zero padded to a multiple of 2 (+2)
+    const double2 *WQ;     // weighted basis, column i at WQ + i*ldq_v
+    long long ldq_v;
+    double *R;             // k_max x M row-major, element = 16 B complex / 8 B real
+    double *r2;            // M
+    DevState *st;
+    Rec *recs;             // one record per CTA
+    unsigned *ticket;      // last-CTA-done counter (returns to 0)
+    long long col_offset;  // global index of local column 0
+    unsigned char *send;   // exchange slot of this rank (NULL on one GPU)
+};
+
+// Pivot decision + iterated MGS (a3 finalize, a5, a6).
+struct ImgsArgs {
+    const double2 *S;
+    long long ldv;
+    long long N, nvec;
+    const double *w;
+    double2 *Q, *WQ;
+    long long ldq_v;
+    DevState *st;
+    double *errors;        // k_max + 1
+    long long *piv;        // k_max
+    int *nu;               // k_max
+    double *rdiag;         // k_max
+    double *r2;            // M_loc
+    long long k_max;
+    double tol;
+    long long col_offset, M_loc;
+    int world;
+    const unsigned char *recv;  // world slots of xchg_slot_bytes(nvec)
+    size_t slot_bytes;
+};
+
+struct SweepConfig {
+    int grid, threads;
+    size_t smem;
+    bool esmem;  // basis vector staged in shared memory (else read through L1/L2)
+};
+
+SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int device);
+cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepConfig &cfg,
+                         cudaStream_t s);
+int imgs_maxv(long long nvec);  // 0 if unsupported
+cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s);
+// First non-finite entry of a device block: writes min(col * N + row) (or -1) to *out.
+cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
+                                long long nvec, bool cplx, unsigned long long *out,
+                                cudaStream_t s);
+
+}  // namespace rbg

@@ -1,0 +1,310 @@
+// sweep.cu -- the fused column sweep: the pivot-search half of each RB-greedy iteration.
+//
+// PAPER.md:838-868 (Sec. 6.1.2): every iteration computes, for all M columns, the
+// coefficient c_kj = <q_k, s_j> and the residual recurrence of Eq. (Residual)
+//     sigma_hat_k^2(s_j) = ||s_j||^2 - sum_{i<=k} |c_ij|^2,
+// then the argmax over j.  "The j-th pivot search has a constant complexity with an
+// asymptotic FLOP count of O(2MN)" -- it streams all of S once and is HBM-bound.
+//
+// B200 design:
+//  * one CTA per SM (persistent over a contiguous block of columns), 16 warps;
+//  * the weighted basis vector e~_k = w o q_k (N x 16 B, 160 KB at N = 10,000 complex) is
+//    staged once per CTA into shared memory with TMA bulk copies (cp.async.bulk) on an
+//    mbarrier;
+//  * one warp per column (L_S = 32 lanes): lane l owns the 16-byte vectors u = l (mod 32)
+//    of the column, streamed with 16-byte ld.global.nc.L1::no_allocate + L2 evict-first,
+//    double-buffered in registers, accumulated with explicit fma() in increasing u;
+//  * xor-butterfly with ascending offsets (= the pairwise lane tree of the CAC);
+//  * lane 0 writes R(k, j), updates r2_j in place, and the warp keeps its maxloc;
+//  * per-CTA maxloc records, the last CTA to finish (atomic ticket) reduces them with the
+//    total order (value desc, index asc) into the device state, and on a sharded run packs
+//    the local candidate column into the exchange slot.
+// Sweep 0 (INIT) is the same kernel with e~ = w and the weighted norm of CAC rule 4.
+#include <cmath>
+
+#include "kernels.h"
+
+namespace rbg {
+
+constexpr int kSweepThreads = 512;
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr int kUnroll = 4;
+constexpr size_t kSmemLimit = 220 * 1024;
+constexpr uint32_t kBulkChunk = 32 * 1024;
+
+// Accumulate one 16-byte vector x of a column against the staged vector e (CAC rules 2, 4).
+template <bool CPLX, bool INIT>
+__device__ __forceinline__ void accum(double &re, double &im, const double2 x, const double2 e) {
+    if (INIT) {
+        // e = (w_{2u}, w_{2u+1}) for real, (w_u, -) for complex
+        if (CPLX) {
+            double t = e.x * x.x;
+            re = fma(t, x.x, re);
+            t = e.x * x.y;
+            re = fma(t, x.y, re);
+        } else {
+            double t = e.x * x.x;
+            re = fma(t, x.x, re);
+            t = e.y * x.y;
+            re = fma(t, x.y, re);
+        }
+    } else {
+        if (CPLX) {
+            re = fma(e.x, x.x, re);
+            re = fma(e.y, x.y, re);
+            im = fma(e.x, x.y, im);
+            im = fma(-e.y, x.x, im);
+        } else {
+            re = fma(e.x, x.x, re);
+            re = fma(e.y, x.y, re);
+        }
+    }
+}
+
+template <bool CPLX, bool INIT, bool ESMEM>
+__device__ __forceinline__ double2 load_e(const double2 *E, const double *Ew, long long u) {
+    if (INIT && CPLX) {
+        // complex sweep 0 reads one weight per vector
+        double wv = ESMEM ? Ew[u] : __ldg(Ew + u);
+        return make_double2(wv, 0.0);
+    }
+    return ESMEM ? E[u] : __ldg(E + u);
+}
+
+template <bool CPLX, bool INIT, bool ESMEM>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ double s_m[kSweepWarps];
+    __shared__ long long s_j[kSweepWarps];
+    __shared__ int s_last;
+
+    const int stop = a.st->stop;
+    if (stop) return;
+    const long long k = a.st->k;  // sweep uses q_{k-1} (k >= 1) unless INIT
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long nvec = a.nvec;
+    const bool odd_tail = !CPLX && (a.N & 1);
+
+    // ---- stage e~ (w o q_{k-1}, or w for sweep 0) ------------------------------------
+    const double2 *Eg = INIT ? reinterpret_cast<const double2 *>(a.w) : a.WQ + (k - 1) * a.ldq_v;
+    const double2 *E = Eg;
+    const double *Ew = a.w;
+    if (ESMEM) {
+        const size_t bytes = (INIT && CPLX) ? ((size_t)nvec * 8 + 15) / 16 * 16 : (size_t)nvec * 16;
+        if (tid == 0) {
+            mbar_init(&mbar, 1);
+            mbar_arrive_expect_tx(&mbar, (uint32_t)bytes);
+            const unsigned char *src = reinterpret_cast<const unsigned char *>(Eg);
+            for (size_t off = 0; off < bytes; off += kBulkChunk) {
+                uint32_t n = (uint32_t)((bytes - off) < kBulkChunk ? (bytes - off) : kBulkChunk);
+                bulk_g2s(smem + off, src + off, n, &mbar);
+            }
+        }
+        __syncthreads();
+        E = reinterpret_cast<const double2 *>(smem);
+        Ew = reinterpret_cast<const double *>(smem);
+    }
+
+    // ---- columns of this CTA ------------------------------------------------------
+    const long long c_begin = (long long)blockIdx.x * a.M / gridDim.x;
+    const long long c_end = (long long)(blockIdx.x + 1) * a.M / gridDim.x;
+    const uint64_t pol = policy_evict_first();
+
+    double best_m = -INFINITY;
+    long long best_j = 0x7fffffffffffffffLL;
+    bool waited = !ESMEM;
+
+    for (long long c = c_begin + warp; c < c_end; c += kSweepWarps) {
+        const double2 *col = a.S + c * a.ldv;
+        double re = 0.0, im = 0.0;
+        double2 xa[kUnroll];
+#pragma unroll
+        for (int t = 0; t < kUnroll; t++) {
+            const long long u = (long long)t * 32 + lane;
+            xa[t] = (u < nvec) ? ld_stream(col + u, pol) : make_double2(0.0, 0.0);
+        }
+        if (!waited) {  // first column: loads are in flight, now wait for e~
+            mbar_wait(&mbar, 0);
+            waited = true;
+        }
+        for (long long base = 0; base < nvec; base += 32 * kUnroll) {
+            double2 xb[kUnroll];
+#pragma unroll
+            for (int t = 0; t < kUnroll; t++) {
+                const long long u = base + 32 * kUnroll + (long long)t * 32 + lane;
+                xb[t] = (u < nvec) ? ld_stream(col + u, pol) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int t = 0; t < kUnroll; t++) {
+                const long long u = base + (long long)t * 32 + lane;
+                if (u < nvec) {
+                    double2 x = xa[t];
+                    if (odd_tail && u == nvec - 1) x.y = 0.0;  // row N is padding
+                    accum<CPLX, INIT>(re, im, x, load_e<CPLX, INIT, ESMEM>(E, Ew, u));
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kUnroll; t++) xa[t] = xb[t];
+        }
+        // lane tree, ascending offsets (CAC rule 3)
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1) {
+            re = re + __shfl_xor_sync(0xffffffffu, re, h);
+            if (CPLX && !INIT) im = im + __shfl_xor_sync(0xffffffffu, im, h);
+        }
+        double r2n;
+        if (INIT) {
+            r2n = re;
+            if (lane == 0) a.r2[c] = r2n;
+        } else {
+            const double cc = CPLX ? fma(re, re, im * im) : re * re;  // CAC rule 5
+            const double old = a.r2[c];
+            r2n = old - cc;                                            // CAC rule 6
+            if (lane == 0) {
+                if (CPLX) {
+                    reinterpret_cast<double2 *>(a.R)[(k - 1) * a.M + c] = make_double2(re, im);
+                } else {
+                    a.R[(k - 1) * a.M + c] = re;
+                }
+                a.r2[c] = r2n;
+            }
+        }
+        if (r2n > best_m) {  // columns visited in increasing order: first max wins
+            best_m = r2n;
+            best_j = c;
+        }
+    }
+    if (!waited) mbar_wait(&mbar, 0);  // never leave with a bulk copy in flight
+
+    // ---- CTA maxloc, then last-CTA-done global maxloc ---------------------------------
+    if (lane == 0) {
+        s_m[warp] = best_m;
+        s_j[warp] = best_j;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double bm = s_m[0];
+        long long bj = s_j[0];
+        for (int w = 1; w < kSweepWarps; w++)
+            if (rec_better(s_m[w], s_j[w], bm, bj)) {
+                bm = s_m[w];
+                bj = s_j[w];
+            }
+        a.recs[blockIdx.x].m = bm;
+        a.recs[blockIdx.x].j = bj;
+        __threadfence();
+        const unsigned t = atomicAdd(a.ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp == 0) {
+        double bm = -INFINITY;
+        long long bj = 0x7fffffffffffffffLL;
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+            const double m = __ldcg(&a.recs[b].m);
+            const long long j = __ldcg(&a.recs[b].j);
+            if (rec_better(m, j, bm, bj)) {
+                bm = m;
+                bj = j;
+            }
+        }
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {  // exact: total order, any combine order
+            const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+            const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+            if (rec_better(om, oj, bm, bj)) {
+                bm = om;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            const long long jg = (bj == 0x7fffffffffffffffLL) ? bj : bj + a.col_offset;
+            a.st->m_loc = bm;
+            a.st->j_loc = jg;
+            *a.ticket = 0u;
+            if (a.send) {
+                Rec *h = reinterpret_cast<Rec *>(a.send);
+                h->m = bm;
+                h->j = jg;
+            }
+        }
+        if (a.send) s_j[0] = bj;
+    }
+    if (a.send) {  // pack the local candidate column for the all-gather
+        __syncthreads();
+        const long long bj = s_j[0];
+        double2 *dst = reinterpret_cast<double2 *>(a.send + sizeof(Rec));
+        const bool valid = bj >= 0 && bj < a.M;
+        for (long long u = tid; u < nvec; u += kSweepThreads) {
+            double2 x = valid ? a.S[bj * a.ldv + u] : make_double2(0.0, 0.0);
+            if (odd_tail && u == nvec - 1) x.y = 0.0;
+            dst[u] = x;
+        }
+    }
+}
+
+SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int device) {
+    SweepConfig c;
+    c.threads = kSweepThreads;
+    const size_t ebytes = (init && cplx) ? ((size_t)nvec * 8 + 15) / 16 * 16 : (size_t)nvec * 16;
+    c.esmem = ebytes <= kSmemLimit;
+    c.smem = c.esmem ? ebytes : 0;
+    int per_sm = 1;
+    // more CTAs per SM only when the staged vector is small enough
+    if (c.smem * 2 + 4096 <= 227 * 1024) per_sm = 2;
+    (void)device;
+    c.grid = num_sms * per_sm;
+    return c;
+}
+
+template <bool CPLX, bool INIT, bool ESMEM>
+static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStream_t s) {
+    auto kern = k_sweep<CPLX, INIT, ESMEM>;
+    if (cfg.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)cfg.smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepConfig &cfg,
+                         cudaStream_t s) {
+    if (cplx) {
+        if (init) return cfg.esmem ? launch_t<true, true, true>(a, cfg, s) : launch_t<true, true, false>(a, cfg, s);
+        return cfg.esmem ? launch_t<true, false, true>(a, cfg, s) : launch_t<true, false, false>(a, cfg, s);
+    }
+    if (init) return cfg.esmem ? launch_t<false, true, true>(a, cfg, s) : launch_t<false, true, false>(a, cfg, s);
+    return cfg.esmem ? launch_t<false, false, true>(a, cfg, s) : launch_t<false, false, false>(a, cfg, s);
+}
+
+// ------------------------------------------------------------------ finiteness scan
+__global__ void k_check_finite(const double2 *S, long long ldv, long long M, long long N,
+                               long long nvec, bool cplx, unsigned long long *out) {
+    const long long total = M * nvec;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long c = t / nvec, u = t - c * nvec;
+        const double2 x = S[c * ldv + u];
+        long long row0 = cplx ? u : 2 * u;
+        bool bad0 = !isfinite(x.x), bad1 = !isfinite(x.y);
+        if (!cplx && row0 + 1 >= N) bad1 = false;  // padding row
+        if (bad0 || bad1) {
+            const long long row = cplx ? u : (bad0 ? row0 : row0 + 1);
+            atomicMin(out, (unsigned long long)(c * N + row));
+        }
+    }
+}
+
+cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
+                                long long nvec, bool cplx, unsigned long long *out,
+                                cudaStream_t s) {
+    k_check_finite<<<148 * 8, 256, 0, s>>>(S, ldv, M, N, nvec, cplx, out);
+    return cudaGetLastError();
+}
+
+}  // namespace rbg

@@ -1,0 +1,363 @@
+"""Python binding of librbg.so (include/rbg.h): argument marshalling only.
+
+Every step of the RB-greedy hot path runs in the library's CUDA kernels; this module only
+turns numpy arrays / torch tensors into pointers and back.  There is no CPU fallback:
+if the extension is missing or no GPU is present, calls raise.
+
+    res = greedy(S, w, tol, k_max)      # S: (M, N) host numpy or cuda torch tensor
+
+``S`` is given as (M, N) C-order (snapshot j = S[j]), which is the column-major N x M
+matrix of the paper.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "librbg.so")
+
+OK, EINVAL, ENONFINITE, ENOMEM, ECUDA, ENCCL, ESTATE = range(7)
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENONFINITE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
+STOP = {0: "NONE", 1: "TOL", 2: "KMAX", 3: "RANK", 4: "ALL_SELECTED"}
+REAL_F64, COMPLEX_F64 = 1, 2
+MEM_HOST, MEM_DEVICE = 0, 1
+COMM_NONE, COMM_NCCL, COMM_EXTERNAL = 0, 1, 2
+
+
+class RbgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [
+        ("S", ctypes.c_void_p), ("S_mem", ctypes.c_int), ("N", ctypes.c_int64),
+        ("M", ctypes.c_int64), ("ld", ctypes.c_int64), ("borrow", ctypes.c_int),
+        ("w", ctypes.c_void_p), ("w_mem", ctypes.c_int), ("dtype", ctypes.c_int),
+        ("tol", ctypes.c_double), ("k_max", ctypes.c_int64), ("stream", ctypes.c_void_p),
+        ("device", ctypes.c_int), ("check_finite", ctypes.c_int), ("comm", ctypes.c_int),
+        ("rank", ctypes.c_int), ("world", ctypes.c_int), ("col_offset", ctypes.c_int64),
+        ("M_global", ctypes.c_int64), ("nccl_id", ctypes.c_uint8 * 128),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int64), ("sweeps", ctypes.c_int64), ("t_init_ms", ctypes.c_double),
+                ("t_sweep_ms", ctypes.c_double), ("t_xchg_ms", ctypes.c_double),
+                ("t_imgs_ms", ctypes.c_double), ("t_total_ms", ctypes.c_double)]
+
+
+# (name, argtypes, restype) for every symbol include/rbg.h and include/rbg_gen.h declare
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+SYMBOLS = {
+    "rbg_desc_init": ([ctypes.POINTER(Desc)], None),
+    "rbg_create": ([ctypes.POINTER(_P), _P, _I64, _I64, _P, ctypes.c_double, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_create_ex": ([ctypes.POINTER(_P), ctypes.POINTER(Desc)], ctypes.c_int),
+    "rbg_get_unique_id": ([ctypes.POINTER(ctypes.c_uint8)], ctypes.c_int),
+    "rbg_run": ([_P], ctypes.c_int),
+    "rbg_step": ([_P, _I64], ctypes.c_int),
+    "rbg_set_timing": ([_P, ctypes.c_int], ctypes.c_int),
+    "rbg_set_graph_batch": ([_P, ctypes.c_int], ctypes.c_int),
+    "rbg_sync": ([_P], ctypes.c_int),
+    "rbg_result_info": ([_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "rbg_get_pivots": ([_P, _P], ctypes.c_int),
+    "rbg_get_errors": ([_P, _P], ctypes.c_int),
+    "rbg_get_nu": ([_P, _P], ctypes.c_int),
+    "rbg_get_rdiag": ([_P, _P], ctypes.c_int),
+    "rbg_get_basis": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_get_R": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_get_r2": ([_P, _P, ctypes.c_int], ctypes.c_int),
+    "rbg_get_stats": ([_P, ctypes.POINTER(Stats)], ctypes.c_int),
+    "rbg_get_timings": ([_P, _P, _P, _P, _I64], ctypes.c_int),
+    "rbg_iter_local": ([_P], ctypes.c_int),
+    "rbg_iter_finish": ([_P], ctypes.c_int),
+    "rbg_xchg_buffers": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "rbg_emulate_allgather": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
+    "rbg_lanes": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], None),
+    "rbg_version": ([], ctypes.c_char_p),
+    "rbg_last_error": ([], ctypes.c_char_p),
+    "rbg_destroy": ([_P], None),
+    "rbg_gen_chirp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
+}
+
+_lib = None
+
+
+def lib():
+    """Load librbg.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1805_06124_b200.build` "
+                              "or __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        for name, (argt, rest) in SYMBOLS.items():
+            f = getattr(L, name)
+            f.argtypes = argt
+            f.restype = rest
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        raise RbgError(status, lib().rbg_last_error().decode())
+
+
+def lanes() -> tuple[int, int]:
+    a, b = ctypes.c_int(), ctypes.c_int()
+    lib().rbg_lanes(ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
+
+
+def version() -> str:
+    return lib().rbg_version().decode()
+
+
+def unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().rbg_get_unique_id(buf))
+    return bytes(buf)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass
+class Result:
+    k: int
+    stop: str
+    pivots: np.ndarray   # (k,) global column ids
+    errors: np.ndarray   # (k+1,)
+    nu: np.ndarray       # (k,)
+    rdiag: np.ndarray    # (k,)
+    Q: np.ndarray | None   # (k, N)
+    R: np.ndarray | None   # (k, M_loc)
+    r2: np.ndarray | None  # (M_loc,)
+
+
+class Context:
+    """One rbg_ctx.  ``S`` is an (M_loc, N) array: host numpy (copied) or a CUDA torch
+    tensor (borrowed when contiguous, i.e. ld = N)."""
+
+    def __init__(self, S, w=None, tol: float = 0.0, k_max: int = 1, *, stream=None,
+                 comm: int = COMM_NONE, rank: int = 0, world: int = 1, col_offset: int = 0,
+                 M_global: int = 0, nccl_id: bytes | None = None, check_finite: bool = True,
+                 borrow: bool = True):
+        L = lib()
+        d = Desc()
+        L.rbg_desc_init(ctypes.byref(d))
+        self._keep = []
+        if _is_torch(S):
+            import torch
+            if not S.is_cuda:
+                S = S.numpy()
+            else:
+                if S.dim() != 2:
+                    raise ValueError("S must be 2-D (M, N)")
+                cplx = S.is_complex()
+                if S.dtype not in (torch.float64, torch.complex128):
+                    raise ValueError("S must be float64 or complex128")
+                if S.stride(1) != 1:
+                    raise ValueError("S rows (snapshots) must be contiguous")
+                d.S = S.data_ptr()
+                d.S_mem = MEM_DEVICE
+                d.ld = S.stride(0)
+                d.borrow = 1 if borrow else 0
+                d.M, d.N = S.shape
+                d.dtype = COMPLEX_F64 if cplx else REAL_F64
+                d.device = S.device.index if S.device.index is not None else torch.cuda.current_device()
+                if stream is None:
+                    stream = torch.cuda.current_stream(S.device).cuda_stream
+                self._keep.append(S)
+        if not _is_torch(S):
+            S = np.ascontiguousarray(S)
+            if S.dtype not in (np.float64, np.complex128):
+                S = S.astype(np.complex128 if np.iscomplexobj(S) else np.float64)
+            d.S = S.ctypes.data
+            d.S_mem = MEM_HOST
+            d.M, d.N = S.shape
+            d.ld = S.shape[1]
+            d.dtype = COMPLEX_F64 if np.iscomplexobj(S) else REAL_F64
+            self._keep.append(S)
+        if w is not None:
+            if _is_torch(w) and w.is_cuda:
+                d.w = w.data_ptr()
+                d.w_mem = MEM_DEVICE
+            else:
+                wn = np.ascontiguousarray(np.asarray(w, dtype=np.float64))
+                if wn.shape != (d.N,):
+                    raise ValueError("w must have N entries")
+                d.w = wn.ctypes.data
+                d.w_mem = MEM_HOST
+            self._keep.append(w)
+        d.tol = float(tol)
+        d.k_max = int(k_max)
+        d.stream = stream
+        d.check_finite = 1 if check_finite else 0
+        d.comm = comm
+        d.rank = rank
+        d.world = world
+        d.col_offset = col_offset
+        d.M_global = M_global
+        if nccl_id is not None:
+            ctypes.memmove(d.nccl_id, nccl_id, 128)
+        self.N, self.M = int(d.N), int(d.M)
+        self.cplx = d.dtype == COMPLEX_F64
+        self.k_max = int(k_max)
+        h = ctypes.c_void_p()
+        _check(L.rbg_create_ex(ctypes.byref(h), ctypes.byref(d)))
+        self.h = h
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rbg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- execution
+    def run(self):
+        _check(lib().rbg_run(self.h))
+        return self
+
+    def step(self, n: int):
+        _check(lib().rbg_step(self.h, int(n)))
+
+    def sync(self):
+        _check(lib().rbg_sync(self.h))
+
+    def set_timing(self, on: bool):
+        _check(lib().rbg_set_timing(self.h, 1 if on else 0))
+
+    def set_graph_batch(self, batch: int):
+        _check(lib().rbg_set_graph_batch(self.h, int(batch)))
+
+    def iter_local(self):
+        _check(lib().rbg_iter_local(self.h))
+
+    def iter_finish(self):
+        _check(lib().rbg_iter_finish(self.h))
+
+    # -- results
+    def info(self) -> tuple[int, int, str]:
+        k, m, why = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        _check(lib().rbg_result_info(self.h, ctypes.byref(k), ctypes.byref(m), ctypes.byref(why)))
+        return k.value, m.value, STOP[why.value]
+
+    def pivots(self) -> np.ndarray:
+        k = self.info()[0]
+        out = np.zeros(max(k, 1), np.int64)
+        _check(lib().rbg_get_pivots(self.h, out.ctypes.data))
+        return out[:k]
+
+    def errors(self) -> np.ndarray:
+        k, _, why = self.info()
+        n = k + 1 if why != "NONE" else k
+        out = np.zeros(max(n, 1))
+        _check(lib().rbg_get_errors(self.h, out.ctypes.data))
+        return out[:n]
+
+    def nu(self) -> np.ndarray:
+        k = self.info()[0]
+        out = np.zeros(max(k, 1), np.int32)
+        _check(lib().rbg_get_nu(self.h, out.ctypes.data))
+        return out[:k]
+
+    def rdiag(self) -> np.ndarray:
+        k = self.info()[0]
+        out = np.zeros(max(k, 1))
+        _check(lib().rbg_get_rdiag(self.h, out.ctypes.data))
+        return out[:k]
+
+    def basis(self) -> np.ndarray:
+        k = self.info()[0]
+        out = np.zeros((max(k, 1), self.N), np.complex128 if self.cplx else np.float64)
+        _check(lib().rbg_get_basis(self.h, out.ctypes.data, self.N, 0))
+        return out[:k]
+
+    def R(self) -> np.ndarray:
+        k = self.info()[0]
+        out = np.zeros((max(k, 1), self.M), np.complex128 if self.cplx else np.float64)
+        _check(lib().rbg_get_R(self.h, out.ctypes.data, self.M, 0))
+        return out[:k]
+
+    def r2(self) -> np.ndarray:
+        out = np.zeros(self.M)
+        _check(lib().rbg_get_r2(self.h, out.ctypes.data, 0))
+        return out
+
+    def stats(self) -> Stats:
+        s = Stats()
+        _check(lib().rbg_get_stats(self.h, ctypes.byref(s)))
+        return s
+
+    def timings(self, n: int):
+        a, b, c = np.zeros(n), np.zeros(n), np.zeros(n)
+        _check(lib().rbg_get_timings(self.h, a.ctypes.data, b.ctypes.data, c.ctypes.data, n))
+        return a, b, c
+
+    def xchg_buffers(self):
+        s, r, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().rbg_xchg_buffers(self.h, ctypes.byref(s), ctypes.byref(r), ctypes.byref(n)))
+        return s.value, r.value, n.value
+
+    def result(self, full: bool = True) -> Result:
+        k, _, why = self.info()
+        return Result(k=k, stop=why, pivots=self.pivots(), errors=self.errors(), nu=self.nu(),
+                      rdiag=self.rdiag(), Q=self.basis() if full else None,
+                      R=self.R() if full else None, r2=self.r2() if full else None)
+
+
+def emulate_allgather(ctxs: list[Context]):
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.h for c in ctxs])
+    _check(lib().rbg_emulate_allgather(arr, len(ctxs)))
+
+
+def greedy(S, w=None, tol: float = 0.0, k_max: int = 1, full: bool = True, **kw) -> Result:
+    """Run the RB-greedy to its stop reason on one GPU and return the results (host)."""
+    with Context(S, w, tol, k_max, **kw) as ctx:
+        ctx.run()
+        return ctx.result(full)
+
+
+def gen_chirp(S, t, w, q, chi, psi, spin: bool, stream=None):
+    """Fill the CUDA complex128 tensor S (M, N) with chirps on the device (rbg_gen.h)."""
+    import torch
+    from .inputs import CHIRP_EPS, CHIRP_F0
+    dev = S.device
+    x = (-np.asarray(t) + CHIRP_EPS)
+    A = torch.as_tensor(x ** -0.25, device=dev)
+    base = torch.as_tensor(-2.0 * np.pi * CHIRP_F0 * x ** 0.625 / 0.625, device=dev)
+    wt = torch.as_tensor(np.asarray(w, dtype=np.float64), device=dev)
+    qt = torch.as_tensor(np.asarray(q, dtype=np.float64), device=dev)
+    ct = torch.as_tensor(np.asarray(chi, dtype=np.float64), device=dev)
+    pt = torch.as_tensor(np.asarray(psi, dtype=np.float64), device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    M, N = S.shape
+    rc = lib().rbg_gen_chirp(S.data_ptr(), N, M, S.stride(0), A.data_ptr(), base.data_ptr(),
+                             wt.data_ptr(), qt.data_ptr(), ct.data_ptr(), pt.data_ptr(),
+                             1 if spin else 0, stream)
+    if rc != 0:
+        raise RbgError(ECUDA, f"rbg_gen_chirp failed ({rc})")
+    torch.cuda.current_stream(dev).synchronize()
+    del A, base, wt, qt, ct, pt

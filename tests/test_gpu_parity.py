@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, same seeded inputs.
+
+Canonical mode (lanes (32, 2048)) evaluates the same floating-point expression DAG as
+the kernels, so pivots, stop reason, k, nu
+are compared exactly and Q, R, errors, r2 bit for bit.  BASELINE.json's tolerance
+(1e-10 relative) is asserted as well so that a failure says which bar was missed.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1805_06124_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rbg():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1805_06124_b200 import build as B
+    B.build()
+    from paper_1805_06124_b200 import rbg as R
+    return R
+
+
+def compare(g, o, scale=None, exact=True):
+    """g: rbg.Result, o: oracle.GreedyResult."""
+    assert (g.k, g.stop) == (o.k, o.stop), ((g.k, g.stop), (o.k, o.stop))
+    np.testing.assert_array_equal(g.pivots, o.pivots)
+    np.testing.assert_array_equal(g.nu, o.nu)
+    # BASELINE.json bar: 1e-10 relative (per column for R)
+    s = scale if scale is not None else max(o.errors[0], 1e-300)
+    np.testing.assert_allclose(g.errors, o.errors, rtol=0, atol=1e-10 * s)
+    np.testing.assert_allclose(g.Q, o.Q, rtol=0, atol=1e-10 * np.abs(o.Q).max(initial=1.0))
+    np.testing.assert_allclose(g.R, o.R, rtol=0, atol=1e-10 * s)
+    if exact:  # the canonical contract: 0 ulp
+        np.testing.assert_array_equal(g.errors, o.errors)
+        np.testing.assert_array_equal(g.rdiag, o.rdiag)
+        np.testing.assert_array_equal(g.Q, o.Q)
+        np.testing.assert_array_equal(g.R, o.R)
+        np.testing.assert_array_equal(g.r2, o.r2)
+
+
+def both(rbg, orc, S, w, tol, k_max, **kw):
+    g = rbg.greedy(S, w, tol, k_max, **kw)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    return g, o
+
+
+def test_config0_full(rbg, orc):
+    S, w, tol, k_max = inputs.config0()
+    g, o = both(rbg, orc, S, w, tol, k_max)
+    compare(g, o)
+    assert g.stop == "RANK"          # reading R8: the recurrence floor stops it by rank
+
+
+def test_config1_reduced(rbg, orc):
+    S, w, tol, k_max = inputs.config1(M=3000, N=2000)
+    g, o = both(rbg, orc, S, w, tol, k_max)
+    compare(g, o)
+
+
+def test_config1_full(rbg, orc):
+    S, w, tol, k_max = inputs.config1()
+    g, o = both(rbg, orc, S, w, tol, k_max)
+    compare(g, o)
+
+
+def test_config2_reduced(rbg, orc):
+    S, w, tol, k_max = inputs.config2(M=3000, N=10000)
+    g, o = both(rbg, orc, S, w, tol, 60)
+    compare(g, o)
+    assert g.stop == "KMAX"
+
+
+def test_config4_reduced(rbg, orc):
+    S, w, tol, k_max, _ = inputs.config4(M=4096, N=1024, r=256)
+    g, o = both(rbg, orc, S, w, tol, k_max)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("N,M,cplx", [(1, 1, False), (1, 7, True), (7, 1, True), (33, 5, False),
+                                      (257, 1000, False), (255, 3, True), (4097, 300, True),
+                                      (2049, 64, False), (100, 2000, True)])
+def test_ragged_shapes(rbg, orc, N, M, cplx):
+    """Odd N (real padding row), N not a multiple of 32 / 2048, M below the grid size,
+    single row / single column."""
+    rng = np.random.default_rng(N * 7919 + M)
+    S = rng.standard_normal((M, N)) + (1j * rng.standard_normal((M, N)) if cplx else 0)
+    w = rng.uniform(0.5, 1.5, N)
+    k_max = min(N, M, 40)
+    g, o = both(rbg, orc, S, w, 0.0, k_max)
+    compare(g, o)
+
+
+def test_degenerate_inputs(rbg, orc):
+    g = rbg.greedy(np.zeros((5, 4)), None, 0.0, 3)
+    assert (g.k, g.stop, list(g.errors)) == (0, "RANK", [0.0])
+    g = rbg.greedy(np.eye(3), None, 0.0, 3)
+    assert (g.k, g.stop, list(g.pivots), list(g.errors)) == (3, "ALL_SELECTED", [0, 1, 2], [1, 1, 1, 0])
+    g = rbg.greedy(np.diag([3.0, 2.0, 1.0]), None, 1.5, 3)
+    assert (g.k, g.stop, list(g.errors)) == (2, "TOL", [3.0, 2.0, 1.0])
+    g = rbg.greedy(np.diag([3.0, 2.0, 1.0]), None, 0.0, 2)
+    assert (g.k, g.stop) == (2, "KMAX")
+    # exact ties: lowest global index
+    S = np.ones((6, 4))
+    g = rbg.greedy(S, None, 0.0, 2)
+    assert g.pivots[0] == 0 and g.stop == "RANK"
+
+
+def test_device_tensor_borrowed_and_strided(rbg, orc):
+    import torch
+    S, w, tol, k_max = inputs.config1(M=1500, N=512)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    St = torch.as_tensor(S, device="cuda")
+    g = rbg.greedy(St, torch.as_tensor(w, device="cuda"), tol, k_max)
+    compare(g, o)
+    big = torch.zeros((1500, 520), dtype=torch.complex128, device="cuda")
+    big[:, :512] = St
+    g2 = rbg.greedy(big[:, :512], w, tol, k_max)          # ld = 520 > N
+    compare(g2, o)
+    g3 = rbg.greedy(St, w, tol, k_max, borrow=False)      # device copy path
+    compare(g3, o)
+
+
+def test_nonfinite_device_input(rbg):
+    import torch
+    S = torch.ones((10, 8), dtype=torch.float64, device="cuda")
+    S[6, 3] = float("nan")
+    with pytest.raises(rbg.RbgError) as e:
+        rbg.greedy(S, None, 0.0, 3)
+    assert e.value.status == rbg.ENONFINITE and "row 3, col 6" in str(e.value)
+
+
+def test_graph_batches_match_plain(rbg, orc):
+    S, w, tol, k_max = inputs.config1(M=2000, N=1000)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    with rbg.Context(S, w, tol, k_max) as ctx:
+        ctx.set_graph_batch(8)
+        ctx.run()
+        compare(ctx.result(), o)
+
+
+def test_step_api_and_timing_identity(rbg):
+    """rbg_step enqueues iterations; the cost-model identity T = T_sweep + T_xchg + T_IMGS
+     holds to 1% from the library's own events."""
+    S, w, tol, k_max = inputs.config2(M=20000, N=4000)
+    with rbg.Context(S, w, tol, 40) as ctx:
+        ctx.step(10)
+        k, _, why = ctx.info()
+        assert (k, why) == (10, "NONE")
+        ctx.step(3)
+        ctx.run()
+        assert ctx.info()[::2] == (40, "KMAX")
+    with rbg.Context(S, w, tol, 40) as ctx:
+        ctx.set_timing(True)
+        ctx.step(10)                  # no host synchronisation between step and run
+        ctx.run()
+        st = ctx.stats()
+        assert st.k == 40 and st.sweeps == 40
+        parts = st.t_init_ms + st.t_sweep_ms + st.t_xchg_ms + st.t_imgs_ms
+        assert abs(st.t_total_ms - parts) <= 0.01 * st.t_total_ms
+        sw, xc, im = ctx.timings(40)
+        assert np.all(np.isfinite(sw)) and np.all(sw > 0)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_path_on_one_gpu(rbg, orc, world):
+    """The column-sharded algorithm (EXTERNAL exchange) gives the single-GPU results bit
+    for bit: per-column arithmetic is partition independent and the maxloc order total."""
+    S, w, tol, k_max = inputs.config1(M=3001, N=700)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    M = S.shape[0]
+    bounds = [M * p // world for p in range(world + 1)]
+    ctxs = [rbg.Context(S[bounds[p]:bounds[p + 1]], w, tol, k_max, comm=rbg.COMM_EXTERNAL,
+                        rank=p, world=world, col_offset=bounds[p], M_global=M)
+            for p in range(world)]
+    for _ in range(k_max + 1):
+        for c in ctxs:
+            c.iter_local()
+        rbg.emulate_allgather(ctxs)
+        for c in ctxs:
+            c.iter_finish()
+    res = [c.result() for c in ctxs]
+    for r in res:
+        assert (r.k, r.stop) == (o.k, o.stop)
+        np.testing.assert_array_equal(r.pivots, o.pivots)
+        np.testing.assert_array_equal(r.errors, o.errors)
+        np.testing.assert_array_equal(r.Q, o.Q)
+    R = np.concatenate([r.R for r in res], axis=1)
+    np.testing.assert_array_equal(R, o.R)
+    np.testing.assert_array_equal(np.concatenate([r.r2 for r in res]), o.r2)
+    for c in ctxs:
+        c.close()
