@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""bench.py -- the RB-greedy hot path (arXiv 1805.06124) on B200, one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1, one rank per GPU)
+
+Workload (BASELINE.json config 2; config 3 weak scaling for N > 1): complex fp64 chirp
+snapshots, N = 10,000 rows x 409,600 columns PER GPU (65.5 GB per GPU, generated on the
+device), Simpson weights, tol 0, k_max 300.  One step = one greedy iteration (pivot
+decision + IMGS + fused sweep over all columns).  W warm-up iterations (plus sweep 0) run
+untimed, then exactly K iterations are timed with CUDA events on the library's stream,
+max over ranks.  Inputs (65.5 GB) exceed the 126 MB L2, so no flush is needed.
+
+``value`` is whole-job throughput: greedy iterations/s times the number of 409,600-column
+shards (= plain iterations/s at N = 1, the metric BASELINE.json quotes).  The JSON line
+also carries the fused sweep's roofline (HBM bytes per launch / event-timed duration,
+against MEASURED_PEAKS.json), the CPU oracle baseline on a bounded sample, an end-to-end
+number through the C ABI with host buffers, and the SM clocks seen during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "greedy iterations/s and achieved HBM GB/s (% of B200 peak) at 1/2/4/8 GPUs"
+N_ROWS = 10_000
+M_PER_GPU = 409_600
+K_MAX = 300
+CPU_SAMPLE_COLS = 16_384
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=K_MAX - 3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--rows", type=int, default=N_ROWS)
+    p.add_argument("--cols-per-gpu", type=int, default=M_PER_GPU)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--graph-batch", type=int, default=0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "-i", str(device),
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def peaks() -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {}
+
+
+def ncu_traffic():
+    """dram bytes per sweep launch from the committed ncu --set full capture, if any."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "sweep_traffic.json")))["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def cpu_sample(cols: int, iters: int, cfg: int = 2):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
+    from oracle import oracle as O
+    from paper_1805_06124_b200 import inputs
+    S, w, _, _ = inputs.config2(M=cols, N=N_ROWS, cfg=cfg)
+    t0 = time.perf_counter()
+    r = O.greedy(S, w, 0.0, K_MAX, lanes=O.CANONICAL, max_iters=iters)
+    wall = time.perf_counter() - t0
+    return r, wall
+
+
+def oracle_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def full_iter_seconds(r, lo: int, hi: int, cols: int, m_full: int) -> float:
+    """Per-iteration oracle time on the full workload from a column sample: the column sweep
+    and pivot search scale with the column count, IMGS does not."""
+    t_it = np.asarray(r.t_iter[lo:hi])
+    t_im = np.asarray(r.t_imgs[lo:hi])
+    return float(np.mean((t_it - t_im) * (m_full / cols) + t_im))
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    world = a.gpus
+    m_full = a.cols_per_gpu * world
+    W, K = a.warmup, a.steps
+    r, wall = cpu_sample(CPU_SAMPLE_COLS, W + K)
+    t = full_iter_seconds(r, W, W + K, CPU_SAMPLE_COLS, m_full)
+    val = 1.0 / t * world
+    cores = oracle_cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "it/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(a, world),
+        "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "oracle",
+                         "sample": f"CPU oracle (canonical lanes) on {CPU_SAMPLE_COLS} of "
+                                   f"{m_full} columns x {a.rows} rows, iterations {W}..{W + K - 1}; "
+                                   "sweep+pivot time scaled by the column ratio, IMGS as measured"},
+        "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(a, world):
+    return {"workload": ("config2: complex fp64 chirp snapshots 10,000 x 409,600 (65.5 GB), k_max 300"
+                         if world == 1 else
+                         f"config3 weak: 10,000 x 409,600 per GPU x {world} GPUs, k_max 300"),
+            "rows": a.rows, "cols_per_gpu": a.cols_per_gpu, "cols_global": a.cols_per_gpu * world,
+            "k_window": [a.warmup, a.warmup + a.steps], "parallelism": f"column-sharded x{world}",
+            "l2": "inputs (65.5 GB/GPU) >> 126 MB L2; no flush",
+            "value_unit": "greedy iterations/s x (cols_global / 409,600) -- plain it/s at 1 GPU"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_06124_b200 import inputs
+    from paper_1805_06124_b200 import rbg
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    W, K = a.warmup, a.steps
+    if W < 3:
+        raise SystemExit("--warmup must be >= 3")
+    k_max = max(K_MAX, W + K)
+    N, M_loc = a.rows, a.cols_per_gpu
+    M_glob = M_loc * world
+    cfg = 2 if world == 1 else 3
+
+    # ---- synthetic input, generated on the device
+    t_grid = inputs.chirp_grid(N)
+    w = inputs.simpson_weights(N)
+    q, chi, psi = inputs.chirp_params(M_glob, cfg, spin=True)
+    sl = slice(rank * M_loc, (rank + 1) * M_loc)
+    S = torch.empty((M_loc, N), dtype=torch.complex128, device=dev)
+    rbg.gen_chirp(S, t_grid, w, q[sl], chi[sl], psi[sl], spin=True)
+
+    nccl_id = None
+    comm = rbg.COMM_NONE
+    if world > 1:
+        obj = [rbg.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+        comm = rbg.COMM_NCCL
+    stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
+    torch.cuda.set_stream(stream)
+    ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
+                      world=world, col_offset=rank * M_loc, M_global=M_glob, nccl_id=nccl_id)
+    ctx.set_timing(True)
+    if a.graph_batch:
+        ctx.set_graph_batch(a.graph_batch)
+
+    # ---- warm-up (sweep 0 + W iterations), then exactly K timed iterations
+    ctx.step(W)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.step(K)
+    e1.record(stream)
+    e1.synchronize()
+    clocks = clk.stop()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    k, _, why = ctx.info()
+    if k != W + K:
+        raise SystemExit(f"greedy stopped early ({why} at k={k}); the timed steps were not all real")
+    sweep_ms, xchg_ms, imgs_ms = ctx.timings(W + K)
+    # iteration t's sweep uses q_{t-1}: timed iterations W..W+K-1 -> sweeps W-1..W+K-2
+    sw = sweep_ms[W - 1:W + K - 1]
+    im = imgs_ms[W:W + K]
+    xc = xchg_ms[W:W + K]
+    errs = ctx.errors()
+    ctx.close()
+
+    it_s = K / (ms / 1e3)
+    value = it_s * (M_glob / M_PER_GPU)
+    bytes_sweep = N * M_loc * 16 + M_loc * (8 + 8 + 16)      # DESIGN.md "Roofline" per launch
+    sweep_avg_s = float(np.mean(sw)) / 1e3
+    achieved = bytes_sweep / sweep_avg_s / 1e9
+    pk = peaks()
+    peak = pk.get("hbm_gbs") or 6650.0
+    roof = {"kernel": "k_sweep (fused coefficient sweep + r2 update + maxloc)", "bound": "hbm",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if pk.get("hbm_gbs") else "fallback 6.65 TB/s",
+            "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": bytes_sweep,
+            "sweep_ms_avg": sweep_avg_s * 1e3,
+            "share_of_step": float(np.sum(sw) / ms)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (device-generated chirps, BASELINE.json config 2/3 recipe)",
+        "config": config_dict(a, world), "iters_per_s": it_s,
+        "hbm_gbs_per_gpu": achieved, "hbm_gbs_total": achieved * world,
+        "phase_ms_avg": {"sweep": float(np.mean(sw)), "xchg": float(np.mean(xc)), "imgs": float(np.mean(im))},
+        "final_err": float(errs[-1]) if len(errs) else None,
+        "roofline": roof, "clocks": clocks, "gpu_launches": 2 * K,
+    }
+
+    # ---- end to end through the C ABI with host buffers (pinned), all iterations
+    if not a.no_e2e:
+        line["e2e"] = e2e(a, S, w, k_max, W + K, stream, rank, world, M_loc, M_glob, nccl_id, dev)
+    del S
+    torch.cuda.empty_cache()
+
+    # ---- CPU oracle baseline (rank 0, one GPU only)
+    if rank == 0 and world == 1 and not a.no_cpu:
+        iters = 12
+        r, wall = cpu_sample(CPU_SAMPLE_COLS, iters)
+        t_full = full_iter_seconds(r, 2, iters, CPU_SAMPLE_COLS, M_glob)
+        line["cpu_baseline"] = {
+            "value": 1.0 / t_full, "unit": "it/s", "cores": oracle_cores(), "kind": "oracle",
+            "sample": f"CPU oracle (canonical lanes, OpenMP) on {CPU_SAMPLE_COLS} x {N} columns of "
+                      f"the same recipe, iterations 2..{iters - 1} ({wall:.1f} s wall); sweep+pivot "
+                      f"time scaled by {M_glob}/{CPU_SAMPLE_COLS}, IMGS as measured (small k)"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def e2e(a, S, w, k_max, iters, stream, rank, world, M_loc, M_glob, nccl_id, dev):
+    """Same metric through the public API with HOST buffers: H2D of S inside the timed
+    region (create), all iterations, and the D2H read of pivots, errors and basis."""
+    import torch
+    import torch.distributed as dist
+    from paper_1805_06124_b200 import rbg
+
+    host = torch.empty(S.shape, dtype=S.dtype, pin_memory=True)
+    host.copy_(S)
+    S_cols = S.shape
+    del S
+    torch.cuda.empty_cache()
+    Sh = host.numpy()
+    if world > 1:
+        dist.barrier()
+        obj = [rbg.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx = rbg.Context(Sh, w, 0.0, k_max, stream=stream.cuda_stream,
+                      comm=rbg.COMM_NCCL if world > 1 else rbg.COMM_NONE, rank=rank, world=world,
+                      col_offset=rank * M_loc, M_global=M_glob, nccl_id=nccl_id)
+    ctx.step(iters)
+    piv = ctx.pivots()
+    err = ctx.errors()
+    Q = ctx.basis()
+    t1 = time.perf_counter()
+    wall = t1 - t0
+    if world > 1:
+        t = torch.tensor([wall], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    ctx.close()
+    del host, Sh
+    h2d = S_cols[0] * S_cols[1] * 16
+    d2h = piv.nbytes + err.nbytes + Q.nbytes
+    return {"value": iters / wall * (M_glob / M_PER_GPU), "unit": "it/s",
+            "h2d_bytes_per_step": h2d / iters, "d2h_bytes_per_step": d2h / iters,
+            "wall_s": wall, "steps": iters,
+            "note": "rbg_create from pinned host S (H2D + NaN scan) + all iterations + D2H of "
+                    "pivots/errors/basis, wall clock with device sync"}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

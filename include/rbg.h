@@ -83,7 +83,8 @@ typedef struct rbg_desc {
     rbg_dtype dtype;
     double tol;           /* >= 0; stop when err_k < tol                                 */
     int64_t k_max;        /* 1 <= k_max <= min(N, M_global)                              */
-    void *stream;         /* cudaStream_t to enqueue on; NULL => library-owned stream    */
+    void *stream;         /* cudaStream_t to enqueue on (cudaStreamLegacy for the legacy
+                             default stream); NULL => a library-owned stream             */
     int device;           /* CUDA ordinal; -1 => current device                          */
     int check_finite;     /* 1 (default) => scan S for NaN/Inf at create                 */
     rbg_comm comm;

@@ -76,7 +76,7 @@ def lib():
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, i64,
                                  ctypes.POINTER(i64), d, d, d, d,
                                  ctypes.POINTER(ctypes.c_int), d, d,
-                                 ctypes.POINTER(ctypes.c_int), d, d]
+                                 ctypes.POINTER(ctypes.c_int), d, d, d]
         L.orc_greedy.restype = i64
         _lib = L
     return _lib
@@ -151,6 +151,7 @@ class GreedyResult:
     r2: np.ndarray        # (M,) final squared residuals (selected = -inf)
     t_sweep: np.ndarray   # (k,) seconds per sweep
     t_imgs: np.ndarray    # (k,) seconds per IMGS
+    t_iter: np.ndarray    # (k,) seconds per whole iteration (argmax + IMGS + sweep)
 
 
 def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
@@ -177,16 +178,17 @@ def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
     stop = ctypes.c_int()
     ts = np.zeros(k_max)
     ti = np.zeros(k_max)
+    tt = np.zeros(k_max)
     k = lib().orc_greedy(
         _p(Sf), N, M, N * nv, _p(w), cplx, float(tol), int(k_max), lanes[0], lanes[1],
         threads, int(max_iters),
         piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _p(Q.view(np.float64)),
         _p(WQ.view(np.float64)), _p(R.view(np.float64)), _p(err),
         nu.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _p(rdiag), _p(r2),
-        ctypes.byref(stop), _p(ts), _p(ti))
+        ctypes.byref(stop), _p(ts), _p(ti), _p(tt))
     if k < 0:
         raise ValueError("oracle: bad arguments")
     return GreedyResult(k=int(k), stop=STOP_NAMES[stop.value], pivots=piv[:k].copy(),
                         Q=Q[:k].copy(), R=R[:k].copy(), errors=err[:k + 1].copy(),
                         nu=nu[:k].copy(), rdiag=rdiag[:k].copy(), r2=r2, t_sweep=ts[:k].copy(),
-                        t_imgs=ti[:k].copy())
+                        t_imgs=ti[:k].copy(), t_iter=tt[:k].copy())

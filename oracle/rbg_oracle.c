@@ -204,7 +204,8 @@ static double now_s(void)
  * S: column-major, column j at S + j*lds (lds in doubles, >= N*(1+cplx)).
  * Outputs (caller-allocated): piv[k_max], Q/WQ[N*(1+cplx) x k_max] (ldq = N*(1+cplx)),
  * R[k_max x M] row-major (row stride M*(1+cplx) doubles), err[k_max+1], nu[k_max],
- * rdiag[k_max], r2[M].  t_sweep/t_imgs (may be NULL): per-iteration seconds.
+ * rdiag[k_max], r2[M].  t_sweep/t_imgs/t_iter (may be NULL): per-iteration seconds
+ * (t_iter: pivot search + IMGS + sweep of iteration k).
  * L_S / L_I: lane counts for the sweep and for IMGS (powers of two).
  * max_iters >= 0 stops after that many completed iterations with stop = NONE (used to
  * time a bounded sample); pass -1 for no limit.
@@ -215,7 +216,7 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
                    int64_t max_iters,
                    int64_t *piv, double *Q, double *WQ, double *R, double *err, int *nu,
                    double *rdiag, double *r2, int *stop_out,
-                   double *t_sweep, double *t_imgs)
+                   double *t_sweep, double *t_imgs, double *t_iter)
 {
     if (N < 1 || M < 1 || k_max < 1 || !is_pow2(L_S) || !is_pow2(L_I)) return -1;
     const int nv = cplx ? 2 : 1;
@@ -229,7 +230,7 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
 
     /* sweep 0: r2_j = ||s_j||_w^2 */
     double t0 = now_s();
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (M * N > 65536)
     for (int64_t j = 0; j < M; j++) r2[j] = orc_nrm(S + j * lds, w, N, cplx, L_S);
     double t_init = now_s() - t0;
     (void)t_init;
@@ -237,6 +238,7 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
     int64_t k = 0;
     int stop = ORC_STOP_NONE;
     for (;;) {
+        double t_it = now_s();
         /* pivot: argmax of r2 over unselected columns (selected hold -inf), lowest j on ties */
         int64_t J = -1;
         double m = -INFINITY;
@@ -268,7 +270,7 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
         double ts = now_s();
         const double *wq = WQ + (k - 1) * ldq;
         double *Rrow = R + (k - 1) * M * nv;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (M * N > 65536)
         for (int64_t j = 0; j < M; j++) {
             double cr, ci;
             orc_dot(wq, S + j * lds, N, cplx, L_S, &cr, &ci);
@@ -277,6 +279,7 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
             if (r2[j] != -INFINITY) r2[j] = r2[j] - abs2(cr, ci, cplx);
         }
         if (t_sweep) t_sweep[k - 1] = now_s() - ts;
+        if (t_iter) t_iter[k - 1] = now_s() - t_it;
     }
     free(v);
     *stop_out = stop;

@@ -324,16 +324,6 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         for (long long i = 0; i < d->N; i++)
             if (!(wh[i] > 0.0) || std::isinf(wh[i])) return fail(RBG_EINVAL, "w[%lld]=%g must be positive and finite", i, wh[i]);
     }
-    // host S: finiteness check in column-major order (first offending (row, col))
-    if (d->S_mem == RBG_MEM_HOST && d->check_finite) {
-        const double *Sh = static_cast<const double *>(d->S);
-        const long long per = cplx ? 2 : 1;
-        for (long long j = 0; j < d->M; j++)
-            for (long long i = 0; i < d->N; i++)
-                for (long long r = 0; r < per; r++)
-                    if (!std::isfinite(Sh[(j * ld + i) * per + r]))
-                        return fail(RBG_ENONFINITE, "non-finite S entry at (row %lld, col %lld)", i, j + d->col_offset);
-    }
     if (d->S_mem == RBG_MEM_DEVICE && d->borrow) {
         if (reinterpret_cast<uintptr_t>(d->S) % 16) return fail(RBG_EINVAL, "borrowed S must be 16-byte aligned");
         if (!cplx && (ld % 2)) return fail(RBG_EINVAL, "borrowed real S needs an even ld");
@@ -394,7 +384,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         else
             CUB(cudaMemcpy2DAsync(c->S, dst_pitch, d->S, (size_t)ld * c->se, col_bytes, d->M, kind, c->stream));
     }
-    if (d->S_mem == RBG_MEM_DEVICE && d->check_finite) {
+    if (d->check_finite) {  // first non-finite entry in column-major order, on the device
         unsigned long long *bad = nullptr, hbad = ~0ull;
         CUB(cudaMalloc(&bad, sizeof *bad));
         CUB(cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream));

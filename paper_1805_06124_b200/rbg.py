@@ -200,7 +200,9 @@ class Context:
             self._keep.append(w)
         d.tol = float(tol)
         d.k_max = int(k_max)
-        d.stream = stream
+        # an explicit handle 0 is the legacy default stream (cudaStreamLegacy = 0x1); a NULL
+        # stream in the descriptor would make the library create its own stream
+        d.stream = None if stream is None else (1 if int(stream) == 0 else int(stream))
         d.check_finite = 1 if check_finite else 0
         d.comm = comm
         d.rank = rank

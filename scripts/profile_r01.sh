@@ -1,0 +1,8 @@
+set -x
+python bench.py > gpurun_out/bench_full.log 2>&1; echo full rc=$?
+C1="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu"
+$C1 > gpurun_out/plain1.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $C1 > gpurun_out/ncu1.log 2>&1; echo ncu1 rc=$?
+$C1 > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 3 -c 1 -o gpurun_out/prof_sweep $C1 > gpurun_out/ncu2.log 2>&1; echo ncu2 rc=$?
+C2="python bench.py --steps 200 --warmup 3 --no-e2e --no-cpu"
+$C2 > gpurun_out/plain3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_imgs -s 150 -c 1 -o gpurun_out/prof_imgs $C2 > gpurun_out/ncu3.log 2>&1; echo ncu3 rc=$?
+tail -3 gpurun_out/ncu*.log

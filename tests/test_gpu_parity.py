@@ -125,13 +125,18 @@ def test_device_tensor_borrowed_and_strided(rbg, orc):
     compare(g3, o)
 
 
-def test_nonfinite_device_input(rbg):
+def test_nonfinite_input(rbg):
     import torch
     S = torch.ones((10, 8), dtype=torch.float64, device="cuda")
     S[6, 3] = float("nan")
     with pytest.raises(rbg.RbgError) as e:
         rbg.greedy(S, None, 0.0, 3)
     assert e.value.status == rbg.ENONFINITE and "row 3, col 6" in str(e.value)
+    H = np.ones((5, 4), np.complex128)
+    H[3, 2] = complex(1.0, np.inf)
+    with pytest.raises(rbg.RbgError) as e:
+        rbg.greedy(H, None, 0.0, 3)
+    assert e.value.status == rbg.ENONFINITE and "row 2, col 3" in str(e.value)
 
 
 def test_graph_batches_match_plain(rbg, orc):
