@@ -102,6 +102,7 @@ typedef struct rbg_stats {
     double t_xchg_ms;       /* sum of exchange time (C_j); 0 on one GPU                  */
     double t_imgs_ms;       /* sum of pivot decision + IMGS (T_IMGS)                     */
     double t_total_ms;      /* first event to last event (T_j summed)      */
+    double t_gap_ms;        /* launch gaps between iterations (part of C_j)              */
 } rbg_stats;
 
 /* Fill *d with defaults: ld = 0, borrow = 0, w = NULL, device = -1, check_finite = 1,

@@ -618,6 +618,10 @@ rbg_status rbg_get_stats(rbg_ctx *c, rbg_stats *o) {
     for (long long t = 0; t <= last; t++) {
         if (c->ev_iter[t] != t) continue;
         const PhaseEvents &p = c->ev[t];
+        if (t > 0 && c->ev_iter[t - 1] == t - 1) {
+            CU(cudaEventElapsedTime(&ms, c->ev[t - 1].e[3], p.e[0]));
+            o->t_gap_ms += ms;
+        }
         CU(cudaEventElapsedTime(&ms, p.e[0], p.e[1]));
         if (t == 0) o->t_init_ms = ms;
         else {

@@ -78,6 +78,41 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// Cluster-scope acquire wait (data arriving from other CTAs through st.async).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 16-byte store into another CTA's shared memory, completion counted on that CTA's mbarrier.
+__device__ __forceinline__ void st_async_v2(uint32_t dst, double a, double b, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                 "d"(a), "d"(b), "r"(remote_bar)
+                 : "memory");
+}
+
+// L2 evict-last policy for the basis vectors (re-read by every later IMGS).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ double2 ld_keep(const double2 *p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ void st_keep(double2 *p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // L2 evict-first policy for the streamed snapshot matrix (read exactly once per sweep).
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

@@ -9,46 +9,56 @@
 // reductions of length N, so the kernel is latency-bound.  It runs as ONE thread-block
 // cluster of 8 CTAs x 256 threads (L_I = 2048 lanes); the candidate vector v lives in
 // registers (vector u on lane u mod 2048); each MGS step is a lane-local fma chain, a
-// warp xor-butterfly, a tree over the 8 warps in shared memory, an all-to-all of the 8
-// CTA partials through distributed shared memory and one cluster barrier, after which
-// every CTA holds the bit-identical coefficient and updates its slice of v.  The next
-// step's basis vectors are loaded before the reduction so the L2 latency overlaps it.
-// The kernel is replicated on every GPU of a sharded run (no broadcast of q needed).
+// warp xor-butterfly, an all-to-all of the 64 warp partials through distributed shared
+// memory (st.async + mbarrier transaction counts, no CTA or cluster barrier) and a
+// 64-leaf tree evaluated by every warp, after which every CTA holds the bit-identical
+// coefficient and updates its slice of v.  The next step's basis vectors are loaded
+// (L2 evict-last) before the reduction so their latency overlaps it.  The kernel is
+// replicated on every GPU of a sharded run (no broadcast of q needed).
 #include <cmath>
 
 #include "kernels.h"
 
 namespace rbg {
 
+// Sum over the 2048 lanes with the balanced pairwise tree of CAC rule 3.
+//  1. xor-butterfly in the warp (offsets 1..16): every lane holds its warp's partial;
+//  2. lanes 0..7 of warp w of CTA r st.async the partial into slot 8r+w of CTA 0..7's
+//     shared memory, each store counted (16 B) on the receiving CTA's mbarrier;
+//  3. every warp waits for its CTA's 64 slots (1024 B), then lane l adds slots 2l, 2l+1 and
+//     an xor-butterfly over the lanes finishes the tree over the 64 (CTA, warp) leaves.
+// No CTA or cluster barrier is needed; every warp of every CTA ends with the same bits.
+// Slots and mbarriers are double-buffered by reduction parity: a CTA can only receive the
+// data of reduction n+2 after all of its own warps have sent reduction n+1, i.e. after
+// they finished reading the buffers of reduction n.
 struct ClusterReducer {
-    double2 (*s_warp)[8];
-    double2 (*s_cta)[8];
+    double2 (*slots)[64];
+    uint64_t *bars;
     uint32_t rank;
-    int tid, warp, lane, par;
+    int warp, lane, par;
+    uint32_t phase;  // bit p: parity of the next phase to wait for on bars[p]
 
-    // Sum over the 2048 lanes with the balanced pairwise tree of CAC rule 3:
-    // offsets 1..16 in the warp, 32..128 across the 8 warps, 256..1024 across the 8 CTAs.
     __device__ __forceinline__ double2 sum(double re, double im) {
 #pragma unroll
         for (int h = 1; h < 32; h <<= 1) {
             re = re + __shfl_xor_sync(0xffffffffu, re, h);
             im = im + __shfl_xor_sync(0xffffffffu, im, h);
         }
-        if (lane == 0) s_warp[par][warp] = make_double2(re, im);
-        __syncthreads();
-        if (tid < kImgsCtas) {
-            const double2 *p = s_warp[par];
-            const double a = (p[0].x + p[1].x) + (p[2].x + p[3].x);
-            const double b = (p[4].x + p[5].x) + (p[6].x + p[7].x);
-            const double c = (p[0].y + p[1].y) + (p[2].y + p[3].y);
-            const double d = (p[4].y + p[5].y) + (p[6].y + p[7].y);
-            const uint32_t dst = map_dsmem(smem_u32(&s_cta[par][rank]), (uint32_t)tid);
-            st_dsmem_v2(dst, a + b, c + d);
+        if (lane < kImgsCtas) {
+            const uint32_t dst = map_dsmem(smem_u32(&slots[par][rank * 8 + warp]), (uint32_t)lane);
+            const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
+            st_async_v2(dst, re, im, bar);
         }
-        cluster_sync_all();
-        const double2 *q = s_cta[par];
-        const double x = ((q[0].x + q[1].x) + (q[2].x + q[3].x)) + ((q[4].x + q[5].x) + (q[6].x + q[7].x));
-        const double y = ((q[0].y + q[1].y) + (q[2].y + q[3].y)) + ((q[4].y + q[5].y) + (q[6].y + q[7].y));
+        mbar_wait_cluster(&bars[par], (phase >> par) & 1u);
+        phase ^= 1u << par;
+        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[par], 64 * 16);  // re-arm for n+2
+        const double2 a = slots[par][2 * lane], b = slots[par][2 * lane + 1];
+        double x = a.x + b.x, y = a.y + b.y;
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1) {
+            x = x + __shfl_xor_sync(0xffffffffu, x, h);
+            y = y + __shfl_xor_sync(0xffffffffu, y, h);
+        }
         par ^= 1;
         return make_double2(x, y);
     }
@@ -82,8 +92,8 @@ __device__ __forceinline__ double nrm_partial(const double2 (&v)[MAXV], const do
 template <bool CPLX, int MAXV>
 __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads, 1)
     k_imgs(const ImgsArgs a) {
-    __shared__ double2 s_warp[2][8];
-    __shared__ double2 s_cta[2][8];
+    __shared__ double2 s_slots[2][64];
+    __shared__ __align__(8) uint64_t s_bars[2];
 
     const int stop0 = a.st->stop;
     if (stop0) return;
@@ -119,7 +129,15 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     else if (err < a.tol) why = kStopTol;
     else if (k == a.k_max) why = kStopKmax;
 
-    cluster_sync_all();  // every CTA has read the state before rank 0 changes it
+    if (tid == 0) {
+        mbar_init(&s_bars[0], 1);
+        mbar_init(&s_bars[1], 1);
+        mbar_arrive_expect_tx(&s_bars[0], 64 * 16);
+        mbar_arrive_expect_tx(&s_bars[1], 64 * 16);
+    }
+    // every CTA has read the state before rank 0 changes it, and every CTA's mbarriers are
+    // initialised before any remote st.async can target them
+    cluster_sync_all();
     const bool leader = (rank == 0 && tid == 0);
     if (leader) a.errors[k] = err;
     if (why != kStopNone) {
@@ -140,7 +158,8 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
         if (odd_tail && u == nvec - 1) v[mm].y = 0.0;
     }
 
-    ClusterReducer red{s_warp, s_cta, rank, tid, tid >> 5, tid & 31, 0};
+    ClusterReducer red{s_slots, s_bars, rank, tid >> 5, tid & 31, 0, 0u};
+    const uint64_t keep = policy_evict_last();
     const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, lane_g, nvec), 0.0).x);
     double n_prev = n0, nn = 0.0;
     int nu = 0;
@@ -153,8 +172,8 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
 #pragma unroll
             for (int mm = 0; mm < MAXV; mm++) {
                 const long long u = lane_g + (long long)mm * kLaneImgs;
-                wq[mm] = (u < nvec) ? a.WQ[u] : make_double2(0.0, 0.0);
-                q[mm] = (u < nvec) ? a.Q[u] : make_double2(0.0, 0.0);
+                wq[mm] = (u < nvec) ? ld_keep(a.WQ + u, keep) : make_double2(0.0, 0.0);
+                q[mm] = (u < nvec) ? ld_keep(a.Q + u, keep) : make_double2(0.0, 0.0);
             }
         }
         for (long long i = 0; i < k; i++) {
@@ -182,8 +201,8 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
 #pragma unroll
                 for (int mm = 0; mm < MAXV; mm++) {
                     const long long u = lane_g + (long long)mm * kLaneImgs;
-                    wq_n[mm] = (u < nvec) ? wqp[u] : make_double2(0.0, 0.0);
-                    q_n[mm] = (u < nvec) ? qp[u] : make_double2(0.0, 0.0);
+                    wq_n[mm] = (u < nvec) ? ld_keep(wqp + u, keep) : make_double2(0.0, 0.0);
+                    q_n[mm] = (u < nvec) ? ld_keep(qp + u, keep) : make_double2(0.0, 0.0);
                 }
             }
             const double2 c = red.sum(pr, pi);
@@ -236,12 +255,12 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
         const long long u = lane_g + (long long)mm * kLaneImgs;
         if (u < nvec) {
             const double2 qq = make_double2(v[mm].x / nn, v[mm].y / nn);
-            qo[u] = qq;
+            st_keep(qo + u, qq, keep);
             if (CPLX) {
                 const double wu = a.w[u];
-                wqo[u] = make_double2(wu * qq.x, wu * qq.y);
+                st_keep(wqo + u, make_double2(wu * qq.x, wu * qq.y), keep);
             } else {
-                wqo[u] = make_double2(a.w[2 * u] * qq.x, a.w[2 * u + 1] * qq.y);
+                st_keep(wqo + u, make_double2(a.w[2 * u] * qq.x, a.w[2 * u + 1] * qq.y), keep);
             }
         }
     }

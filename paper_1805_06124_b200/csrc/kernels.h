@@ -53,6 +53,7 @@ struct SweepConfig {
     int grid, threads;
     size_t smem;
     bool esmem;  // basis vector staged in shared memory (else read through L1/L2)
+    int unroll;  // 16-byte loads in flight per lane (4, 8, 12, 16)
 };
 
 SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int device);

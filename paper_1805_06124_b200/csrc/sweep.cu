@@ -12,8 +12,10 @@
 //    staged once per CTA into shared memory with TMA bulk copies (cp.async.bulk) on an
 //    mbarrier;
 //  * one warp per column (L_S = 32 lanes): lane l owns the 16-byte vectors u = l (mod 32)
-//    of the column, streamed with 16-byte ld.global.nc.L1::no_allocate + L2 evict-first,
-//    double-buffered in registers, accumulated with explicit fma() in increasing u;
+//    of the column, streamed with 16-byte ld.global.nc.L1::no_allocate + L2 evict-first
+//    through a register ring of U loads in flight per lane (U = 12 on the 10,000-row case:
+//    ~96 KB outstanding per SM, the read-stream ceiling of scripts/hbm_probe.cu),
+//    accumulated with explicit fma() in increasing u;
 //  * xor-butterfly with ascending offsets (= the pairwise lane tree of the CAC);
 //  * lane 0 writes R(k, j), updates r2_j in place, and the warp keeps its maxloc;
 //  * per-CTA maxloc records, the last CTA to finish (atomic ticket) reduces them with the
@@ -21,6 +23,7 @@
 //    the local candidate column into the exchange slot.
 // Sweep 0 (INIT) is the same kernel with e~ = w and the weighted norm of CAC rule 4.
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -28,7 +31,6 @@ namespace rbg {
 
 constexpr int kSweepThreads = 512;
 constexpr int kSweepWarps = kSweepThreads / 32;
-constexpr int kUnroll = 4;
 constexpr size_t kSmemLimit = 220 * 1024;
 constexpr uint32_t kBulkChunk = 32 * 1024;
 
@@ -71,7 +73,7 @@ __device__ __forceinline__ double2 load_e(const double2 *E, const double *Ew, lo
     return ESMEM ? E[u] : __ldg(E + u);
 }
 
-template <bool CPLX, bool INIT, bool ESMEM>
+template <bool CPLX, bool INIT, bool ESMEM, int U>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar;
@@ -118,34 +120,30 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     for (long long c = c_begin + warp; c < c_end; c += kSweepWarps) {
         const double2 *col = a.S + c * a.ldv;
         double re = 0.0, im = 0.0;
-        double2 xa[kUnroll];
+        // ring of U 16-byte loads in flight per lane: slot t is consumed, then immediately
+        // refilled with the vector U*32 further down the column
+        double2 xr[U];
 #pragma unroll
-        for (int t = 0; t < kUnroll; t++) {
+        for (int t = 0; t < U; t++) {
             const long long u = (long long)t * 32 + lane;
-            xa[t] = (u < nvec) ? ld_stream(col + u, pol) : make_double2(0.0, 0.0);
+            xr[t] = (u < nvec) ? ld_stream(col + u, pol) : make_double2(0.0, 0.0);
         }
         if (!waited) {  // first column: loads are in flight, now wait for e~
             mbar_wait(&mbar, 0);
             waited = true;
         }
-        for (long long base = 0; base < nvec; base += 32 * kUnroll) {
-            double2 xb[kUnroll];
+        for (long long base = 0; base < nvec; base += 32 * U) {
 #pragma unroll
-            for (int t = 0; t < kUnroll; t++) {
-                const long long u = base + 32 * kUnroll + (long long)t * 32 + lane;
-                xb[t] = (u < nvec) ? ld_stream(col + u, pol) : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int t = 0; t < kUnroll; t++) {
+            for (int t = 0; t < U; t++) {
                 const long long u = base + (long long)t * 32 + lane;
+                double2 x = xr[t];
+                const long long un = u + 32 * U;
+                xr[t] = (un < nvec) ? ld_stream(col + un, pol) : make_double2(0.0, 0.0);
                 if (u < nvec) {
-                    double2 x = xa[t];
                     if (odd_tail && u == nvec - 1) x.y = 0.0;  // row N is padding
                     accum<CPLX, INIT>(re, im, x, load_e<CPLX, INIT, ESMEM>(E, Ew, u));
                 }
             }
-#pragma unroll
-            for (int t = 0; t < kUnroll; t++) xa[t] = xb[t];
         }
         // lane tree, ascending offsets (CAC rule 3)
 #pragma unroll
@@ -257,12 +255,25 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
     if (c.smem * 2 + 4096 <= 227 * 1024) per_sm = 2;
     (void)device;
     c.grid = num_sms * per_sm;
+    // loads in flight per lane: ~12 keeps ~96 KB per SM outstanding (scripts/hbm_probe.cu)
+    const long long trips = (nvec + 31) / 32;
+    c.unroll = trips >= 12 ? 12 : (trips >= 8 ? 8 : 4);
+    if (const char *env = getenv("RBG_SWEEP_UNROLL")) {
+        const int u = atoi(env);
+        if (u == 4 || u == 8 || u == 12 || u == 16) c.unroll = u;
+    }
     return c;
 }
 
 template <bool CPLX, bool INIT, bool ESMEM>
 static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStream_t s) {
-    auto kern = k_sweep<CPLX, INIT, ESMEM>;
+    auto kern = k_sweep<CPLX, INIT, ESMEM, 4>;
+    switch (cfg.unroll) {
+        case 8: kern = k_sweep<CPLX, INIT, ESMEM, 8>; break;
+        case 12: kern = k_sweep<CPLX, INIT, ESMEM, 12>; break;
+        case 16: kern = k_sweep<CPLX, INIT, ESMEM, 16>; break;
+        default: break;
+    }
     if (cfg.smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)cfg.smem);

@@ -49,7 +49,8 @@ class Desc(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int64), ("sweeps", ctypes.c_int64), ("t_init_ms", ctypes.c_double),
                 ("t_sweep_ms", ctypes.c_double), ("t_xchg_ms", ctypes.c_double),
-                ("t_imgs_ms", ctypes.c_double), ("t_total_ms", ctypes.c_double)]
+                ("t_imgs_ms", ctypes.c_double), ("t_total_ms", ctypes.c_double),
+                ("t_gap_ms", ctypes.c_double)]
 
 
 # (name, argtypes, restype) for every symbol include/rbg.h and include/rbg_gen.h declare

@@ -165,8 +165,11 @@ def test_step_api_and_timing_identity(rbg):
         ctx.run()
         st = ctx.stats()
         assert st.k == 40 and st.sweeps == 40
-        parts = st.t_init_ms + st.t_sweep_ms + st.t_xchg_ms + st.t_imgs_ms
+        # C_j = exchange + launch gaps between iterations
+        c_j = st.t_xchg_ms + st.t_gap_ms
+        parts = st.t_init_ms + st.t_sweep_ms + c_j + st.t_imgs_ms
         assert abs(st.t_total_ms - parts) <= 0.01 * st.t_total_ms
+        assert st.t_gap_ms <= 0.05 * st.t_total_ms
         sw, xc, im = ctx.timings(40)
         assert np.all(np.isfinite(sw)) and np.all(sw > 0)
 
