@@ -49,7 +49,7 @@ struct ClusterReducer {
             const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
             st_async_v2(dst, re, im, bar);
         }
-        mbar_wait_cluster(&bars[par], (phase >> par) & 1u);
+        mbar_wait(&bars[par], (phase >> par) & 1u);
         phase ^= 1u << par;
         if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[par], 64 * 16);  // re-arm for n+2
         const double2 a = slots[par][2 * lane], b = slots[par][2 * lane + 1];
@@ -65,13 +65,12 @@ struct ClusterReducer {
 };
 
 template <bool CPLX, int MAXV>
-__device__ __forceinline__ double nrm_partial(const double2 (&v)[MAXV], const double *w, long long lane_g,
-                                              long long nvec) {
+__device__ __forceinline__ double nrm_partial(const double2 (&v)[MAXV], const double *w, int u0, int nm) {
     double acc = 0.0;
 #pragma unroll
     for (int m = 0; m < MAXV; m++) {
-        const long long u = lane_g + (long long)m * kLaneImgs;
-        if (u < nvec) {  // CAC rule 4
+        if (m < nm) {  // CAC rule 4
+            const int u = u0 + m * kLaneImgs;
             if (CPLX) {
                 const double wu = w[u];
                 double t = wu * v[m].x;
@@ -90,18 +89,131 @@ __device__ __forceinline__ double nrm_partial(const double2 (&v)[MAXV], const do
 }
 
 template <bool CPLX, int MAXV>
-__global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads, 1)
+__device__ __forceinline__ void dot_partial(const double2 (&v)[MAXV], const double2 *wq, int stride, int nm,
+                                            double &pr, double &pi) {
+    pr = 0.0;
+    pi = 0.0;
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) {
+        if (m < nm) {  // DOT(WQ_i, v), CAC rule 2
+            const double2 e = wq[m * stride];
+            if (CPLX) {
+                pr = fma(e.x, v[m].x, pr);
+                pr = fma(e.y, v[m].y, pr);
+                pi = fma(e.x, v[m].y, pi);
+                pi = fma(-e.y, v[m].x, pi);
+            } else {
+                pr = fma(e.x, v[m].x, pr);
+                pr = fma(e.y, v[m].y, pr);
+            }
+        }
+    }
+}
+
+template <bool CPLX, int MAXV>
+__device__ __forceinline__ void axpy(double2 (&v)[MAXV], const double2 *q, int stride, int nm, double2 c) {
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) {
+        if (m < nm) {  // v <- v - c q_i, CAC rule 9
+            const double2 qq = q[m * stride];
+            if (CPLX) {
+                double vr = v[m].x, vi = v[m].y;
+                vr = fma(-c.x, qq.x, vr);
+                vr = fma(c.y, qq.y, vr);
+                vi = fma(-c.x, qq.y, vi);
+                vi = fma(-c.y, qq.x, vi);
+                v[m] = make_double2(vr, vi);
+            } else {
+                v[m].x = fma(-c.x, qq.x, v[m].x);
+                v[m].y = fma(-c.x, qq.y, v[m].y);
+            }
+        }
+    }
+}
+
+// Basis-vector pipeline.  STAGED (D > 0): the CTA's slices of w o q_b and q_b (MAXV chunks of
+// 256 vectors: chunk m starts at vector 2048 m + 256 rank) are prefetched D MGS steps ahead
+// into shared memory by TMA bulk copies issued by a dedicated producer warp (warp 8), one
+// full-mbarrier (TMA bytes) and one empty-mbarrier (8 consumer warps) per stage, so issuing
+// copies never delays a warp on the reduction's critical path.  D = 0: the slices are loaded
+// straight from global memory one step ahead (large N only).
+template <int MAXV, int D>
+struct BasisPipe {
+    unsigned char *smem;
+    uint64_t *full, *empty;
+    const double2 *WQ, *Q;
+    long long ldq_v;
+    int k, rank, nvec;
+
+    static constexpr int kStageBytes = 2 * MAXV * kImgsThreads * 16;
+
+    __device__ __forceinline__ double2 *wq_stage(long long s) const {
+        return reinterpret_cast<double2 *>(smem + (size_t)(s % D) * kStageBytes);
+    }
+    __device__ __forceinline__ double2 *q_stage(long long s) const { return wq_stage(s) + MAXV * kImgsThreads; }
+
+    __device__ void issue(long long s) const {  // one producer thread
+        const int b = (int)(s % k);
+        uint32_t bytes = 0;
+        int len[MAXV];
+#pragma unroll
+        for (int m = 0; m < MAXV; m++) {
+            const int u0 = m * kLaneImgs + rank * kImgsThreads;
+            const int l = nvec - u0;
+            len[m] = l < 0 ? 0 : (l > kImgsThreads ? kImgsThreads : l);
+            bytes += 2u * (uint32_t)len[m] * 16u;
+        }
+        uint64_t *bar = &full[s % D];
+        mbar_arrive_expect_tx(bar, bytes);
+        const double2 *wq = WQ + (long long)b * ldq_v, *q = Q + (long long)b * ldq_v;
+        double2 *dw = wq_stage(s), *dq = q_stage(s);
+#pragma unroll
+        for (int m = 0; m < MAXV; m++) {
+            if (len[m] > 0) {
+                const int u0 = m * kLaneImgs + rank * kImgsThreads;
+                bulk_g2s(dw + m * kImgsThreads, wq + u0, (uint32_t)len[m] * 16u, bar);
+                bulk_g2s(dq + m * kImgsThreads, q + u0, (uint32_t)len[m] * 16u, bar);
+            }
+        }
+    }
+
+    // Producer loop: steps D.. until the consumers publish their final step count in *done
+    // (>= 0); then wait for every copy still in flight so none outlives the CTA.
+    __device__ void produce(long long issued, long long limit, volatile long long *done) const {
+        while (issued < limit) {
+            const uint32_t par = (uint32_t)((issued / D - 1) & 1);
+            bool ok = false;
+            while (!(ok = mbar_try_wait(&empty[issued % D], par)))
+                if (*done >= 0) break;
+            if (!ok) break;
+            issue(issued++);
+        }
+        long long consumed;
+        while ((consumed = *done) < 0) {
+        }
+        for (long long s = consumed; s < issued; s++) mbar_wait(&full[s % D], (uint32_t)((s / D) & 1));
+    }
+};
+
+template <bool CPLX, int MAXV, int D>
+__global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads + 32, 1)
     k_imgs(const ImgsArgs a) {
+    constexpr int DD = D > 0 ? D : 1;
+    extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double2 s_slots[2][64];
     __shared__ __align__(8) uint64_t s_bars[2];
+    __shared__ __align__(8) uint64_t s_full[DD], s_empty[DD];
+    __shared__ long long s_done;
 
     const int stop0 = a.st->stop;
     if (stop0) return;
     const long long k = a.st->k;
     const uint32_t rank = cluster_ctarank();
     const int tid = threadIdx.x;
-    const long long lane_g = (long long)rank * kImgsThreads + tid;
-    const long long nvec = a.nvec;
+    const bool producer = tid >= kImgsThreads;   // warp 8 (D > 0 only)
+    const int nvec = (int)a.nvec;
+    const int u0 = (int)rank * kImgsThreads + tid;             // this lane's first vector
+    const int nm = (!producer && u0 < nvec) ? (nvec - u0 + kLaneImgs - 1) / kLaneImgs : 0;
     const bool odd_tail = !CPLX && (a.N & 1);
 
     // ---- a3: pivot decision (identical in every CTA and on every rank) ------------------
@@ -129,11 +241,22 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     else if (err < a.tol) why = kStopTol;
     else if (k == a.k_max) why = kStopKmax;
 
+    const BasisPipe<MAXV, DD> pipe{dsm, s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec};
+    const long long limit = (long long)kNuMax * k;  // MGS steps that can ever be needed
     if (tid == 0) {
         mbar_init(&s_bars[0], 1);
         mbar_init(&s_bars[1], 1);
         mbar_arrive_expect_tx(&s_bars[0], 64 * 16);
         mbar_arrive_expect_tx(&s_bars[1], 64 * 16);
+        s_done = -1;
+    }
+    if (D > 0 && tid == kImgsThreads) {
+        for (int i = 0; i < DD; i++) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], kImgsThreads / 32);
+        }
+        if (why == kStopNone)
+            for (long long s = 0; s < DD && s < limit; s++) pipe.issue(s);
     }
     // every CTA has read the state before rank 0 changes it, and every CTA's mbarriers are
     // initialised before any remote st.async can target them
@@ -142,6 +265,10 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     if (leader) a.errors[k] = err;
     if (why != kStopNone) {
         if (leader) a.st->stop = why;
+        return;
+    }
+    if (producer) {
+        if (D > 0 && tid == kImgsThreads) pipe.produce(DD < limit ? DD : limit, limit, &s_done);
         return;
     }
 
@@ -153,77 +280,52 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     double2 v[MAXV];
 #pragma unroll
     for (int mm = 0; mm < MAXV; mm++) {
-        const long long u = lane_g + (long long)mm * kLaneImgs;
-        v[mm] = (u < nvec) ? src[u] : make_double2(0.0, 0.0);
+        const int u = u0 + mm * kLaneImgs;
+        v[mm] = (mm < nm) ? src[u] : make_double2(0.0, 0.0);
         if (odd_tail && u == nvec - 1) v[mm].y = 0.0;
     }
 
-    ClusterReducer red{s_slots, s_bars, rank, tid >> 5, tid & 31, 0, 0u};
+    const int warp = tid >> 5, lane = tid & 31;
+    ClusterReducer red{s_slots, s_bars, rank, warp, lane, 0, 0u};
     const uint64_t keep = policy_evict_last();
-    const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, lane_g, nvec), 0.0).x);
+    const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
     double n_prev = n0, nn = 0.0;
     int nu = 0;
     bool accepted = false;
+    long long s = 0;  // MGS steps taken (basis index s mod k)
+    // direct-load path (D == 0): one step of register prefetch
+    double2 wq[MAXV], q[MAXV];
+    if (D == 0 && k > 0) {
+#pragma unroll
+        for (int mm = 0; mm < MAXV; mm++) {
+            wq[mm] = (mm < nm) ? ld_keep(a.WQ + u0 + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
+            q[mm] = (mm < nm) ? ld_keep(a.Q + u0 + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
+        }
+    }
     while (nu < kNuMax) {
         nu++;
-        // prefetch basis vector 0
-        double2 wq[MAXV], q[MAXV];
-        if (k > 0) {
-#pragma unroll
-            for (int mm = 0; mm < MAXV; mm++) {
-                const long long u = lane_g + (long long)mm * kLaneImgs;
-                wq[mm] = (u < nvec) ? ld_keep(a.WQ + u, keep) : make_double2(0.0, 0.0);
-                q[mm] = (u < nvec) ? ld_keep(a.Q + u, keep) : make_double2(0.0, 0.0);
-            }
-        }
-        for (long long i = 0; i < k; i++) {
-            double pr = 0.0, pi = 0.0;
-#pragma unroll
-            for (int mm = 0; mm < MAXV; mm++) {
-                const long long u = lane_g + (long long)mm * kLaneImgs;
-                if (u < nvec) {  // DOT(WQ_i, v), CAC rule 2
-                    if (CPLX) {
-                        pr = fma(wq[mm].x, v[mm].x, pr);
-                        pr = fma(wq[mm].y, v[mm].y, pr);
-                        pi = fma(wq[mm].x, v[mm].y, pi);
-                        pi = fma(-wq[mm].y, v[mm].x, pi);
-                    } else {
-                        pr = fma(wq[mm].x, v[mm].x, pr);
-                        pr = fma(wq[mm].y, v[mm].y, pr);
-                    }
-                }
-            }
-            // next basis vector's loads overlap the cluster reduction
-            double2 wq_n[MAXV], q_n[MAXV];
-            if (i + 1 < k) {
-                const double2 *wqp = a.WQ + (i + 1) * a.ldq_v;
-                const double2 *qp = a.Q + (i + 1) * a.ldq_v;
+        for (long long i = 0; i < k; i++, s++) {
+            double pr, pi;
+            double2 c;
+            if (D > 0) {
+                mbar_wait(&s_full[s % DD], (uint32_t)((s / DD) & 1));
+                dot_partial<CPLX, MAXV>(v, pipe.wq_stage(s) + tid, kImgsThreads, nm, pr, pi);
+                c = red.sum(pr, pi);
+                axpy<CPLX, MAXV>(v, pipe.q_stage(s) + tid, kImgsThreads, nm, c);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[s % DD]);  // this warp is done with the stage
+            } else {
+                dot_partial<CPLX, MAXV>(v, wq, 1, nm, pr, pi);
+                double2 wq_n[MAXV], q_n[MAXV];
+                const long long bn = (i + 1 < k) ? i + 1 : 0;
+                const double2 *wqp = a.WQ + bn * a.ldq_v + u0, *qp = a.Q + bn * a.ldq_v + u0;
 #pragma unroll
                 for (int mm = 0; mm < MAXV; mm++) {
-                    const long long u = lane_g + (long long)mm * kLaneImgs;
-                    wq_n[mm] = (u < nvec) ? ld_keep(wqp + u, keep) : make_double2(0.0, 0.0);
-                    q_n[mm] = (u < nvec) ? ld_keep(qp + u, keep) : make_double2(0.0, 0.0);
+                    wq_n[mm] = (mm < nm) ? ld_keep(wqp + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
+                    q_n[mm] = (mm < nm) ? ld_keep(qp + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
                 }
-            }
-            const double2 c = red.sum(pr, pi);
-#pragma unroll
-            for (int mm = 0; mm < MAXV; mm++) {
-                const long long u = lane_g + (long long)mm * kLaneImgs;
-                if (u < nvec) {  // v <- v - c q_i
-                    if (CPLX) {
-                        double vr = v[mm].x, vi = v[mm].y;
-                        vr = fma(-c.x, q[mm].x, vr);
-                        vr = fma(c.y, q[mm].y, vr);
-                        vi = fma(-c.x, q[mm].y, vi);
-                        vi = fma(-c.y, q[mm].x, vi);
-                        v[mm] = make_double2(vr, vi);
-                    } else {
-                        v[mm].x = fma(-c.x, q[mm].x, v[mm].x);
-                        v[mm].y = fma(-c.x, q[mm].y, v[mm].y);
-                    }
-                }
-            }
-            if (i + 1 < k) {
+                c = red.sum(pr, pi);
+                axpy<CPLX, MAXV>(v, q, 1, nm, c);
 #pragma unroll
                 for (int mm = 0; mm < MAXV; mm++) {
                     wq[mm] = wq_n[mm];
@@ -231,13 +333,14 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
                 }
             }
         }
-        nn = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, lane_g, nvec), 0.0).x);
+        nn = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
         if (nn > n_prev / 2.0) {  // Hoffmann's test with kappa = 2
             accepted = true;
             break;
         }
         n_prev = nn;
     }
+    if (tid == 0) s_done = s;  // release the producer: it drains the copies it issued
     const double delta = 1000.0 * 0x1p-52;
     if (!accepted || !(nn >= delta * n0) || nn == 0.0) {
         if (leader) {
@@ -252,8 +355,8 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     double2 *wqo = a.WQ + k * a.ldq_v;
 #pragma unroll
     for (int mm = 0; mm < MAXV; mm++) {
-        const long long u = lane_g + (long long)mm * kLaneImgs;
-        if (u < nvec) {
+        const int u = u0 + mm * kLaneImgs;
+        if (mm < nm) {
             const double2 qq = make_double2(v[mm].x / nn, v[mm].y / nn);
             st_keep(qo + u, qq, keep);
             if (CPLX) {
@@ -274,27 +377,42 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     }
 }
 
+// (MAXV, D): vectors per lane and prefetch depth, D * MAXV * 8 KB of shared memory.
 int imgs_maxv(long long nvec) {
     const long long per = (nvec + kLaneImgs - 1) / kLaneImgs;
-    if (per <= 1) return 1;
-    if (per <= 2) return 2;
-    if (per <= 4) return 4;
+    if (per <= 6) return (int)(per < 1 ? 1 : per);
     if (per <= 8) return 8;
+    if (per <= 12) return 12;
     if (per <= 16) return 16;
     return 0;
+}
+
+template <bool CPLX, int MAXV, int D>
+static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
+    auto kern = k_imgs<CPLX, MAXV, D>;
+    const size_t smem = D > 0 ? (size_t)D * 2 * MAXV * kImgsThreads * 16 : 0;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<kImgsCtas, kImgsThreads + 32, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <bool CPLX>
 static cudaError_t launch_c(const ImgsArgs &a, cudaStream_t s) {
     switch (imgs_maxv(a.nvec)) {
-        case 1: k_imgs<CPLX, 1><<<kImgsCtas, kImgsThreads, 0, s>>>(a); break;
-        case 2: k_imgs<CPLX, 2><<<kImgsCtas, kImgsThreads, 0, s>>>(a); break;
-        case 4: k_imgs<CPLX, 4><<<kImgsCtas, kImgsThreads, 0, s>>>(a); break;
-        case 8: k_imgs<CPLX, 8><<<kImgsCtas, kImgsThreads, 0, s>>>(a); break;
-        case 16: k_imgs<CPLX, 16><<<kImgsCtas, kImgsThreads, 0, s>>>(a); break;
+        case 1: return launch_md<CPLX, 1, 8>(a, s);
+        case 2: return launch_md<CPLX, 2, 6>(a, s);
+        case 3: return launch_md<CPLX, 3, 6>(a, s);
+        case 4: return launch_md<CPLX, 4, 5>(a, s);
+        case 5: return launch_md<CPLX, 5, 4>(a, s);
+        case 6: return launch_md<CPLX, 6, 4>(a, s);
+        case 8: return launch_md<CPLX, 8, 3>(a, s);
+        case 12: return launch_md<CPLX, 12, 0>(a, s);
+        case 16: return launch_md<CPLX, 16, 0>(a, s);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s) {
