@@ -175,6 +175,7 @@ def run_ours(a):
     import torch
     import torch.distributed as dist
 
+    from paper_1805_06124_b200 import dist as D
     from paper_1805_06124_b200 import inputs
     from paper_1805_06124_b200 import rbg
 
@@ -199,21 +200,21 @@ def run_ours(a):
     t_grid = inputs.chirp_grid(N)
     w = inputs.simpson_weights(N)
     q, chi, psi = inputs.chirp_params(M_glob, cfg, spin=True)
-    sl = slice(rank * M_loc, (rank + 1) * M_loc)
+    off, m_loc = D.partition(M_glob, world, rank)
+    assert m_loc == M_loc
+    sl = slice(off, off + M_loc)
     S = torch.empty((M_loc, N), dtype=torch.complex128, device=dev)
     rbg.gen_chirp(S, t_grid, w, q[sl], chi[sl], psi[sl], spin=True)
 
     nccl_id = None
     comm = rbg.COMM_NONE
     if world > 1:
-        obj = [rbg.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = D.nccl_unique_id()
         comm = rbg.COMM_NCCL
     stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
     torch.cuda.set_stream(stream)
     ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
-                      world=world, col_offset=rank * M_loc, M_global=M_glob, nccl_id=nccl_id)
+                      world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id)
     ctx.set_timing(True)
     if a.graph_batch:
         ctx.set_graph_batch(a.graph_batch)
@@ -235,11 +236,7 @@ def run_ours(a):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = D.max_over_ranks(e0.elapsed_time(e1), device=dev)
     k, _, why = ctx.info()
     if k != W + K:
         raise SystemExit(f"greedy stopped early ({why} at k={k}); the timed steps were not all real")
@@ -313,26 +310,21 @@ def e2e(a, S, w, k_max, iters, stream, rank, world, M_loc, M_glob, nccl_id, dev)
     del S
     torch.cuda.empty_cache()
     Sh = host.numpy()
+    from paper_1805_06124_b200 import dist as D
     if world > 1:
         dist.barrier()
-        obj = [rbg.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = D.nccl_unique_id()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx = rbg.Context(Sh, w, 0.0, k_max, stream=stream.cuda_stream,
                       comm=rbg.COMM_NCCL if world > 1 else rbg.COMM_NONE, rank=rank, world=world,
-                      col_offset=rank * M_loc, M_global=M_glob, nccl_id=nccl_id)
+                      col_offset=D.partition(M_glob, world, rank)[0], M_global=M_glob, nccl_id=nccl_id)
     ctx.step(iters)
     piv = ctx.pivots()
     err = ctx.errors()
     Q = ctx.basis()
     t1 = time.perf_counter()
-    wall = t1 - t0
-    if world > 1:
-        t = torch.tensor([wall], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        wall = float(t.item())
+    wall = D.max_over_ranks(t1 - t0, device=dev)
     ctx.close()
     del host, Sh
     h2d = S_cols[0] * S_cols[1] * 16

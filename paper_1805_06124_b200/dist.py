@@ -1,0 +1,67 @@
+"""Multi-GPU plumbing for the column-sharded greedy.
+
+One process per GPU; torch.distributed supplies the process group (NCCL on GPUs, gloo in
+the CPU tests) and is used only for setup: the column partition, the broadcast of the
+NCCL unique id that the library's own communicator is built from, and max-over-ranks
+timing.  The per-iteration exchange (one ncclAllGather of a {maxloc record, candidate
+column} slot per rank) happens inside librbg.so on the library's stream.
+
+The paper distributes columns over "pivot cores" ("distributing N/P
+columns" read as M/P, reading R11); here contiguous blocks, the last ranks taking the
+remainder one column at a time.
+"""
+from __future__ import annotations
+
+
+def partition(M_global: int, world: int, rank: int) -> tuple[int, int]:
+    """(col_offset, M_loc) of `rank`: contiguous blocks, sizes differ by at most one."""
+    if world < 1 or not 0 <= rank < world or M_global < world:
+        raise ValueError(f"cannot split {M_global} columns over {world} ranks")
+    base, extra = divmod(M_global, world)
+    offset = rank * base + max(0, rank - (world - extra))
+    size = base + (1 if rank >= world - extra else 0)
+    return offset, size
+
+
+def broadcast_bytes(payload: bytes | None, group=None, src: int = 0) -> bytes:
+    """Rank `src` sends `payload` (e.g. the 128-byte NCCL unique id) to every rank."""
+    import torch.distributed as dist
+    obj = [payload]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return obj[0]
+
+
+def nccl_unique_id(group=None) -> bytes:
+    """rbg_get_unique_id on rank 0, broadcast over the process group."""
+    import torch.distributed as dist
+    from . import rbg
+    uid = rbg.unique_id() if dist.get_rank(group) == 0 else None
+    return broadcast_bytes(uid, group)
+
+
+def max_over_ranks(x: float, group=None, device=None) -> float:
+    """Multi-GPU timings are reported as the max over ranks (bench contract)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def sharded_context(S_local, w, tol: float, k_max: int, M_global: int, group=None, **kw):
+    """rbg.Context for this rank's column block, wired to an NCCL communicator shared by the
+    ranks of `group`.  S_local must be this rank's partition(M_global, world, rank) block."""
+    import torch.distributed as dist
+    from . import rbg
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    off, m_loc = partition(M_global, world, rank)
+    if S_local.shape[0] != m_loc:
+        raise ValueError(f"rank {rank} holds {S_local.shape[0]} columns, partition says {m_loc}")
+    if world == 1:
+        return rbg.Context(S_local, w, tol, k_max, **kw)
+    uid = nccl_unique_id(group)
+    return rbg.Context(S_local, w, tol, k_max, comm=rbg.COMM_NCCL, rank=rank, world=world,
+                       col_offset=off, M_global=M_global, nccl_id=uid, **kw)
