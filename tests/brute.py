@@ -6,6 +6,8 @@ the oracle shows up as a disagreement.
 """
 from __future__ import annotations
 
+import ctypes
+import ctypes.util
 from fractions import Fraction
 
 import numpy as np
@@ -99,3 +101,13 @@ def direct_residuals(St: np.ndarray, Qt: np.ndarray) -> np.ndarray:
         return np.sqrt(np.sum(np.abs(St) ** 2, axis=0))
     E = St - Qt @ (Qt.conj().T @ St)
     return np.sqrt(np.sum(np.abs(E) ** 2, axis=0))
+
+
+_libm = ctypes.CDLL(ctypes.util.find_library("m"))
+_libm.fma.restype = ctypes.c_double
+_libm.fma.argtypes = [ctypes.c_double] * 3
+
+
+def fma(a: float, b: float, c: float) -> float:
+    """Correctly rounded a*b + c (C99 fma; Python 3.12 has no math.fma)."""
+    return _libm.fma(a, b, c)

@@ -83,7 +83,11 @@ def test_config4_reduced(rbg, orc):
 
 @pytest.mark.parametrize("N,M,cplx", [(1, 1, False), (1, 7, True), (7, 1, True), (33, 5, False),
                                       (257, 1000, False), (255, 3, True), (4097, 300, True),
-                                      (2049, 64, False), (100, 2000, True)])
+                                      (2049, 64, False), (100, 2000, True),
+                                      # staged IMGS limit, global-memory e~ (N*16 B > smem),
+                                      # unstaged IMGS (12/16 vectors per lane), maximum N
+                                      (16384, 40, True), (14000, 33, True), (20000, 24, True),
+                                      (32768, 20, True), (30001, 25, False), (65536, 12, False)])
 def test_ragged_shapes(rbg, orc, N, M, cplx):
     """Odd N (real padding row), N not a multiple of 32 / 2048, M below the grid size,
     single row / single column."""
