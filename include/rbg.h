@@ -82,7 +82,7 @@ typedef struct rbg_desc {
     rbg_mem w_mem;
     rbg_dtype dtype;
     double tol;           /* >= 0; stop when err_k < tol                                 */
-    int64_t k_max;        /* 1 <= k_max <= min(N, M_global)                              */
+    int64_t k_max;        /* 1 <= k_max <= N (k_max > M_global stops ALL_SELECTED)        */
     void *stream;         /* cudaStream_t to enqueue on (cudaStreamLegacy for the legacy
                              default stream); NULL => a library-owned stream             */
     int device;           /* CUDA ordinal; -1 => current device                          */
@@ -111,7 +111,7 @@ void rbg_desc_init(rbg_desc *d);
 
 /* North-star entry point: host S (N x M, ld = N) and host w (NULL => ones).  The matrix
  * is copied to the current device.  Errors: EINVAL (N < 1, M < 1, k_max outside
- * [1, min(N, M)], tol < 0 or NaN, w_i <= 0 or non-finite, unknown dtype, NULL S or ctx),
+ * [1, N], tol < 0 or NaN, w_i <= 0 or non-finite, unknown dtype, NULL S or ctx),
  * ENONFINITE (first NaN/Inf position in the message), ENOMEM, ECUDA. */
 rbg_status rbg_create(rbg_ctx **ctx, const void *S, int64_t N, int64_t M, const double *w,
                       double tol, int64_t k_max, rbg_dtype dtype);
@@ -158,6 +158,25 @@ rbg_status rbg_get_stats(rbg_ctx *ctx, rbg_stats *out);
 /* Per-iteration phase times (timing mode): n entries each, any pointer may be NULL.     */
 rbg_status rbg_get_timings(rbg_ctx *ctx, double *sweep_ms, double *xchg_ms, double *imgs_ms,
                            int64_t n);
+
+/* Out-of-sample validation ("performs out-of-sample validation of the
+ * resulting basis"; DESIGN.md NEXT f-1): for each column v_j of the N x M_v block V
+ * (column stride ldv elements, 0 => N; host or device), the coefficients
+ * C(i, j) = <q_i, v_j>_w against the current basis (i < k) and the projection error
+ * err_j = sqrt(max(||v_j||_w^2 - sum_i |C(i,j)|^2, 0)) evaluated with the same per-column
+ * arithmetic as the greedy's own residuals (sweep 0 + one sweep per basis vector).
+ * err: M_v doubles (may be NULL); C: k x M_v row-major with row stride ldc (may be NULL);
+ * both on the device if out_on_device.  Blocking.  ENONFINITE if V holds NaN/Inf.         */
+rbg_status rbg_validate(rbg_ctx *ctx, const void *V, int64_t M_v, int64_t ldv, rbg_mem V_mem, double *err,
+                        void *C, int64_t ldc, int out_on_device);
+
+/* Enrichment ("automatically enrich the basis by iterative refinement"):
+ * append the N x M_f block F (column stride ldf, 0 => N) to the training columns of a
+ * single-GPU context.  Their R rows and residuals are computed with the greedy's own
+ * arithmetic, the pivot search restarts over all columns and a stopped greedy may continue
+ * (rbg_run / rbg_step).  The snapshot matrix becomes library-owned (a borrowed S is copied).
+ * ESTATE on sharded contexts.  Blocking.                                                   */
+rbg_status rbg_add_columns(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem);
 
 /* Sharded path driven by the caller (comm = EXTERNAL).  One iteration is
  *   rbg_iter_local (sweep + maxloc + pack the local candidate into the send buffer),

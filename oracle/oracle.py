@@ -73,11 +73,14 @@ def lib():
                                d, d, d, d, ctypes.POINTER(ctypes.c_int)]
         L.orc_imgs.restype = ctypes.c_int
         L.orc_greedy.argtypes = [d, i64, i64, i64, d, ctypes.c_int, ctypes.c_double, i64,
-                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, i64,
+                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, i64,
                                  ctypes.POINTER(i64), d, d, d, d,
                                  ctypes.POINTER(ctypes.c_int), d, d,
                                  ctypes.POINTER(ctypes.c_int), d, d, d]
         L.orc_greedy.restype = i64
+        L.orc_validate.argtypes = [d, i64, i64, d, i64, i64, d, i64, ctypes.c_int, ctypes.c_int,
+                                   d, d, ctypes.c_int]
+        L.orc_validate.restype = None
         _lib = L
     return _lib
 
@@ -156,10 +159,11 @@ class GreedyResult:
 
 def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
            lanes: tuple[int, int] = CANONICAL, threads: int = 0,
-           max_iters: int = -1) -> GreedyResult:
+           max_iters: int = -1, resume: "GreedyResult | None" = None) -> GreedyResult:
     """RB-greedy (Algorithm 3) on S given as an (M, N) C-order array (column-major N x M).
 
-    ``lanes=(L_S, L_I)``; ``threads=0`` lets OpenMP choose.
+    ``lanes=(L_S, L_I)``; ``threads=0`` lets OpenMP choose.  ``resume`` continues from a
+    previous state whose R / r2 already cover all M columns (enrichment).
     """
     Sf, cplx = _flat(S)
     M, N = S.shape
@@ -175,13 +179,25 @@ def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
     nu = np.zeros(k_max, np.int32)
     rdiag = np.zeros(k_max)
     r2 = np.zeros(M)
+    k0 = -1
+    if resume is not None:
+        k0 = resume.k
+        assert resume.R.shape == (k0, M) and resume.r2.shape == (M,)
+        piv[:k0] = resume.pivots
+        Q[:k0] = resume.Q
+        WQ[:k0] = resume.Q * w[None, :]
+        R[:k0] = resume.R
+        err[:k0 + 1] = resume.errors[:k0 + 1]
+        nu[:k0] = resume.nu
+        rdiag[:k0] = resume.rdiag
+        r2[:] = resume.r2
     stop = ctypes.c_int()
     ts = np.zeros(k_max)
     ti = np.zeros(k_max)
     tt = np.zeros(k_max)
     k = lib().orc_greedy(
         _p(Sf), N, M, N * nv, _p(w), cplx, float(tol), int(k_max), lanes[0], lanes[1],
-        threads, int(max_iters),
+        threads, int(max_iters), int(k0),
         piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _p(Q.view(np.float64)),
         _p(WQ.view(np.float64)), _p(R.view(np.float64)), _p(err),
         nu.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _p(rdiag), _p(r2),
@@ -192,3 +208,47 @@ def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
                         Q=Q[:k].copy(), R=R[:k].copy(), errors=err[:k + 1].copy(),
                         nu=nu[:k].copy(), rdiag=rdiag[:k].copy(), r2=r2, t_sweep=ts[:k].copy(),
                         t_imgs=ti[:k].copy(), t_iter=tt[:k].copy())
+
+
+def validate(Q: np.ndarray, V: np.ndarray, w: np.ndarray, L_S: int = CANONICAL[0], threads: int = 0):
+    """Out-of-sample validation against the basis Q (k, N): returns (err, C, e2) with
+    C (k, M_v) the coefficients <q_i, v_j>_w and e2 the recurrence residual (DESIGN.md f-1)."""
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    cplx = np.iscomplexobj(Q) or np.iscomplexobj(V)
+    dt = np.complex128 if cplx else np.float64
+    V = np.ascontiguousarray(V, dtype=dt)
+    M_v, N = V.shape
+    k = Q.shape[0]
+    WQ = np.ascontiguousarray(np.asarray(Q, dtype=dt) * w[None, :]) if k else np.zeros((1, N), dt)
+    C = np.zeros((max(k, 1), M_v), dt)
+    e2 = np.zeros(M_v)
+    nv = 2 if cplx else 1
+    lib().orc_validate(_p(WQ.view(np.float64)), N * nv, k, _p(V.view(np.float64)), M_v, N * nv, _p(w), N,
+                       int(cplx), L_S, _p(C.view(np.float64)), _p(e2), threads)
+    return np.sqrt(np.maximum(e2, 0.0)), C[:k], e2
+
+
+def enrich(S: np.ndarray, V: np.ndarray, w: np.ndarray, tol: float, k_max: int, rounds: int = 3,
+           lanes: tuple[int, int] = CANONICAL):
+    """Iterative refinement (SPEC enrich): greedy on S; per round validate V,
+    append every failing column (err >= tol) not appended before to the training set and
+    continue the greedy from its state.  Returns (result, S_final, history, passed)."""
+    res = greedy(S, w, tol, k_max, lanes=lanes)
+    added = np.zeros(V.shape[0], bool)
+    history = []
+    for _ in range(rounds):
+        err, _, _ = validate(res.Q, V, w, lanes[0])
+        history.append(float(err.max()) if err.size else 0.0)
+        fail = (err >= tol) & ~added
+        if not fail.any():
+            return res, S, history, bool(np.all(err < tol))
+        F = V[fail]
+        added |= fail
+        _, C, e2 = validate(res.Q, F, w, lanes[0])
+        S = np.concatenate([S, F])
+        res.R = np.concatenate([res.R, C], axis=1)
+        res.r2 = np.concatenate([res.r2, e2])
+        res = greedy(S, w, tol, k_max, lanes=lanes, resume=res)
+    err, _, _ = validate(res.Q, V, w, lanes[0])
+    history.append(float(err.max()) if err.size else 0.0)
+    return res, S, history, bool(np.all(err < tol))

@@ -208,12 +208,13 @@ static double now_s(void)
  * (t_iter: pivot search + IMGS + sweep of iteration k).
  * L_S / L_I: lane counts for the sweep and for IMGS (powers of two).
  * max_iters >= 0 stops after that many completed iterations with stop = NONE (used to
- * time a bounded sample); pass -1 for no limit.
+ * time a bounded sample); pass -1 for no limit.  k0 >= 0 resumes from k0 iterations of
+ * state held in the output arrays (enrichment); k0 < 0 starts fresh with sweep 0.
  * Returns k (basis size) or -1 on bad arguments.
  */
 int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const double *w,
                    int cplx, double tol, int64_t k_max, int L_S, int L_I, int nthreads,
-                   int64_t max_iters,
+                   int64_t max_iters, int64_t k0,
                    int64_t *piv, double *Q, double *WQ, double *R, double *err, int *nu,
                    double *rdiag, double *r2, int *stop_out,
                    double *t_sweep, double *t_imgs, double *t_iter)
@@ -228,14 +229,16 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
 #endif
     double *v = (double *)malloc(sizeof(double) * (size_t)ldq);
 
-    /* sweep 0: r2_j = ||s_j||_w^2 */
-    double t0 = now_s();
-#pragma omp parallel for schedule(static) if (M * N > 65536)
-    for (int64_t j = 0; j < M; j++) r2[j] = orc_nrm(S + j * lds, w, N, cplx, L_S);
-    double t_init = now_s() - t0;
-    (void)t_init;
-
     int64_t k = 0;
+    if (k0 >= 0) {
+        /* resume (enrichment): the caller's arrays hold k0 iterations of state and r2 holds
+         * the residuals of all M columns; the loop continues at the pivot decision */
+        k = k0;
+    } else {
+        /* sweep 0: r2_j = ||s_j||_w^2 */
+#pragma omp parallel for schedule(static) if (M * N > 65536)
+        for (int64_t j = 0; j < M; j++) r2[j] = orc_nrm(S + j * lds, w, N, cplx, L_S);
+    }
     int stop = ORC_STOP_NONE;
     for (;;) {
         double t_it = now_s();
@@ -284,4 +287,35 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
     free(v);
     *stop_out = stop;
     return k;
+}
+
+/*
+ * Out-of-sample validation (DESIGN.md NEXT f-1): for each column v_j of V,
+ * the coefficients C(i,j) = <q_i, v_j>_w (i < k) and the squared projection error
+ *   e2_j = NRM(v_j) - |C(0,j)|^2 - ... - |C(k-1,j)|^2   (subtracted in order i = 0..k-1),
+ * i.e. exactly the residual recurrence the greedy applies to its own columns.
+ * C: k x M_v row-major (row stride M_v elements); e2: M_v.
+ */
+void orc_validate(const double *WQ, int64_t ldq, int64_t k, const double *V, int64_t M_v, int64_t ldv,
+                  const double *w, int64_t N, int cplx, int L_S, double *C, double *e2, int nthreads)
+{
+    const int nv = cplx ? 2 : 1;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(static) if (M_v * N > 65536)
+    for (int64_t j = 0; j < M_v; j++) {
+        const double *v = V + j * ldv;
+        double acc = orc_nrm(v, w, N, cplx, L_S);
+        for (int64_t i = 0; i < k; i++) {
+            double cr, ci;
+            orc_dot(WQ + i * ldq, v, N, cplx, L_S, &cr, &ci);
+            C[(i * M_v + j) * nv] = cr;
+            if (cplx) C[(i * M_v + j) * nv + 1] = ci;
+            acc = acc - abs2(cr, ci, cplx);
+        }
+        e2[j] = acc;
+    }
 }

@@ -88,6 +88,7 @@ struct rbg_ctx {
     SweepConfig cfg_init{}, cfg_sweep{};
     bool started = false;
     bool local_pending = false;  // EXTERNAL: local done, finish not yet
+    bool resume_pending = false; // columns were added: next iteration starts at the decision
     long long iters = 0;         // iterations enqueued
     bool timing = false;
     std::vector<PhaseEvents> ev;  // per iteration when timing
@@ -135,6 +136,8 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.WQ = c->WQ;
     a.ldq_v = c->ldq_v;
     a.R = c->R;
+    a.ldr = c->M;
+    a.qi = -1;
     a.r2 = c->r2;
     a.st = c->st;
     a.recs = c->recs;
@@ -171,6 +174,10 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
 }
 
 rbg_status enqueue_local(rbg_ctx *c) {
+    if (c->resume_pending) {  // r2 / R of the added columns are already up to date
+        c->resume_pending = false;
+        return RBG_OK;
+    }
     const bool init = !c->started;
     CU(launch_sweep(sweep_args(c), c->cplx, init, init ? c->cfg_init : c->cfg_sweep, c->stream));
     c->started = true;
@@ -232,7 +239,7 @@ rbg_status build_graph(rbg_ctx *c) {
 
 rbg_status enqueue_n(rbg_ctx *c, long long n) {
     while (n > 0) {
-        if (!c->started || c->timing || c->graph_batch <= 0 || n < c->graph_batch) {
+        if (!c->started || c->resume_pending || c->timing || c->graph_batch <= 0 || n < c->graph_batch) {
             TRY(enqueue_iteration(c));
             n--;
             continue;
@@ -254,6 +261,79 @@ rbg_status check_ctx(rbg_ctx *c) {
 rbg_status read_state(rbg_ctx *c, DevState *h) {
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaMemcpy(h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+// Device copy of a caller block in the library's column layout (nvec 16-byte vectors per
+// column, zero padded), with the NaN/Inf scan.  *out is owned by the caller of this helper.
+rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld, rbg_mem mem, double2 **out) {
+    *out = nullptr;
+    if (!src || Mb < 1) return fail(RBG_EINVAL, "null block or no columns");
+    if (ld == 0) ld = c->N;
+    if (ld < c->N) return fail(RBG_EINVAL, "ld=%lld < N=%lld", ld, c->N);
+    const size_t pitch = (size_t)c->nvec * 16, col_bytes = (size_t)c->N * c->se;
+    double2 *d = nullptr;
+    CU(cudaMalloc(&d, pitch * Mb));
+    const cudaMemcpyKind kind = mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    cudaError_t e = cudaSuccess;
+    if (pitch != col_bytes) e = cudaMemsetAsync(d, 0, pitch * Mb, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(d, pitch, src, (size_t)ld * c->se, col_bytes, Mb, kind, c->stream);
+    unsigned long long *bad = nullptr, hbad = ~0ull;
+    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof *bad);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = launch_check_finite(d, c->nvec, Mb, c->N, c->nvec, c->cplx, bad, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(bad);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return fail(RBG_ECUDA, "uploading a column block: %s", cudaGetErrorString(e));
+    }
+    if (hbad != ~0ull) {
+        cudaFree(d);
+        return fail(RBG_ENONFINITE, "non-finite entry at (row %lld, col %lld)", (long long)(hbad % c->N),
+                    (long long)(hbad / c->N));
+    }
+    *out = d;
+    return RBG_OK;
+}
+
+// Sweep 0 and sweeps with q_0..q_{k-1} over an extra column block: exactly the per-column
+// arithmetic the block would have received inside the greedy (R rows, recurrence r2).
+rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, long long ldr, double *r2,
+                        long long k) {
+    DevState *vst = nullptr;
+    Rec *recs = nullptr;
+    unsigned *ticket = nullptr;
+    const int grid = std::max(c->cfg_init.grid, c->cfg_sweep.grid);
+    cudaError_t e = cudaMalloc(&vst, sizeof(DevState));
+    if (e == cudaSuccess) e = cudaMalloc(&recs, sizeof(Rec) * grid);
+    if (e == cudaSuccess) e = cudaMalloc(&ticket, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemsetAsync(vst, 0, sizeof(DevState), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned), c->stream);
+    SweepArgs a = sweep_args(c);
+    a.S = V;
+    a.ldv = c->nvec;
+    a.M = Mv;
+    a.R = R;
+    a.ldr = ldr;
+    a.r2 = r2;
+    a.st = vst;
+    a.recs = recs;
+    a.ticket = ticket;
+    a.col_offset = 0;
+    a.send = nullptr;
+    a.qi = -1;
+    if (e == cudaSuccess) e = launch_sweep(a, c->cplx, true, c->cfg_init, c->stream);
+    for (long long i = 0; i < k && e == cudaSuccess; i++) {
+        a.qi = i;
+        e = launch_sweep(a, c->cplx, false, c->cfg_sweep, c->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(vst);
+    cudaFree(recs);
+    cudaFree(ticket);
+    if (e != cudaSuccess) return fail(RBG_ECUDA, "coefficient passes: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
 
@@ -304,9 +384,10 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     if (world == 1 && (d->col_offset != 0 || Mg != d->M))
         return fail(RBG_EINVAL, "one rank must own all columns");
     if (d->col_offset < 0 || d->col_offset + d->M > Mg) return fail(RBG_EINVAL, "column range outside M_global");
-    if (d->k_max < 1 || d->k_max > std::min<long long>(d->N, Mg))
-        return fail(RBG_EINVAL, "k_max=%lld outside [1, min(N, M)=%lld]", (long long)d->k_max,
-                    std::min<long long>(d->N, Mg));
+    // k_max <= N (a basis of R^N); k_max > M is allowed (the greedy stops ALL_SELECTED, or
+    // continues after rbg_add_columns)
+    if (d->k_max < 1 || d->k_max > d->N)
+        return fail(RBG_EINVAL, "k_max=%lld outside [1, N=%lld]", (long long)d->k_max, (long long)d->N);
     if (world > 1 && d->comm == RBG_COMM_NONE) return fail(RBG_EINVAL, "world > 1 needs comm NCCL or EXTERNAL");
     const bool cplx = d->dtype == RBG_COMPLEX_F64;
     const long long nvec = cplx ? d->N : (d->N + 1) / 2;
@@ -682,6 +763,108 @@ rbg_status rbg_emulate_allgather(rbg_ctx **ctxs, int world) {
         for (int r = 0; r < world; r++)
             CU(cudaMemcpy(ctxs[p]->recv + (size_t)r * ctxs[p]->slot, ctxs[r]->send, ctxs[r]->slot,
                           cudaMemcpyDeviceToDevice));
+    return RBG_OK;
+}
+
+rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg_mem V_mem, double *err, void *C,
+                        int64_t ldc, int out_on_device) {
+    TRY(check_ctx(c));
+    if (C && ldc < M_v) return fail(RBG_EINVAL, "ldc < M_v");
+    if (c->local_pending) return fail(RBG_ESTATE, "validate inside an EXTERNAL iteration");
+    DevState h;
+    TRY(read_state(c, &h));
+    double2 *Vd = nullptr;
+    TRY(upload_block(c, V, M_v, ldv, V_mem, &Vd));
+    const long long k = h.k;
+    double *Rv = nullptr, *e2 = nullptr, *ed = nullptr;
+    cudaError_t e = cudaMalloc(&Rv, (size_t)std::max<long long>(k, 1) * M_v * c->se);
+    if (e == cudaSuccess) e = cudaMalloc(&e2, sizeof(double) * M_v);
+    if (e == cudaSuccess) e = cudaMalloc(&ed, sizeof(double) * M_v);
+    rbg_status st = e == cudaSuccess ? coeff_passes(c, Vd, M_v, Rv, M_v, e2, k)
+                                     : fail(RBG_ENOMEM, "validation buffers: %s", cudaGetErrorString(e));
+    const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (st == RBG_OK && err) {
+        e = launch_sqrt_clamp(e2, ed, M_v, c->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(err, ed, sizeof(double) * M_v, kind, c->stream);
+        if (e != cudaSuccess) st = fail(RBG_ECUDA, "validation errors: %s", cudaGetErrorString(e));
+    }
+    if (st == RBG_OK && C && k) {
+        e = cudaMemcpy2DAsync(C, (size_t)ldc * c->se, Rv, (size_t)M_v * c->se, (size_t)M_v * c->se, k, kind, c->stream);
+        if (e != cudaSuccess) st = fail(RBG_ECUDA, "validation coefficients: %s", cudaGetErrorString(e));
+    }
+    cudaStreamSynchronize(c->stream);
+    cudaFree(Vd);
+    cudaFree(Rv);
+    cudaFree(e2);
+    cudaFree(ed);
+    return st;
+}
+
+rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem) {
+    TRY(check_ctx(c));
+    if (c->world != 1 || c->comm != RBG_COMM_NONE) return fail(RBG_ESTATE, "add_columns needs a single-GPU context");
+    DevState h;
+    TRY(read_state(c, &h));
+    double2 *Fd = nullptr;
+    TRY(upload_block(c, F, M_f, ldf, F_mem, &Fd));
+    const long long M0 = c->M, M1 = c->M + M_f;
+    const size_t pitch = (size_t)c->nvec * 16;
+    double2 *S1 = nullptr;
+    double *R1 = nullptr, *r21 = nullptr;
+    cudaError_t e = cudaMalloc(&S1, pitch * M1);
+    if (e == cudaSuccess) e = cudaMalloc(&R1, (size_t)c->k_max * M1 * c->se);
+    if (e == cudaSuccess) e = cudaMalloc(&r21, sizeof(double) * M1);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(S1, pitch, c->S, (size_t)c->ldv * 16, pitch, M0, cudaMemcpyDeviceToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(S1 + M0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(R1, 0, (size_t)c->k_max * M1 * c->se, c->stream);
+    if (e == cudaSuccess && h.k)
+        e = cudaMemcpy2DAsync(R1, (size_t)M1 * c->se, c->R, (size_t)M0 * c->se, (size_t)M0 * c->se, h.k,
+                              cudaMemcpyDeviceToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(r21, c->r2, sizeof(double) * M0, cudaMemcpyDeviceToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(Fd);
+    if (e != cudaSuccess) {
+        cudaFree(S1);
+        cudaFree(R1);
+        cudaFree(r21);
+        return fail(e == cudaErrorMemoryAllocation ? RBG_ENOMEM : RBG_ECUDA, "add_columns: %s", cudaGetErrorString(e));
+    }
+    if (c->started) {
+        // the new columns get R rows 0..k-1 and the recurrence residual, then the pivot
+        // search restarts over all columns and the next iteration begins at the decision
+        rbg_status st = coeff_passes(c, S1 + M0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), M1, r21 + M0, h.k);
+        if (st != RBG_OK) {
+            cudaFree(S1);
+            cudaFree(R1);
+            cudaFree(r21);
+            return st;
+        }
+    }
+    if (c->own_S) cudaFree(c->S);
+    cudaFree(c->R);
+    cudaFree(c->r2);
+    c->S = S1;
+    c->own_S = true;
+    c->ldv = c->nvec;
+    c->R = R1;
+    c->r2 = r21;
+    c->M = M1;
+    c->M_global = M1;
+    for (auto &p : c->ev)
+        for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
+    c->ev.clear();
+    c->ev_iter.clear();
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    if (c->started) {
+        CU(launch_maxloc(c->r2, M1, 0, c->st, c->stream));
+        CU(cudaMemsetAsync(&c->st->stop, 0, sizeof(int), c->stream));
+        c->resume_pending = true;
+        c->iters = h.k;
+    }
+    CU(cudaStreamSynchronize(c->stream));
     return RBG_OK;
 }
 

@@ -18,7 +18,9 @@ struct SweepArgs {
     const double *w;       // weights, zero padded to a multiple of 2 (+2)
     const double2 *WQ;     // weighted basis, column i at WQ + i*ldq_v
     long long ldq_v;
-    double *R;             // k_max x M row-major, element = 16 B complex / 8 B real
+    double *R;             // k_max rows of ldr elements (16 B complex / 8 B real), row-major
+    long long ldr;         // R row stride in elements (>= M)
+    long long qi;          // >= 0: use basis vector qi and R row qi (validation); -1: q_{k-1}
     double *r2;            // M
     DevState *st;
     Rec *recs;             // one record per CTA
@@ -61,6 +63,11 @@ cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepCo
                          cudaStream_t s);
 int imgs_maxv(long long nvec);  // 0 if unsupported
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s);
+// Deterministic maxloc of r2[0..M) (value desc, index asc) into st->m_loc / st->j_loc.
+cudaError_t launch_maxloc(const double *r2, long long M, long long col_offset, DevState *st,
+                          cudaStream_t s);
+// out[j] = sqrt(max(in[j], 0)) (CAC rule 8), j < M.
+cudaError_t launch_sqrt_clamp(const double *in, double *out, long long M, cudaStream_t s);
 // First non-finite entry of a device block: writes min(col * N + row) (or -1) to *out.
 cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
                                 long long nvec, bool cplx, unsigned long long *out,

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
 
     const int stop = a.st->stop;
     if (stop) return;
-    const long long k = a.st->k;  // sweep uses q_{k-1} (k >= 1) unless INIT
+    // sweep uses q_{k-1} (k >= 1) unless INIT; a validation pass names its basis vector
+    const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long nvec = a.nvec;
     const bool odd_tail = !CPLX && (a.N & 1);
@@ -161,9 +162,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
             r2n = old - cc;                                            // CAC rule 6
             if (lane == 0) {
                 if (CPLX) {
-                    reinterpret_cast<double2 *>(a.R)[(k - 1) * a.M + c] = make_double2(re, im);
+                    reinterpret_cast<double2 *>(a.R)[(k - 1) * a.ldr + c] = make_double2(re, im);
                 } else {
-                    a.R[(k - 1) * a.M + c] = re;
+                    a.R[(k - 1) * a.ldr + c] = re;
                 }
                 a.r2[c] = r2n;
             }
@@ -291,6 +292,62 @@ cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepCo
     }
     if (init) return cfg.esmem ? launch_t<false, true, true>(a, cfg, s) : launch_t<false, true, false>(a, cfg, s);
     return cfg.esmem ? launch_t<false, false, true>(a, cfg, s) : launch_t<false, false, false>(a, cfg, s);
+}
+
+// ------------------------------------------------------------------ maxloc / sqrt helpers
+// Used when columns are added to a context (enrichment): the pivot search over the whole
+// residual vector without a sweep.  One CTA, total order, exact.
+__global__ void __launch_bounds__(1024) k_maxloc(const double *r2, long long M, long long col_offset,
+                                                 DevState *st) {
+    __shared__ double s_m[32];
+    __shared__ long long s_j[32];
+    double bm = -INFINITY;
+    long long bj = 0x7fffffffffffffffLL;
+    for (long long j = threadIdx.x; j < M; j += blockDim.x) {
+        const double m = r2[j];
+        if (rec_better(m, j, bm, bj)) {
+            bm = m;
+            bj = j;
+        }
+    }
+    for (int h = 16; h >= 1; h >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+        const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+        if (rec_better(om, oj, bm, bj)) {
+            bm = om;
+            bj = oj;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_m[threadIdx.x >> 5] = bm;
+        s_j[threadIdx.x >> 5] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+            if (rec_better(s_m[w], s_j[w], bm, bj)) {
+                bm = s_m[w];
+                bj = s_j[w];
+            }
+        st->m_loc = bm;
+        st->j_loc = (bj == 0x7fffffffffffffffLL) ? bj : bj + col_offset;
+    }
+}
+
+cudaError_t launch_maxloc(const double *r2, long long M, long long col_offset, DevState *st, cudaStream_t s) {
+    k_maxloc<<<1, 1024, 0, s>>>(r2, M, col_offset, st);
+    return cudaGetLastError();
+}
+
+__global__ void k_sqrt_clamp(const double *in, double *out, long long M) {
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < M; j += (long long)gridDim.x * blockDim.x)
+        out[j] = sqrt(fmax(in[j], 0.0));
+}
+
+cudaError_t launch_sqrt_clamp(const double *in, double *out, long long M, cudaStream_t s) {
+    const long long blocks = (M + 255) / 256;
+    k_sqrt_clamp<<<(unsigned)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, s>>>(in, out, M);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ finiteness scan

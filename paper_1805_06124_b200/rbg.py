@@ -84,6 +84,8 @@ SYMBOLS = {
     "rbg_version": ([], ctypes.c_char_p),
     "rbg_last_error": ([], ctypes.c_char_p),
     "rbg_destroy": ([_P], None),
+    "rbg_validate": ([_P, _P, _I64, _I64, ctypes.c_int, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_add_columns": ([_P, _P, _I64, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_gen_chirp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
 }
 
@@ -318,6 +320,38 @@ class Context:
         _check(lib().rbg_get_timings(self.h, a.ctypes.data, b.ctypes.data, c.ctypes.data, n))
         return a, b, c
 
+    def _block(self, X):
+        """(pointer, M_b, ld, mem, keepalive) of an (M_b, N) host array or CUDA tensor."""
+        if _is_torch(X) and X.is_cuda:
+            if X.dim() != 2 or X.stride(1) != 1 or X.shape[1] != self.N:
+                raise ValueError("block must be (M_b, N) with contiguous rows")
+            return X.data_ptr(), X.shape[0], X.stride(0), MEM_DEVICE, X
+        if _is_torch(X):
+            X = X.numpy()
+        X = np.ascontiguousarray(X, dtype=np.complex128 if self.cplx else np.float64)
+        if X.ndim != 2 or X.shape[1] != self.N:
+            raise ValueError("block must be (M_b, N)")
+        return X.ctypes.data, X.shape[0], X.shape[1], MEM_HOST, X
+
+    def validate(self, V, coeffs: bool = False):
+        """Projection errors (and optionally coefficients) of the columns of V (M_v, N)
+        against the current basis (rbg_validate)."""
+        ptr, mv, ld, mem, keep = self._block(V)
+        k = self.info()[0]
+        err = np.zeros(mv)
+        C = np.zeros((max(k, 1), mv), np.complex128 if self.cplx else np.float64) if coeffs else None
+        _check(lib().rbg_validate(self.h, ptr, mv, ld, mem, err.ctypes.data,
+                                  C.ctypes.data if coeffs else None, mv, 0))
+        del keep
+        return (err, C[:k]) if coeffs else err
+
+    def add_columns(self, F):
+        """Append the columns of F (M_f, N) to the training set (rbg_add_columns)."""
+        ptr, mf, ld, mem, keep = self._block(F)
+        _check(lib().rbg_add_columns(self.h, ptr, mf, ld, mem))
+        self.M += mf
+        del keep
+
     def xchg_buffers(self):
         s, r, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().rbg_xchg_buffers(self.h, ctypes.byref(s), ctypes.byref(r), ctypes.byref(n)))
@@ -328,6 +362,27 @@ class Context:
         return Result(k=k, stop=why, pivots=self.pivots(), errors=self.errors(), nu=self.nu(),
                       rdiag=self.rdiag(), Q=self.basis() if full else None,
                       R=self.R() if full else None, r2=self.r2() if full else None)
+
+
+def enrich(ctx: Context, V, tol: float, rounds: int = 3):
+    """Iterative refinement (SPEC enrich): validate V against the basis,
+    append every failing column (err >= tol) not appended before, continue the greedy, and
+    repeat up to `rounds` times.  Returns (per-round max validation error, passed)."""
+    Vh = V.cpu().numpy() if _is_torch(V) else np.asarray(V)
+    added = np.zeros(Vh.shape[0], bool)
+    history = []
+    for _ in range(rounds):
+        err = ctx.validate(Vh)
+        history.append(float(err.max()) if err.size else 0.0)
+        fail = (err >= tol) & ~added
+        if not fail.any():
+            return history, bool(np.all(err < tol))
+        ctx.add_columns(Vh[fail])
+        added |= fail
+        ctx.run()
+    err = ctx.validate(Vh)
+    history.append(float(err.max()) if err.size else 0.0)
+    return history, bool(np.all(err < tol))
 
 
 def emulate_allgather(ctxs: list[Context]):

@@ -65,7 +65,7 @@ def test_invalid_arguments_rejected(rbg, case):
     if case == "kmax0":
         k_max = 0
     elif case == "kmax_big":
-        k_max = 5                          # > min(N, M) = 4
+        k_max = 5                          # > N = 4
     elif case == "tol_neg":
         tol = -1.0
     elif case == "tol_nan":

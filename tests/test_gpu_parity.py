@@ -108,6 +108,8 @@ def test_degenerate_inputs(rbg, orc):
     assert (g.k, g.stop, list(g.errors)) == (2, "TOL", [3.0, 2.0, 1.0])
     g = rbg.greedy(np.diag([3.0, 2.0, 1.0]), None, 0.0, 2)
     assert (g.k, g.stop) == (2, "KMAX")
+    g = rbg.greedy(np.eye(4)[:2], None, 0.0, 3)                  # k_max > M
+    assert (g.k, g.stop, list(g.errors)) == (2, "ALL_SELECTED", [1, 1, 0])
     # exact ties: lowest global index
     S = np.ones((6, 4))
     g = rbg.greedy(S, None, 0.0, 2)
