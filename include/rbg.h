@@ -178,6 +178,20 @@ rbg_status rbg_validate(rbg_ctx *ctx, const void *V, int64_t M_v, int64_t ldv, r
  * ESTATE on sharded contexts.  Blocking.                                                   */
 rbg_status rbg_add_columns(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem);
 
+/* Gram matrix G = R R^H of the k x M coefficient block (k = basis size): k x k Hermitian,
+ * column-major with leading dimension ldg >= k, complex (16-byte) entries even for a real
+ * dtype.  Summation order: columns in chunks of 4096, each chunk one sequential fma chain,
+ * chunks added in order (reading R30).  Single-GPU contexts (ESTATE otherwise).   */
+rbg_status rbg_gram(rbg_ctx *ctx, void *G, int64_t ldg, int on_device);
+
+/* Algorithm 4 "Reconstruction": SVD of R(1:k, :) through its Gram
+ * matrix (cyclic Jacobi on the GPU), sigma = singular values in descending order (k
+ * entries, may be NULL), kr = #{sigma_i > tau2} capped at kr_max (0 => no cap), and the
+ * reconstructed basis X = Q V(:, 1:kr) (N x kr column-major, leading dimension ldx >= N;
+ * W-orthonormal; may be NULL).  Single-GPU contexts.  Blocking.                             */
+rbg_status rbg_reconstruct(rbg_ctx *ctx, double tau2, int64_t kr_max, int64_t *kr, double *sigma, void *X,
+                           int64_t ldx, int on_device);
+
 /* Sharded path driven by the caller (comm = EXTERNAL).  One iteration is
  *   rbg_iter_local (sweep + maxloc + pack the local candidate into the send buffer),
  *   the caller's all-gather of send buffers into every rank's receive buffer

@@ -81,6 +81,8 @@ def lib():
         L.orc_validate.argtypes = [d, i64, i64, d, i64, i64, d, i64, ctypes.c_int, ctypes.c_int,
                                    d, d, ctypes.c_int]
         L.orc_validate.restype = None
+        L.orc_gram.argtypes = [d, i64, i64, ctypes.c_int, i64, d]
+        L.orc_gram.restype = None
         _lib = L
     return _lib
 
@@ -252,3 +254,37 @@ def enrich(S: np.ndarray, V: np.ndarray, w: np.ndarray, tol: float, k_max: int, 
     err, _, _ = validate(res.Q, V, w, lanes[0])
     history.append(float(err.max()) if err.size else 0.0)
     return res, S, history, bool(np.all(err < tol))
+
+
+GRAM_CHUNK = 4096  # DESIGN.md reading R30 (written here from the document, not the library)
+
+
+def gram(R: np.ndarray, chunk: int = GRAM_CHUNK) -> np.ndarray:
+    """G = R R^H (k x k, complex) in the chunked order of DESIGN.md R30."""
+    Rf, cplx = _flat(R)
+    k, M = R.shape
+    buf = np.zeros(k * k, np.complex128)            # column-major k x k
+    if k:
+        lib().orc_gram(_p(Rf), k, M, cplx, chunk, _p(buf.view(np.float64)))
+    return buf.reshape((k, k), order="F")
+
+
+def reconstruct(res: GreedyResult, tau2: float = 0.0, kr_max: int = 0):
+    """Algorithm 4: SVD of R(1:k, :) through its Gram matrix (LAPACK
+    eigh as the library step), sigma descending (ties by index), kr = #{sigma > tau2} (prefix,
+    capped at kr_max), X = Q V(:, 1:kr).  Returns (sigma, kr, X (kr, N), V)."""
+    k = res.k
+    if k == 0:
+        return np.zeros(0), 0, np.zeros((0, res.Q.shape[1] if res.Q.ndim == 2 else 0)), None
+    G = gram(res.R)
+    lam, V = np.linalg.eigh(G)
+    order = sorted(range(k), key=lambda i: (-lam[i], i))
+    sigma = np.sqrt(np.maximum(lam[order], 0.0))
+    kr = 0
+    while kr < k and sigma[kr] > tau2:
+        kr += 1
+    if kr_max:
+        kr = min(kr, kr_max)
+    Vs = V[:, order]
+    X = (res.Q.T @ Vs[:, :kr]).T
+    return sigma, kr, X, Vs

@@ -319,3 +319,45 @@ void orc_validate(const double *WQ, int64_t ldq, int64_t k, const double *V, int
         e2[j] = acc;
     }
 }
+
+/*
+ * Gram matrix of the coefficient block for Algorithm 4, reading R30:
+ * G(a,b) = sum_j R(a,j) conj(R(b,j)) for the k x M block R (row-major, row stride M).
+ * Order: the columns are cut into chunks of `chunk`; within a chunk the terms of each pair
+ * are accumulated in increasing j with DOT rule 2 (x~ = R(b,:), y = R(a,:)); the chunk
+ * partials are then added in chunk order; the diagonal's imaginary part is set to 0.
+ * G: k x k column-major, complex interleaved.
+ */
+void orc_gram(const double *R, int64_t k, int64_t M, int cplx, int64_t chunk, double *G)
+{
+    const int nv = cplx ? 2 : 1;
+#pragma omp parallel for schedule(dynamic) if (k * k * M > 1000000)
+    for (int64_t a = 0; a < k; a++) {
+        for (int64_t b = a; b < k; b++) {
+            const double *ra = R + a * M * nv, *rb = R + b * M * nv;
+            double gr = 0.0, gi = 0.0;
+            for (int64_t j0 = 0; j0 < M; j0 += chunk) {
+                const int64_t j1 = j0 + chunk < M ? j0 + chunk : M;
+                double pr = 0.0, pi = 0.0;
+                for (int64_t j = j0; j < j1; j++) {
+                    if (cplx) {
+                        double p = rb[2 * j], q = rb[2 * j + 1], x = ra[2 * j], y = ra[2 * j + 1];
+                        pr = fma(p, x, pr);
+                        pr = fma(q, y, pr);
+                        pi = fma(p, y, pi);
+                        pi = fma(-q, x, pi);
+                    } else {
+                        pr = fma(rb[j], ra[j], pr);
+                    }
+                }
+                gr = gr + pr;
+                gi = gi + pi;
+            }
+            if (a == b) gi = 0.0;  /* a Hermitian matrix has a real diagonal */
+            G[2 * (a + b * k)] = gr;
+            G[2 * (a + b * k) + 1] = gi;
+            G[2 * (b + a * k)] = gr;
+            G[2 * (b + a * k) + 1] = -gi;
+        }
+    }
+}

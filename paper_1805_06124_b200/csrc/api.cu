@@ -868,6 +868,116 @@ rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, 
     return RBG_OK;
 }
 
+namespace {
+// G = R(0:k, :) R(0:k, :)^H into a zero-padded kp x kp column-major device buffer.
+rbg_status gram_device(rbg_ctx *c, int k, int kp, double2 *G) {
+    const long long nchunks = std::max<long long>(1, (c->M + kGramChunk - 1) / kGramChunk);
+    const int nt = (k + 31) / 32;
+    std::vector<int2> tiles;
+    for (int a = 0; a < nt; a++)
+        for (int b = a; b < nt; b++) tiles.push_back(make_int2(a, b));
+    int2 *tiles_d = nullptr;
+    double2 *P = nullptr;
+    cudaError_t e = cudaMalloc(&tiles_d, sizeof(int2) * tiles.size());
+    if (e == cudaSuccess) e = cudaMalloc(&P, sizeof(double2) * (size_t)nchunks * k * k);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(tiles_d, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+        e = launch_gram(c->R, c->M, k, c->M, c->cplx, P, kGramChunk, nchunks, tiles_d, (int)tiles.size(), c->stream);
+    if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(tiles_d);
+    cudaFree(P);
+    if (e != cudaSuccess) return fail(RBG_ECUDA, "gram: %s", cudaGetErrorString(e));
+    return RBG_OK;
+}
+}  // namespace
+
+rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
+    TRY(check_ctx(c));
+    if (c->world != 1) return fail(RBG_ESTATE, "gram needs a single-GPU context");
+    DevState h;
+    TRY(read_state(c, &h));
+    const int k = (int)h.k;
+    if (!G || ldg < k) return fail(RBG_EINVAL, "null output or ldg < k");
+    if (k == 0) return RBG_OK;
+    const int kp = k + (k & 1);
+    double2 *Gd = nullptr;
+    CU(cudaMalloc(&Gd, sizeof(double2) * (size_t)kp * kp));
+    rbg_status st = gram_device(c, k, kp, Gd);
+    if (st == RBG_OK) {
+        cudaError_t e = cudaMemcpy2D(G, (size_t)ldg * 16, Gd, (size_t)kp * 16, (size_t)k * 16, k,
+                                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = fail(RBG_ECUDA, "gram copy: %s", cudaGetErrorString(e));
+    }
+    cudaFree(Gd);
+    return st;
+}
+
+rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_out, double *sigma, void *X,
+                           int64_t ldx, int on_device) {
+    TRY(check_ctx(c));
+    if (c->world != 1) return fail(RBG_ESTATE, "reconstruct needs a single-GPU context");
+    if (!(tau2 >= 0.0) || kr_max < 0) return fail(RBG_EINVAL, "tau2 < 0 or kr_max < 0");
+    if (X && ldx < c->N) return fail(RBG_EINVAL, "ldx < N");
+    DevState h;
+    TRY(read_state(c, &h));
+    const int k = (int)h.k;
+    if (kr_out) *kr_out = 0;
+    if (k == 0) return RBG_OK;
+    const int kp = k + (k & 1);
+    double2 *G = nullptr, *V = nullptr, *Xd = nullptr;
+    Rot *rots = nullptr;
+    unsigned long long *flags = nullptr;
+    int *sweeps = nullptr, *order = nullptr, *krd = nullptr;
+    double *sig = nullptr;
+    cudaError_t e = cudaMalloc(&G, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = cudaMalloc(&V, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = cudaMalloc(&rots, rot_bytes(kp));
+    if (e == cudaSuccess) e = cudaMalloc(&flags, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&sweeps, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&order, sizeof(int) * kp);
+    if (e == cudaSuccess) e = cudaMalloc(&krd, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&sig, sizeof(double) * kp);
+    rbg_status st = e == cudaSuccess ? RBG_OK : fail(RBG_ENOMEM, "reconstruct buffers: %s", cudaGetErrorString(e));
+    if (st == RBG_OK) st = gram_device(c, k, kp, G);
+    if (st == RBG_OK) {
+        std::vector<double2> I((size_t)kp * kp, make_double2(0.0, 0.0));
+        for (int i = 0; i < kp; i++) I[(size_t)i * kp + i] = make_double2(1.0, 0.0);
+        e = cudaMemcpyAsync(V, I.data(), sizeof(double2) * I.size(), cudaMemcpyHostToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), c->stream);
+        if (e == cudaSuccess) e = launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
+        if (e == cudaSuccess)
+            e = launch_eig_sort(G, k, kp, tau2, (int)std::min<int64_t>(kr_max ? kr_max : k, k), order, sig, krd,
+                                c->stream);
+        int kr = 0;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&kr, krd, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e == cudaSuccess && sigma) e = cudaMemcpy(sigma, sig, sizeof(double) * k, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && X && kr > 0) {
+            e = cudaMalloc(&Xd, (size_t)kr * c->nvec * 16);
+            if (e == cudaSuccess)
+                e = launch_recon_x(c->Q, c->ldq_v, c->nvec, k, V, kp, order, kr, Xd, c->nvec, c->cplx, c->stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(X, (size_t)ldx * c->se, Xd, (size_t)c->nvec * 16, (size_t)c->N * c->se, kr,
+                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        }
+        if (e != cudaSuccess) st = fail(RBG_ECUDA, "reconstruct: %s", cudaGetErrorString(e));
+        else if (kr_out) *kr_out = kr;
+    }
+    cudaFree(G);
+    cudaFree(V);
+    cudaFree(Xd);
+    cudaFree(rots);
+    cudaFree(flags);
+    cudaFree(sweeps);
+    cudaFree(order);
+    cudaFree(krd);
+    cudaFree(sig);
+    return st;
+}
+
 void rbg_destroy(rbg_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);

@@ -68,6 +68,20 @@ cudaError_t launch_maxloc(const double *r2, long long M, long long col_offset, D
                           cudaStream_t s);
 // out[j] = sqrt(max(in[j], 0)) (CAC rule 8), j < M.
 cudaError_t launch_sqrt_clamp(const double *in, double *out, long long M, cudaStream_t s);
+// Algorithm 4 (recon.cu)
+struct Rot;
+constexpr long long kGramChunk = 4096;  // columns per Gram chunk (R30)
+cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool cplx, double2 *P, long long chunk,
+                        long long nchunks, int2 *tiles_d, int ntiles, cudaStream_t s);
+cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, double2 *G, cudaStream_t s);
+cudaError_t launch_jacobi(double2 *G, double2 *V, int kp, Rot *rots, unsigned long long *flags, int *sweeps,
+                          int num_sms, cudaStream_t s);
+cudaError_t launch_eig_sort(const double2 *G, int k, int kp, double tau2, int kr_max, int *order, double *sigma,
+                            int *kr, cudaStream_t s);
+cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, int k, const double2 *V, int kp,
+                           const int *order, int kr, double2 *X, long long ldx_v, bool cplx, cudaStream_t s);
+size_t rot_bytes(int kp);
+
 // First non-finite entry of a device block: writes min(col * N + row) (or -1) to *out.
 cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
                                 long long nvec, bool cplx, unsigned long long *out,

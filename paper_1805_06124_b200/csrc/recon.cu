@@ -1,0 +1,315 @@
+// recon.cu -- Algorithm 4 "Reconstruction" (Thm 5.8):
+// after a j-term MGS with pivoting S = Q_j R(1:j, 1:M), take the SVD of the j x M block
+// R(1:j, :) = V Sigma W^H and return X_k = Q_j V(:, 1:k) with sigma_{k+1} < tau2 < sigma_k,
+// a POD-quality basis at O(M j^2 + N j^2) cost.
+//
+// The SVD is taken through the j x j Gram matrix G = R R^H = V Sigma^2 V^H (DESIGN.md
+// reading R30), in three deterministic kernels:
+//  * k_gram: G = R R^H over 32 x 32 tiles of (a, b) pairs (upper triangle of tiles), the
+//    column range cut into chunks of kGramChunk columns; within a chunk every pair is one
+//    sequential fma chain in increasing column index, chunk partials are summed in chunk
+//    order by k_gram_reduce (the order the oracle's orc_gram writes out);
+//  * k_jacobi: cyclic two-sided Jacobi on the Hermitian G with the round-robin (tournament)
+//    ordering, one cooperative grid, three grid-wide barriers per round; converges when
+//    max |g_pq| / sqrt(g_pp g_qq) < 1e-15 (or 40 sweeps);
+//  * k_recon_x: X = Q V(:, 1:k), each element one sequential sum over the basis index.
+#include <cooperative_groups.h>
+
+#include <cmath>
+
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace rbg {
+
+constexpr int kGramTile = 32;   // pairs per tile side
+constexpr int kGramSub = 32;    // columns staged per shared-memory step
+
+// R: k rows of ldr elements (row-major).  P: nchunks x k x k partial sums (complex).
+template <bool CPLX>
+__global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, int k, long long M, long long chunk,
+                                              const int2 *tiles, double2 *P) {
+    __shared__ double2 sa[kGramSub][kGramTile];
+    __shared__ double2 sb[kGramSub][kGramTile];
+    const int2 t = tiles[blockIdx.x];
+    const int a0 = t.x * kGramTile, b0 = t.y * kGramTile;
+    const long long c = blockIdx.y;
+    const long long j0 = c * chunk, j1 = (j0 + chunk < M) ? j0 + chunk : M;
+    const int tid = threadIdx.x;
+    const int ta = (tid >> 4) * 2, tb = (tid & 15) * 2;   // this thread: pairs (a0+ta+{0,1}, b0+tb+{0,1})
+    double re[2][2] = {{0, 0}, {0, 0}}, im[2][2] = {{0, 0}, {0, 0}};
+    for (long long js = j0; js < j1; js += kGramSub) {
+        // stage rows a0..a0+31 and b0..b0+31, columns js..js+31 (transposed: [col][row])
+        for (int e = tid; e < kGramSub * kGramTile; e += 256) {
+            const int r = e / kGramSub, cc = e % kGramSub;
+            const long long j = js + cc;
+            double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
+            if (j < j1) {
+                if (a0 + r < k) va = CPLX ? reinterpret_cast<const double2 *>(R)[(long long)(a0 + r) * ldr + j]
+                                          : make_double2(R[(long long)(a0 + r) * ldr + j], 0.0);
+                if (b0 + r < k) vb = CPLX ? reinterpret_cast<const double2 *>(R)[(long long)(b0 + r) * ldr + j]
+                                          : make_double2(R[(long long)(b0 + r) * ldr + j], 0.0);
+            }
+            sa[cc][r] = va;
+            sb[cc][r] = vb;
+        }
+        __syncthreads();
+        const int n = (int)((j1 - js) < kGramSub ? (j1 - js) : kGramSub);
+        for (int cc = 0; cc < n; cc++) {
+            double2 x[2], y[2];
+            x[0] = sa[cc][ta];
+            x[1] = sa[cc][ta + 1];
+            y[0] = sb[cc][tb];
+            y[1] = sb[cc][tb + 1];
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 2; v++) {
+                    // G_ab += R_a conj(R_b) = DOT(R_b, R_a) term: (p,q) = R_b, (x,y) = R_a
+                    re[u][v] = fma(y[v].x, x[u].x, re[u][v]);
+                    re[u][v] = fma(y[v].y, x[u].y, re[u][v]);
+                    im[u][v] = fma(y[v].x, x[u].y, im[u][v]);
+                    im[u][v] = fma(-y[v].y, x[u].x, im[u][v]);
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) {
+            const int a = a0 + ta + u, b = b0 + tb + v;
+            if (a < k && b < k && b >= a) P[(c * k + a) * k + b] = make_double2(re[u][v], im[u][v]);
+        }
+}
+
+// G (kp x kp column-major, ld kp, zero padded) from chunk partials, summed in chunk order;
+// the lower triangle is the conjugate of the upper.
+__global__ void k_gram_reduce(const double2 *P, long long nchunks, int k, int kp, double2 *G) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)kp * kp;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int a = (int)(e % kp), b = (int)(e / kp);   // G(a, b) at a + b*kp
+        double2 g = make_double2(0.0, 0.0);
+        if (a < k && b < k) {
+            const int lo = a < b ? a : b, hi = a < b ? b : a;
+            for (long long c = 0; c < nchunks; c++) {
+                const double2 p = P[(c * k + lo) * k + hi];
+                g.x = g.x + p.x;
+                g.y = g.y + p.y;
+            }
+            if (a > b) g.y = -g.y;
+            if (a == b) g.y = 0.0;  // a Hermitian matrix has a real diagonal
+        }
+        G[e] = g;
+    }
+}
+
+// ------------------------------------------------------------------ Jacobi eigen-solver
+struct Rot {
+    double cs, sn, er, ei;  // rotation J = [[cs, sn], [-sn e^{-i phi}, cs e^{-i phi}]], e = e^{i phi}
+    int p, q;
+};
+
+__device__ __forceinline__ void round_pair(int r, int i, int kp, int &p, int &q) {
+    // round-robin tournament: player kp-1 fixed, the others rotate
+    if (i == 0) {
+        p = r;
+        q = kp - 1;
+    } else {
+        p = (r + i) % (kp - 1);
+        q = (r - i + kp - 1) % (kp - 1);
+    }
+    if (p > q) {
+        const int t = p;
+        p = q;
+        q = t;
+    }
+}
+
+__device__ __forceinline__ unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }
+
+// G: kp x kp Hermitian (column-major), V: kp x kp (column-major), identity on entry.
+// flags[2]: per-sweep max off-diagonal ratio (double bits, atomicMax; non-negative).
+__global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, Rot *rots,
+                                                unsigned long long *flags, int *sweeps_out) {
+    cg::grid_group grid = cg::this_grid();
+    const int half = kp / 2;
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    int sweep = 0;
+    for (; sweep < 40; sweep++) {
+        unsigned long long *flag = &flags[sweep & 1];
+        for (int r = 0; r < kp - 1; r++) {
+            // A: rotation parameters from the current 2x2 blocks
+            for (long long i = gtid; i < half; i += nthreads) {
+                int p, q;
+                round_pair(r, (int)i, kp, p, q);
+                const double a = G[p + (long long)p * kp].x, b = G[q + (long long)q * kp].x;
+                const double2 c = G[p + (long long)q * kp];  // g_pq
+                const double ac = sqrt(c.x * c.x + c.y * c.y);
+                Rot R;
+                R.p = p;
+                R.q = q;
+                if (ac == 0.0) {
+                    R.cs = 1.0;
+                    R.sn = 0.0;
+                    R.er = 1.0;
+                    R.ei = 0.0;
+                } else {
+                    const double den = sqrt(fabs(a * b));
+                    const double ratio = den > 0.0 ? ac / den : 1.0;
+                    atomicMax(flag, dbits(ratio));
+                    const double tau = (b - a) / (2.0 * ac);
+                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    R.cs = 1.0 / sqrt(1.0 + t * t);
+                    R.sn = t * R.cs;
+                    R.er = c.x / ac;
+                    R.ei = c.y / ac;
+                }
+                rots[i] = R;
+            }
+            grid.sync();
+            // B: columns p, q of G and V: G <- G J, V <- V J
+            for (long long e = gtid; e < (long long)half * kp * 2; e += nthreads) {
+                const long long pair = e / (2LL * kp), rem = e % (2LL * kp);
+                const int row = (int)(rem % kp);
+                double2 *M = (rem < kp) ? G : V;
+                const Rot R = rots[pair];
+                const double2 gp = M[row + (long long)R.p * kp], gq = M[row + (long long)R.q * kp];
+                // e^{-i phi} g_q
+                const double2 eq = make_double2(R.er * gq.x + R.ei * gq.y, R.er * gq.y - R.ei * gq.x);
+                M[row + (long long)R.p * kp] = make_double2(R.cs * gp.x - R.sn * eq.x, R.cs * gp.y - R.sn * eq.y);
+                M[row + (long long)R.q * kp] = make_double2(R.sn * gp.x + R.cs * eq.x, R.sn * gp.y + R.cs * eq.y);
+            }
+            grid.sync();
+            // C: rows p, q of G: G <- J^H G, and the annihilated pair set to zero
+            for (long long e = gtid; e < (long long)half * kp; e += nthreads) {
+                const long long pair = e / kp;
+                const int col = (int)(e % kp);
+                const Rot R = rots[pair];
+                const double2 rp = G[R.p + (long long)col * kp], rq = G[R.q + (long long)col * kp];
+                // e^{i phi} r_q
+                const double2 eq = make_double2(R.er * rq.x - R.ei * rq.y, R.er * rq.y + R.ei * rq.x);
+                double2 np = make_double2(R.cs * rp.x - R.sn * eq.x, R.cs * rp.y - R.sn * eq.y);
+                double2 nq = make_double2(R.sn * rp.x + R.cs * eq.x, R.sn * rp.y + R.cs * eq.y);
+                if (col == R.q) np = make_double2(0.0, 0.0);
+                if (col == R.p) nq = make_double2(0.0, 0.0);
+                if (col == R.p) np.y = 0.0;  // diagonal stays real
+                if (col == R.q) nq.y = 0.0;
+                G[R.p + (long long)col * kp] = np;
+                G[R.q + (long long)col * kp] = nq;
+            }
+            grid.sync();
+        }
+        const double off = __longlong_as_double((long long)*(volatile unsigned long long *)flag);
+        grid.sync();  // everybody has read this sweep's flag
+        if (gtid == 0) flags[(sweep + 1) & 1] = 0ull;
+        grid.sync();
+        if (off < 1e-15) {
+            sweep++;
+            break;
+        }
+    }
+    if (gtid == 0) *sweeps_out = sweep;
+}
+
+// X(:, r) = Q V(:, order[r]) for r < kr: X is N_v x kr vectors (column stride ldx_v), Q is
+// k columns of nvec vectors (stride ldq_v); each element a sequential sum over i.
+template <bool CPLX>
+__global__ void k_recon_x(const double2 *Q, long long ldq_v, long long nvec, int k, const double2 *V, int kp,
+                          const int *order, int kr, double2 *X, long long ldx_v) {
+    const long long total = nvec * kr;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long u = e % nvec;
+        const int r = (int)(e / nvec);
+        const double2 *v = V + (long long)order[r] * kp;
+        double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+        for (int i = 0; i < k; i++) {
+            const double2 q = Q[(long long)i * ldq_v + u];
+            const double2 c = v[i];
+            if (CPLX) {  // q * c
+                acc.x = fma(q.x, c.x, acc.x);
+                acc.x = fma(-q.y, c.y, acc.x);
+                acc.y = fma(q.x, c.y, acc.y);
+                acc.y = fma(q.y, c.x, acc.y);
+            } else {     // two real rows per vector, real eigenvector entries
+                acc.x = fma(q.x, c.x, acc.x);
+                acc2.x = fma(q.y, c.x, acc2.x);
+            }
+        }
+        X[(long long)r * ldx_v + u] = CPLX ? acc : make_double2(acc.x, acc2.x);
+    }
+}
+
+// Eigenvalues (diag of the converged G) in descending order, ties by index; sigma =
+// sqrt(max(lambda, 0)); kr = #{sigma > tau2} capped at kr_max (Algorithm 4 step 6).
+__global__ void k_eig_sort(const double2 *G, int k, int kp, double tau2, int kr_max, int *order, double *sigma,
+                           int *kr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = 0; i < k; i++) order[i] = i;
+    for (int i = 0; i < k; i++) {  // selection sort: k is small
+        int best = i;
+        for (int j = i + 1; j < k; j++) {
+            const double lj = G[order[j] + (long long)order[j] * kp].x, lb = G[order[best] + (long long)order[best] * kp].x;
+            if (lj > lb || (lj == lb && order[j] < order[best])) best = j;
+        }
+        const int t = order[i];
+        order[i] = order[best];
+        order[best] = t;
+    }
+    int n = 0;
+    for (int i = 0; i < k; i++) {
+        sigma[i] = sqrt(fmax(G[order[i] + (long long)order[i] * kp].x, 0.0));
+        if (sigma[i] > tau2 && n == i) n = i + 1;
+    }
+    *kr = n < kr_max ? n : kr_max;
+}
+
+cudaError_t launch_eig_sort(const double2 *G, int k, int kp, double tau2, int kr_max, int *order, double *sigma,
+                            int *kr, cudaStream_t s) {
+    k_eig_sort<<<1, 32, 0, s>>>(G, k, kp, tau2, kr_max, order, sigma, kr);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ host launchers
+cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool cplx, double2 *P, long long chunk,
+                        long long nchunks, int2 *tiles_d, int ntiles, cudaStream_t s) {
+    dim3 grid(ntiles, (unsigned)nchunks);
+    if (cplx) k_gram<true><<<grid, 256, 0, s>>>(R, ldr, k, M, chunk, tiles_d, P);
+    else k_gram<false><<<grid, 256, 0, s>>>(R, ldr, k, M, chunk, tiles_d, P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, double2 *G, cudaStream_t s) {
+    const long long n = (long long)kp * kp;
+    k_gram_reduce<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(P, nchunks, k, kp, G);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jacobi(double2 *G, double2 *V, int kp, Rot *rots, unsigned long long *flags, int *sweeps,
+                          int num_sms, cudaStream_t s) {
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, 256, 0);
+    if (e != cudaSuccess) return e;
+    const int want = (kp * kp + 255) / 256;
+    int grid = per_sm * num_sms;
+    if (grid > want) grid = want;
+    if (grid < 1) grid = 1;
+    void *args[] = {&G, &V, &kp, &rots, &flags, &sweeps};
+    return cudaLaunchCooperativeKernel((void *)k_jacobi, grid, 256, args, 0, s);
+}
+
+cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, int k, const double2 *V, int kp,
+                           const int *order, int kr, double2 *X, long long ldx_v, bool cplx, cudaStream_t s) {
+    const long long n = nvec * kr;
+    const unsigned blocks = (unsigned)((n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192);
+    if (cplx) k_recon_x<true><<<blocks ? blocks : 1, 256, 0, s>>>(Q, ldq_v, nvec, k, V, kp, order, kr, X, ldx_v);
+    else k_recon_x<false><<<blocks ? blocks : 1, 256, 0, s>>>(Q, ldq_v, nvec, k, V, kp, order, kr, X, ldx_v);
+    return cudaGetLastError();
+}
+
+size_t rot_bytes(int kp) { return sizeof(Rot) * (size_t)(kp / 2); }
+
+}  // namespace rbg

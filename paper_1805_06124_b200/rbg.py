@@ -86,6 +86,8 @@ SYMBOLS = {
     "rbg_destroy": ([_P], None),
     "rbg_validate": ([_P, _P, _I64, _I64, ctypes.c_int, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_add_columns": ([_P, _P, _I64, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_gram": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_reconstruct": ([_P, ctypes.c_double, _I64, ctypes.POINTER(_I64), _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_gen_chirp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
 }
 
@@ -351,6 +353,24 @@ class Context:
         _check(lib().rbg_add_columns(self.h, ptr, mf, ld, mem))
         self.M += mf
         del keep
+
+    def gram(self) -> np.ndarray:
+        """G = R R^H of the current coefficient block (k x k complex), rbg_gram."""
+        k = self.info()[0]
+        buf = np.zeros(k * k, np.complex128)        # column-major k x k
+        if k:
+            _check(lib().rbg_gram(self.h, buf.ctypes.data, k, 0))
+        return buf.reshape((k, k), order="F")
+
+    def reconstruct(self, tau2: float = 0.0, kr_max: int = 0):
+        """Algorithm 4: (sigma (k,), kr, X (kr, N)) via rbg_reconstruct."""
+        k = self.info()[0]
+        sigma = np.zeros(max(k, 1))
+        X = np.zeros((max(k, 1), self.N), np.complex128 if self.cplx else np.float64)
+        kr = ctypes.c_int64()
+        _check(lib().rbg_reconstruct(self.h, float(tau2), int(kr_max), ctypes.byref(kr), sigma.ctypes.data,
+                                     X.ctypes.data, self.N, 0))
+        return sigma[:k], kr.value, X[:kr.value]
 
     def xchg_buffers(self):
         s, r, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()
