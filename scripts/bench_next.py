@@ -1,0 +1,83 @@
+#!/usr/bin/env python
+"""Measurements of the NEXT rows (DESIGN.md f-1, f-3) on the config-2 basis (1 x B200).
+
+    python scripts/bench_next.py [--cols 409600] [--val-cols 40960] [--k 300]
+
+After the k-iteration greedy on the device-generated config-2 matrix:
+  * validation of an independent chirp block (k + 1 sweep passes, same fused-sweep kernel):
+    time, HBM GB/s against MEASURED_PEAKS.json;
+  * enrichment step: rbg_add_columns of 4,096 columns (copy + k coefficient passes);
+  * Algorithm 4 reconstruction: Gram (FP64 FLOP/s against the derived FP64 peak), Jacobi,
+    X = Q V; total.
+Prints one JSON line.  Timed with CUDA events / wall clock around blocking ABI calls.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1805_06124_b200 import inputs, rbg  # noqa: E402
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--cols", type=int, default=409600)
+    p.add_argument("--val-cols", type=int, default=40960)
+    p.add_argument("--k", type=int, default=300)
+    a = p.parse_args()
+    N = 10000
+    t = inputs.chirp_grid(N)
+    w = inputs.simpson_weights(N)
+    q, chi, psi = inputs.chirp_params(a.cols, 2, spin=True)
+    S = torch.empty((a.cols, N), dtype=torch.complex128, device="cuda")
+    rbg.gen_chirp(S, t, w, q, chi, psi, spin=True)
+    qv, cv, pv = inputs.chirp_params(a.val_cols, 12, spin=True)
+    V = torch.empty((a.val_cols, N), dtype=torch.complex128, device="cuda")
+    rbg.gen_chirp(V, t, w, qv, cv, pv, spin=True)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    out = {"workload": f"config2 basis k={a.k} on {a.cols} x {N}; validation block {a.val_cols} x {N}"}
+    with rbg.Context(S, w, 0.0, a.k) as ctx:
+        ctx.run()
+        torch.cuda.synchronize()
+        # ---- f-1 validation (warm once)
+        ctx.validate(V[:1024])
+        t0 = time.perf_counter()
+        err = ctx.validate(V)
+        tv = time.perf_counter() - t0
+        bytes_v = (a.k + 1) * (a.val_cols * N * 16 + a.val_cols * 32)
+        out["validate"] = {"s": tv, "passes": a.k + 1, "GBps": bytes_v / tv / 1e9,
+                           "frac_of_measured_hbm": bytes_v / tv / 1e9 / peaks["hbm_gbs"],
+                           "max_err": float(err.max()), "median_err": float(np.median(err)),
+                           "note": "includes the H2D-free device upload copy and NaN scan of V"}
+        # ---- f-3 reconstruction
+        ctx.reconstruct(0.0)               # warm (module load, cooperative launch setup)
+        t0 = time.perf_counter()
+        G = ctx.gram()
+        tg = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sigma, kr, X = ctx.reconstruct(1e-3)
+        tr = time.perf_counter() - t0
+        pairs = a.k * (a.k + 1) / 2
+        flops = pairs * a.cols * 8
+        out["reconstruct"] = {"gram_s": tg, "gram_TFLOPs": flops / tg / 1e12,
+                              "gram_frac_of_fp64_peak": flops / tg / 1e12 / FP64_PEAK_TFLOPS,
+                              "fp64_peak_TFLOPs_derived": FP64_PEAK_TFLOPS,
+                              "total_s": tr, "kr": kr, "sigma_1": float(sigma[0]),
+                              "sigma_k": float(sigma[-1])}
+        # ---- f-1 enrichment step
+        t0 = time.perf_counter()
+        ctx.add_columns(V[:4096])
+        out["add_columns_4096_s"] = time.perf_counter() - t0
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
