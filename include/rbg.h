@@ -192,6 +192,13 @@ rbg_status rbg_gram(rbg_ctx *ctx, void *G, int64_t ldg, int on_device);
 rbg_status rbg_reconstruct(rbg_ctx *ctx, double tau2, int64_t kr_max, int64_t *kr, double *sigma, void *X,
                            int64_t ldx, int on_device);
 
+/* Empirical interpolation nodes (standard greedy EIM in residual form,
+ * DESIGN.md reading R31) for the current basis: nodes[k] row indices (distinct; ties -> lowest
+ * row) and B = Q(nodes, :), the k x k node matrix (column-major, leading dimension ldb >= k,
+ * complex 16-byte entries even for a real dtype; may be NULL).  Requires k <= 1024.  ESTATE
+ * if an interpolation residual vanishes (degenerate basis).  Blocking.                      */
+rbg_status rbg_eim(rbg_ctx *ctx, int64_t *nodes, void *B, int64_t ldb, int on_device);
+
 /* Sharded path driven by the caller (comm = EXTERNAL).  One iteration is
  *   rbg_iter_local (sweep + maxloc + pack the local candidate into the send buffer),
  *   the caller's all-gather of send buffers into every rank's receive buffer

@@ -83,6 +83,8 @@ def lib():
         L.orc_validate.restype = None
         L.orc_gram.argtypes = [d, i64, i64, ctypes.c_int, i64, d]
         L.orc_gram.restype = None
+        L.orc_eim.argtypes = [d, i64, i64, ctypes.POINTER(i64), d]
+        L.orc_eim.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -288,3 +290,20 @@ def reconstruct(res: GreedyResult, tau2: float = 0.0, kr_max: int = 0):
     Vs = V[:, order]
     X = (res.Q.T @ Vs[:, :kr]).T
     return sigma, kr, X, Vs
+
+
+def eim(Q: np.ndarray):
+    """Greedy EIM nodes of the basis Q (k, N) (R31): (nodes (k,), B = Q(nodes, :)
+    as a (k, k) matrix with B[a, b] = q_b(nodes[a])), or None if degenerate."""
+    k, N = Q.shape
+    Qc = np.ascontiguousarray(Q, dtype=np.complex128)
+    nodes = np.zeros(max(k, 1), np.int64)
+    buf = np.zeros(max(k, 1) ** 2, np.complex128)
+    if k == 0:
+        return nodes[:0], np.zeros((0, 0))
+    ok = lib().orc_eim(_p(Qc.view(np.float64)), k, N, nodes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                       _p(buf.view(np.float64)))
+    if not ok:
+        return None
+    B = buf.reshape((k, k), order="F")
+    return nodes, (B if np.iscomplexobj(Q) else B.real.copy())

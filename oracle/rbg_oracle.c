@@ -361,3 +361,78 @@ void orc_gram(const double *R, int64_t k, int64_t M, int cplx, int64_t chunk, do
         }
     }
 }
+
+/* complex helpers for the EIM oracle (R31): v - c*x (CAC rule 9) and a / b */
+static void c_msub(double *vr, double *vi, double cr, double ci, double xr, double xi)
+{
+    double r = *vr, i = *vi;
+    r = fma(-cr, xr, r);
+    r = fma(ci, xi, r);
+    i = fma(-cr, xi, i);
+    i = fma(-ci, xr, i);
+    *vr = r;
+    *vi = i;
+}
+
+static void c_div(double ar, double ai, double br, double bi, double *qr, double *qi)
+{
+    double den = fma(br, br, bi * bi);
+    *qr = fma(ar, br, ai * bi) / den;
+    *qi = fma(ai, br, -(ar * bi)) / den;
+}
+
+/*
+ * Greedy empirical interpolation nodes (the cited Alg. 5 is absent, so
+ * the standard greedy EIM in residual form, reading R31):
+ *   xi_1 = q_1, p_1 = argmax_i |xi_1(i)|^2
+ *   for l = 2..k: c = T^{-1} q_l(P) by forward substitution (T_ab = xi_b(p_a), a >= b),
+ *                 xi_l = q_l - sum_{b<l} c_b xi_b (sequential in b), p_l = argmax |xi_l|^2
+ * ties -> lowest row.  Q: k basis vectors of N complex (interleaved; real data promoted with
+ * zero imaginary parts).  nodes[k]; B (k x k column-major complex) = Q(nodes, :).
+ * Returns 1, or 0 if a residual vanishes (degenerate basis).
+ */
+int orc_eim(const double *Q, int64_t k, int64_t N, int64_t *nodes, double *B)
+{
+    double *Xi = (double *)calloc((size_t)(2 * k * N), sizeof(double));
+    double *T = (double *)calloc((size_t)(2 * k * k), sizeof(double));
+    double *c = (double *)calloc((size_t)(2 * k), sizeof(double));
+    int ok = 1;
+    for (int64_t l = 0; l < k && ok; l++) {
+        const double *q = Q + 2 * l * N;
+        /* forward substitution, row by row, sequential in b */
+        for (int64_t a = 0; a < l; a++) {
+            double vr = q[2 * nodes[a]], vi = q[2 * nodes[a] + 1];
+            for (int64_t b = 0; b < a; b++)
+                c_msub(&vr, &vi, c[2 * b], c[2 * b + 1], T[2 * (a * k + b)], T[2 * (a * k + b) + 1]);
+            c_div(vr, vi, T[2 * (a * k + a)], T[2 * (a * k + a) + 1], &c[2 * a], &c[2 * a + 1]);
+        }
+        /* residual and its argmax */
+        double best = -1.0;
+        int64_t p = 0;
+        for (int64_t i = 0; i < N; i++) {
+            double xr = q[2 * i], xi = q[2 * i + 1];
+            for (int64_t b = 0; b < l; b++)
+                c_msub(&xr, &xi, c[2 * b], c[2 * b + 1], Xi[2 * (b * N + i)], Xi[2 * (b * N + i) + 1]);
+            Xi[2 * (l * N + i)] = xr;
+            Xi[2 * (l * N + i) + 1] = xi;
+            double m = fma(xr, xr, xi * xi);
+            if (m > best) { best = m; p = i; }
+        }
+        if (!(best > 0.0)) { ok = 0; p = 0; }
+        nodes[l] = p;
+        for (int64_t b = 0; b <= l; b++) {
+            T[2 * (l * k + b)] = Xi[2 * (b * N + p)];
+            T[2 * (l * k + b) + 1] = Xi[2 * (b * N + p) + 1];
+        }
+    }
+    if (ok)
+        for (int64_t a = 0; a < k; a++)
+            for (int64_t b = 0; b < k; b++) {
+                B[2 * (a + b * k)] = Q[2 * (b * N + nodes[a])];
+                B[2 * (a + b * k) + 1] = Q[2 * (b * N + nodes[a]) + 1];
+            }
+    free(Xi);
+    free(T);
+    free(c);
+    return ok;
+}

@@ -978,6 +978,33 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     return st;
 }
 
+rbg_status rbg_eim(rbg_ctx *c, int64_t *nodes, void *B, int64_t ldb, int on_device) {
+    TRY(check_ctx(c));
+    DevState h;
+    TRY(read_state(c, &h));
+    const int k = (int)h.k;
+    if (k > 1024) return fail(RBG_EINVAL, "EIM supports k <= 1024 (k = %d)", k);
+    if (B && ldb < k) return fail(RBG_EINVAL, "ldb < k");
+    if (k == 0) return RBG_OK;
+    long long *nd = nullptr;
+    double2 *Bd = nullptr;
+    int *status = nullptr, hs = 0;
+    cudaError_t e = cudaMalloc(&nd, sizeof(long long) * k);
+    if (e == cudaSuccess) e = cudaMalloc(&Bd, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = cudaMalloc(&status, sizeof(int));
+    if (e == cudaSuccess) e = run_eim(c->Q, c->ldq_v, c->N, c->cplx, k, nd, Bd, status, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(&hs, status, sizeof(int), cudaMemcpyDeviceToHost);
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (e == cudaSuccess && nodes) e = cudaMemcpy(nodes, nd, sizeof(long long) * k, kind);
+    if (e == cudaSuccess && B) e = cudaMemcpy2D(B, (size_t)ldb * 16, Bd, (size_t)k * 16, (size_t)k * 16, k, kind);
+    cudaFree(nd);
+    cudaFree(Bd);
+    cudaFree(status);
+    if (e != cudaSuccess) return fail(RBG_ECUDA, "eim: %s", cudaGetErrorString(e));
+    if (hs) return fail(RBG_ESTATE, "EIM residual vanished: the basis is numerically degenerate");
+    return RBG_OK;
+}
+
 void rbg_destroy(rbg_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);

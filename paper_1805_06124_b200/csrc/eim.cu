@@ -1,0 +1,200 @@
+// eim.cu -- empirical interpolation nodes from the greedy basis ("the code
+// also selects a set of empirical interpolation (EI) nodes using a fast algorithm"; the cited
+// Alg. 5 is not in the container, so this is the standard greedy EIM in residual form,
+// DESIGN.md reading R31):
+//     xi_1 = q_1,  p_1 = argmax_i |xi_1(i)|^2
+//     for l = 2..k:  solve T c = q_l(P) by forward substitution, T_ab = xi_b(p_a) (a >= b)
+//                    xi_l = q_l - sum_{b<l} c_b xi_b,   p_l = argmax_i |xi_l(i)|^2
+// Ties go to the lowest row index.  Every sum runs sequentially in b with explicit fma, the
+// complex division uses one fixed formula, so the GPU and the oracle (orc_eim) take the same
+// argmax decisions bit for bit.  Per step: one CTA does the forward substitution column by
+// column (a barrier per column, rows in parallel -- the same per-row DAG as the row-wise
+// sequential sum), then a grid over the N rows forms xi_l, |xi_l|^2 and a deterministic
+// maxloc (last-block-done), and gathers row l of T.
+#include <cmath>
+
+#include "kernels.h"
+
+namespace rbg {
+
+__device__ __forceinline__ double2 load_q(const double2 *Q, long long ldq_v, bool cplx, int col, long long row) {
+    // complex: element row is vector row; real: element row is half of vector row/2
+    const double2 *c = Q + (long long)col * ldq_v;
+    if (cplx) return c[row];
+    const double2 v = c[row >> 1];
+    return make_double2((row & 1) ? v.y : v.x, 0.0);
+}
+
+// acc - c * x  (CAC rule 9 pattern)
+__device__ __forceinline__ double2 cmsub(double2 acc, double2 c, double2 x) {
+    acc.x = fma(-c.x, x.x, acc.x);
+    acc.x = fma(c.y, x.y, acc.x);
+    acc.y = fma(-c.x, x.y, acc.y);
+    acc.y = fma(-c.y, x.x, acc.y);
+    return acc;
+}
+
+// a / b with den = fma(b.x, b.x, b.y*b.y) (R31)
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+    const double den = fma(b.x, b.x, b.y * b.y);
+    return make_double2(fma(a.x, b.x, a.y * b.y) / den, fma(a.y, b.x, -(a.x * b.y)) / den);
+}
+
+struct EimArgs {
+    const double2 *Q;
+    long long ldq_v;
+    long long N;
+    bool cplx;
+    int k;
+    double2 *Xi;     // k columns of N complex
+    double2 *T;      // k x k row-major, T[a*k + b] = xi_b(p_a)
+    double2 *c;      // k coefficients
+    long long *nodes;
+    double *bm;      // per-block maxloc values
+    long long *bj;   // per-block maxloc rows
+    unsigned *ticket;
+    int *status;     // 0 ok, 1 degenerate (zero residual)
+};
+
+// Forward substitution for step l (l >= 1): c_a for a < l.
+__global__ void __launch_bounds__(1024) k_eim_solve(EimArgs a, int l) {
+    __shared__ double2 cb;
+    // one thread per row a (k <= 1024 enforced on the host); rhs a = q_l(p_a)
+    const int r = threadIdx.x;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < l) v = load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]);
+    for (int b = 0; b < l; b++) {
+        if (r == b) {
+            cb = cdiv(v, a.T[(long long)b * a.k + b]);
+            a.c[b] = cb;
+        }
+        __syncthreads();
+        const double2 cc = cb;
+        if (r > b && r < l) v = cmsub(v, cc, a.T[(long long)r * a.k + b]);
+        __syncthreads();
+    }
+}
+
+// xi_l over all rows + maxloc of |xi_l|^2; the last block sets p_l and row l of T.
+__global__ void __launch_bounds__(256) k_eim_residual(EimArgs a, int l) {
+    __shared__ double s_m[8];
+    __shared__ long long s_j[8];
+    __shared__ int s_last;
+    double bm = -1.0;
+    long long bj = 0x7fffffffffffffffLL;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.N; i += (long long)gridDim.x * blockDim.x) {
+        double2 x = load_q(a.Q, a.ldq_v, a.cplx, l, i);
+        for (int b = 0; b < l; b++) x = cmsub(x, a.c[b], a.Xi[(long long)b * a.N + i]);
+        a.Xi[(long long)l * a.N + i] = x;
+        const double m = fma(x.x, x.x, x.y * x.y);
+        if (m > bm) {  // rows visited in increasing order per thread
+            bm = m;
+            bj = i;
+        }
+    }
+    for (int h = 16; h >= 1; h >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+        const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+        if (rec_better(om, oj, bm, bj)) {
+            bm = om;
+            bj = oj;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_m[threadIdx.x >> 5] = bm;
+        s_j[threadIdx.x >> 5] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; w++)
+            if (rec_better(s_m[w], s_j[w], bm, bj)) {
+                bm = s_m[w];
+                bj = s_j[w];
+            }
+        a.bm[blockIdx.x] = bm;
+        a.bj[blockIdx.x] = bj;
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        bm = -1.0;
+        bj = 0x7fffffffffffffffLL;
+        for (int b = 0; b < (int)gridDim.x; b++) {
+            const double m = __ldcg(&a.bm[b]);
+            const long long j = __ldcg(&a.bj[b]);
+            if (rec_better(m, j, bm, bj)) {
+                bm = m;
+                bj = j;
+            }
+        }
+        *a.ticket = 0u;
+        if (!(bm > 0.0)) {
+            *a.status = 1;
+            bj = 0;
+        }
+        a.nodes[l] = bj;
+        s_j[0] = bj;
+    }
+    __syncthreads();
+    const long long p = s_j[0];
+    for (int b = threadIdx.x; b <= l; b += blockDim.x) a.T[(long long)l * a.k + b] = __ldcg(&a.Xi[(long long)b * a.N + p]);
+}
+
+// B_ab = q_b(p_a), column-major k x k (the EIM node matrix).
+__global__ void k_eim_nodes_matrix(EimArgs a, double2 *B) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)a.k * a.k;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(e % a.k), col = (int)(e / a.k);
+        B[e] = load_q(a.Q, a.ldq_v, a.cplx, col, a.nodes[row]);
+    }
+}
+
+cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
+                    int *status_d, cudaStream_t s) {
+    if (k < 1 || k > 1024) return cudaErrorInvalidValue;
+    const int blocks = (int)((N + 255) / 256 < 148 ? (N + 255) / 256 : 148);
+    EimArgs a{};
+    a.Q = Q;
+    a.ldq_v = ldq_v;
+    a.N = N;
+    a.cplx = cplx;
+    a.k = k;
+    a.nodes = nodes_d;
+    a.status = status_d;
+    cudaError_t e = cudaMalloc(&a.Xi, sizeof(double2) * (size_t)k * N);
+    if (e == cudaSuccess) e = cudaMalloc(&a.T, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = cudaMalloc(&a.c, sizeof(double2) * k);
+    if (e == cudaSuccess) e = cudaMalloc(&a.bm, sizeof(double) * blocks);
+    if (e == cudaSuccess) e = cudaMalloc(&a.bj, sizeof(long long) * blocks);
+    if (e == cudaSuccess) e = cudaMalloc(&a.ticket, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(status_d, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.c, 0, sizeof(double2) * k, s);
+    for (int l = 0; l < k && e == cudaSuccess; l++) {
+        if (l > 0) {
+            k_eim_solve<<<1, 1024, 0, s>>>(a, l);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) {
+            k_eim_residual<<<blocks, 256, 0, s>>>(a, l);
+            e = cudaGetLastError();
+        }
+    }
+    if (e == cudaSuccess) {
+        k_eim_nodes_matrix<<<64, 256, 0, s>>>(a, B_d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(a.Xi);
+    cudaFree(a.T);
+    cudaFree(a.c);
+    cudaFree(a.bm);
+    cudaFree(a.bj);
+    cudaFree(a.ticket);
+    return e;
+}
+
+}  // namespace rbg

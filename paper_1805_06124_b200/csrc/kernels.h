@@ -82,6 +82,10 @@ cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, in
                            const int *order, int kr, double2 *X, long long ldx_v, bool cplx, cudaStream_t s);
 size_t rot_bytes(int kp);
 
+// Greedy EIM nodes (eim.cu): nodes_d[k], B_d = Q(P, :) k x k column-major complex.
+cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
+                    int *status_d, cudaStream_t s);
+
 // First non-finite entry of a device block: writes min(col * N + row) (or -1) to *out.
 cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
                                 long long nvec, bool cplx, unsigned long long *out,

@@ -88,6 +88,7 @@ SYMBOLS = {
     "rbg_add_columns": ([_P, _P, _I64, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_gram": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_reconstruct": ([_P, ctypes.c_double, _I64, ctypes.POINTER(_I64), _P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_eim": ([_P, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_gen_chirp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
 }
 
@@ -371,6 +372,16 @@ class Context:
         _check(lib().rbg_reconstruct(self.h, float(tau2), int(kr_max), ctypes.byref(kr), sigma.ctypes.data,
                                      X.ctypes.data, self.N, 0))
         return sigma[:k], kr.value, X[:kr.value]
+
+    def eim(self):
+        """Greedy EIM nodes of the current basis: (nodes (k,), B = Q(nodes, :) (k, k))."""
+        k = self.info()[0]
+        nodes = np.zeros(max(k, 1), np.int64)
+        buf = np.zeros(max(k, 1) ** 2, np.complex128)
+        if k:
+            _check(lib().rbg_eim(self.h, nodes.ctypes.data, buf.ctypes.data, k, 0))
+        B = buf[:k * k].reshape((k, k), order="F")
+        return nodes[:k], (B if self.cplx else B.real.copy())
 
     def xchg_buffers(self):
         s, r, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()

@@ -8,7 +8,8 @@ After the k-iteration greedy on the device-generated config-2 matrix:
     time, HBM GB/s against MEASURED_PEAKS.json;
   * enrichment step: rbg_add_columns of 4,096 columns (copy + k coefficient passes);
   * Algorithm 4 reconstruction: Gram (FP64 FLOP/s against the derived FP64 peak), Jacobi,
-    X = Q V; total.
+    X = Q V; total;
+  * greedy EIM nodes of the k-vector basis.
 Prints one JSON line.  Timed with CUDA events / wall clock around blocking ABI calls.
 """
 import argparse
@@ -72,6 +73,12 @@ def main():
                               "fp64_peak_TFLOPs_derived": FP64_PEAK_TFLOPS,
                               "total_s": tr, "kr": kr, "sigma_1": float(sigma[0]),
                               "sigma_k": float(sigma[-1])}
+        # ---- f-2 EIM nodes
+        ctx.eim()
+        t0 = time.perf_counter()
+        nodes, B = ctx.eim()
+        out["eim"] = {"s": time.perf_counter() - t0, "k": int(len(nodes)),
+                      "cond_B": float(np.linalg.cond(B))}
         # ---- f-1 enrichment step
         t0 = time.perf_counter()
         ctx.add_columns(V[:4096])
