@@ -143,7 +143,7 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.recs = c->recs;
     a.ticket = c->ticket;
     a.col_offset = c->col_offset;
-    a.send = c->world > 1 ? c->send : nullptr;
+    a.send = c->comm != RBG_COMM_NONE ? c->send : nullptr;
     return a;
 }
 
@@ -168,6 +168,7 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.col_offset = c->col_offset;
     a.M_loc = c->M;
     a.world = c->world;
+    a.xchg = c->comm != RBG_COMM_NONE;
     a.recv = c->recv;
     a.slot_bytes = c->slot;
     return a;
@@ -185,7 +186,7 @@ rbg_status enqueue_local(rbg_ctx *c) {
 }
 
 rbg_status enqueue_xchg(rbg_ctx *c) {
-    if (c->world > 1 && c->comm == RBG_COMM_NCCL) {
+    if (c->comm == RBG_COMM_NCCL) {
         const char *msg = nullptr;
         if (nccl_allgather_bytes(c->send, c->recv, c->slot, c->nccl, c->stream, &msg))
             return fail(RBG_ENCCL, "ncclAllGather: %s", msg ? msg : "?");
@@ -506,7 +507,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(cudaMalloc(&c->ticket, sizeof(unsigned)));
     CUB(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
 
-    if (world > 1) {
+    if (d->comm != RBG_COMM_NONE) {  // (world = 1 runs the same exchange path, e.g. in tests)
         c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;
         CUB(cudaMalloc(&c->send, c->slot));
         CUB(cudaMalloc(&c->recv, c->slot * world));

@@ -220,7 +220,7 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     double m;
     long long J;
     int owner = 0;
-    if (a.world == 1) {
+    if (!a.xchg) {
         m = a.st->m_loc;
         J = a.st->j_loc;
     } else {
@@ -273,7 +273,7 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     }
 
     // ---- a5: Hoffmann IMGS (CAC rule 9) ---------------------------------------------
-    const double2 *src = (a.world == 1)
+    const double2 *src = !a.xchg
                              ? a.S + (J - a.col_offset) * a.ldv
                              : reinterpret_cast<const double2 *>(a.recv + (size_t)owner * a.slot_bytes +
                                                                  sizeof(Rec));

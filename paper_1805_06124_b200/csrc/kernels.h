@@ -47,6 +47,7 @@ struct ImgsArgs {
     double tol;
     long long col_offset, M_loc;
     int world;
+    bool xchg;                  // decision from the exchanged records (any world size)
     const unsigned char *recv;  // world slots of xchg_slot_bytes(nvec)
     size_t slot_bytes;
 };

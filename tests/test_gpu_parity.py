@@ -208,3 +208,25 @@ def test_sharded_path_on_one_gpu(rbg, orc, world):
     np.testing.assert_array_equal(np.concatenate([r.r2 for r in res]), o.r2)
     for c in ctxs:
         c.close()
+
+
+def test_nccl_exchange_path_world1(rbg, orc):
+    """comm = NCCL with one rank runs the whole exchange path on one GPU: libnccl loaded at
+    run time, ncclCommInitRank, the sweep's candidate-column pack, ncclAllGather on the
+    library stream and the decision from the gathered records -- bit-identical results."""
+    S, w, tol, k_max = inputs.config1(M=2500, N=800)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    uid = rbg.unique_id()
+    assert len(uid) == 128
+    with rbg.Context(S, w, tol, k_max, comm=rbg.COMM_NCCL, rank=0, world=1, nccl_id=uid) as ctx:
+        ctx.set_timing(True)
+        ctx.run()
+        compare(ctx.result(), o)
+        st = ctx.stats()
+        assert st.t_xchg_ms > 0.0
+    with rbg.Context(S, w, tol, k_max, comm=rbg.COMM_EXTERNAL, rank=0, world=1) as ctx:
+        for _ in range(k_max + 1):
+            ctx.iter_local()
+            rbg.emulate_allgather([ctx])
+            ctx.iter_finish()
+        compare(ctx.result(), o)
