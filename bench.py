@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--graph-batch", type=int, default=0)
+    p.add_argument("--ortho", default="mgs", choices=["mgs", "cgs"],
+                   help="IMGS variant: the paper's MGSCI (default) or Hoffmann CGSCI")
     return p.parse_args()
 
 
@@ -166,6 +168,7 @@ def config_dict(a, world):
             "rows": a.rows, "cols_per_gpu": a.cols_per_gpu, "cols_global": a.cols_per_gpu * world,
             "k_window": [a.warmup, a.warmup + a.steps], "parallelism": f"column-sharded x{world}",
             "l2": "inputs (65.5 GB/GPU) >> 126 MB L2; no flush",
+            "ortho": getattr(a, "ortho", "mgs"),
             "value_unit": "greedy iterations/s x (cols_global / 409,600) -- plain it/s at 1 GPU"}
 
 
@@ -214,7 +217,7 @@ def run_ours(a):
     stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
     torch.cuda.set_stream(stream)
     ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
-                      world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id)
+                      world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id, ortho=a.ortho)
     ctx.set_timing(True)
     if a.graph_batch:
         ctx.set_graph_batch(a.graph_batch)

@@ -70,6 +70,12 @@ typedef enum { RBG_MEM_HOST = 0, RBG_MEM_DEVICE = 1 } rbg_mem;
  * rbg_iter_finish (used to run the sharded path on one GPU in tests). */
 typedef enum { RBG_COMM_NONE = 0, RBG_COMM_NCCL = 1, RBG_COMM_EXTERNAL = 2 } rbg_comm;
 
+/* Orthogonalisation of each new basis vector: Hoffmann's iterated MODIFIED Gram-Schmidt
+ * ("MGSCI", kappa = 2; the paper's choice) or iterated CLASSICAL
+ * Gram-Schmidt ("CGSCI", kappa = 2; same acceptance test, all coefficients of a pass at once:
+ * 2 grid-wide phases per pass instead of k dependent reductions). */
+typedef enum { RBG_ORTHO_MGS = 0, RBG_ORTHO_CGS = 1 } rbg_ortho;
+
 typedef struct rbg_desc {
     const void *S;        /* N x M_loc snapshot block, column-major                      */
     rbg_mem S_mem;        /* where S lives                                               */
@@ -92,6 +98,7 @@ typedef struct rbg_desc {
     int64_t col_offset;   /* global index of local column 0                              */
     int64_t M_global;     /* total columns over all ranks (0 => M)                       */
     uint8_t nccl_id[128]; /* ncclUniqueId from rbg_get_unique_id on rank 0 (comm = NCCL) */
+    rbg_ortho ortho;      /* orthogonalisation of the pivot column (default MGS)         */
 } rbg_desc;
 
 typedef struct rbg_stats {
@@ -106,7 +113,7 @@ typedef struct rbg_stats {
 } rbg_stats;
 
 /* Fill *d with defaults: ld = 0, borrow = 0, w = NULL, device = -1, check_finite = 1,
- * comm = NONE, rank = 0, world = 1, col_offset = 0, M_global = 0. */
+ * comm = NONE, rank = 0, world = 1, col_offset = 0, M_global = 0, ortho = MGS. */
 void rbg_desc_init(rbg_desc *d);
 
 /* North-star entry point: host S (N x M, ld = N) and host w (NULL => ones).  The matrix

@@ -183,6 +183,64 @@ int orc_imgs(const double *Q, const double *WQ, int64_t ldq, int64_t k,
     return 1;
 }
 
+/*
+ * Iterated CLASSICAL Gram-Schmidt, Hoffmann "CGSCI" with kappa = 2 (the same family and
+ * acceptance test as orc_imgs; DESIGN.md CAC rule 11): per sweep all
+ * coefficients c_i = <q_i, v>_w are taken from the same v, then v <- v - sum_i c_i q_i
+ * (per element, sequentially over i = 1..k).  Lanes L for every dot / norm.
+ */
+int orc_imgs_cgs(const double *Q, const double *WQ, int64_t ldq, int64_t k,
+                 double *v, const double *w, int64_t n, int cplx, int L,
+                 double *q_out, double *wq_out, double *n_out, int *nu_out)
+{
+    const double delta = 1000.0 * 0x1p-52;
+    double *c = (double *)calloc((size_t)(2 * (k > 0 ? k : 1)), sizeof(double));
+    double n0 = sqrt(orc_nrm(v, w, n, cplx, L));
+    double n_prev = n0, nn = 0.0;
+    int nu = 0, accepted = 0;
+    while (nu < ORC_NU_MAX) {
+        nu++;
+        for (int64_t i = 0; i < k; i++) orc_dot(WQ + i * ldq, v, n, cplx, L, &c[2 * i], &c[2 * i + 1]);
+        for (int64_t e = 0; e < n; e++) {
+            if (cplx) {
+                double vr = v[2 * e], vi = v[2 * e + 1];
+                for (int64_t i = 0; i < k; i++) {
+                    const double *q = Q + i * ldq;
+                    double cr = c[2 * i], ci = c[2 * i + 1], qr = q[2 * e], qi = q[2 * e + 1];
+                    vr = fma(-cr, qr, vr);
+                    vr = fma(ci, qi, vr);
+                    vi = fma(-cr, qi, vi);
+                    vi = fma(-ci, qr, vi);
+                }
+                v[2 * e] = vr;
+                v[2 * e + 1] = vi;
+            } else {
+                double x = v[e];
+                for (int64_t i = 0; i < k; i++) x = fma(-c[2 * i], Q[i * ldq + e], x);
+                v[e] = x;
+            }
+        }
+        nn = sqrt(orc_nrm(v, w, n, cplx, L));
+        if (nn > n_prev / ORC_KAPPA) { accepted = 1; break; }
+        n_prev = nn;
+    }
+    free(c);
+    *nu_out = nu;
+    *n_out = nn;
+    if (!accepted || !(nn >= delta * n0) || nn == 0.0) return 0;
+    const int nv = cplx ? 2 : 1;
+    for (int64_t e = 0; e < n * nv; e++) q_out[e] = v[e] / nn;
+    if (cplx) {
+        for (int64_t e = 0; e < n; e++) {
+            wq_out[2 * e] = w[e] * q_out[2 * e];
+            wq_out[2 * e + 1] = w[e] * q_out[2 * e + 1];
+        }
+    } else {
+        for (int64_t e = 0; e < n; e++) wq_out[e] = w[e] * q_out[e];
+    }
+    return 1;
+}
+
 static double now_s(void)
 {
     struct timespec ts;
@@ -210,11 +268,13 @@ static double now_s(void)
  * max_iters >= 0 stops after that many completed iterations with stop = NONE (used to
  * time a bounded sample); pass -1 for no limit.  k0 >= 0 resumes from k0 iterations of
  * state held in the output arrays (enrichment); k0 < 0 starts fresh with sweep 0.
+ * ortho: 0 = Hoffmann MGSCI (orc_imgs, the paper's), 1 = CGSCI (orc_imgs_cgs); L_I is the
+ * lane count of whichever is used.
  * Returns k (basis size) or -1 on bad arguments.
  */
 int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const double *w,
                    int cplx, double tol, int64_t k_max, int L_S, int L_I, int nthreads,
-                   int64_t max_iters, int64_t k0,
+                   int64_t max_iters, int64_t k0, int ortho,
                    int64_t *piv, double *Q, double *WQ, double *R, double *err, int *nu,
                    double *rdiag, double *r2, int *stop_out,
                    double *t_sweep, double *t_imgs, double *t_iter)
@@ -259,8 +319,8 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
         memcpy(v, S + J * lds, sizeof(double) * (size_t)ldq);
         double nrm;
         int nuk;
-        int ok = orc_imgs(Q, WQ, ldq, k, v, w, N, cplx, L_I, Q + k * ldq, WQ + k * ldq,
-                          NULL, &nrm, &nuk);
+        int ok = ortho ? orc_imgs_cgs(Q, WQ, ldq, k, v, w, N, cplx, L_I, Q + k * ldq, WQ + k * ldq, &nrm, &nuk)
+                       : orc_imgs(Q, WQ, ldq, k, v, w, N, cplx, L_I, Q + k * ldq, WQ + k * ldq, NULL, &nrm, &nuk);
         if (t_imgs) t_imgs[k] = now_s() - ti;
         if (!ok) { stop = ORC_STOP_RANK; break; }
         piv[k] = J;

@@ -95,6 +95,9 @@ struct rbg_ctx {
     std::vector<long long> ev_iter;
     int graph_batch = 0;
     cudaGraphExec_t graph = nullptr;
+    rbg_ortho ortho = RBG_ORTHO_MGS;
+    double2 *cgs_v = nullptr, *cgs_c = nullptr;
+    int cgs_grid = 0;
 };
 
 namespace {
@@ -121,6 +124,8 @@ void free_ctx(rbg_ctx *c) {
     cudaFree(c->ticket);
     cudaFree(c->send);
     cudaFree(c->recv);
+    cudaFree(c->cgs_v);
+    cudaFree(c->cgs_c);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -195,7 +200,10 @@ rbg_status enqueue_xchg(rbg_ctx *c) {
 }
 
 rbg_status enqueue_finish(rbg_ctx *c) {
-    CU(launch_imgs(imgs_args(c), c->cplx, c->stream));
+    if (c->ortho == RBG_ORTHO_CGS)
+        CU(launch_imgs_cgs(imgs_args(c), c->cplx, c->cgs_v, c->cgs_c, c->cgs_grid, c->stream));
+    else
+        CU(launch_imgs(imgs_args(c), c->cplx, c->stream));
     return RBG_OK;
 }
 
@@ -352,6 +360,7 @@ void rbg_desc_init(rbg_desc *d) {
     d->check_finite = 1;
     d->comm = RBG_COMM_NONE;
     d->world = 1;
+    d->ortho = RBG_ORTHO_MGS;
 }
 
 const char *rbg_last_error(void) { return g_err.c_str(); }
@@ -390,6 +399,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     if (d->k_max < 1 || d->k_max > d->N)
         return fail(RBG_EINVAL, "k_max=%lld outside [1, N=%lld]", (long long)d->k_max, (long long)d->N);
     if (world > 1 && d->comm == RBG_COMM_NONE) return fail(RBG_EINVAL, "world > 1 needs comm NCCL or EXTERNAL");
+    if (d->ortho != RBG_ORTHO_MGS && d->ortho != RBG_ORTHO_CGS) return fail(RBG_EINVAL, "unknown ortho %d", (int)d->ortho);
     const bool cplx = d->dtype == RBG_COMPLEX_F64;
     const long long nvec = cplx ? d->N : (d->N + 1) / 2;
     if (imgs_maxv(nvec) == 0) return fail(RBG_EINVAL, "N=%lld exceeds the IMGS register tile (max %d vectors)", (long long)d->N, 16 * kLaneImgs);
@@ -500,6 +510,12 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(cudaMalloc(&c->piv, sizeof(long long) * c->k_max));
     CUB(cudaMalloc(&c->nu, sizeof(int) * c->k_max));
     CUB(cudaMemsetAsync(c->nu, 0, sizeof(int) * c->k_max, c->stream));
+    c->ortho = d->ortho;
+    if (c->ortho == RBG_ORTHO_CGS) {
+        CUB(cudaMalloc(&c->cgs_v, (size_t)nvec * 16));
+        CUB(cudaMalloc(&c->cgs_c, sizeof(double2) * (size_t)c->k_max));
+        c->cgs_grid = cgs_grid(c->num_sms);
+    }
     c->cfg_init = sweep_config(cplx, true, nvec, c->num_sms, c->device);
     c->cfg_sweep = sweep_config(cplx, false, nvec, c->num_sms, c->device);
     const int max_grid = std::max(c->cfg_init.grid, c->cfg_sweep.grid);

@@ -63,6 +63,9 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
 cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepConfig &cfg,
                          cudaStream_t s);
 int imgs_maxv(long long nvec);  // 0 if unsupported
+// Hoffmann CGSCI variant (imgs_cgs.cu): cooperative grid, vbuf nvec vectors, cbuf k_max.
+int cgs_grid(int num_sms);
+cudaError_t launch_imgs_cgs(const ImgsArgs &a, bool cplx, double2 *vbuf, double2 *cbuf, int grid, cudaStream_t s);
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s);
 // Deterministic maxloc of r2[0..M) (value desc, index asc) into st->m_loc / st->j_loc.
 cudaError_t launch_maxloc(const double *r2, long long M, long long col_offset, DevState *st,

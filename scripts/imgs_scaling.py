@@ -13,13 +13,14 @@ from paper_1805_06124_b200 import inputs, rbg  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 40960
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+ORTHO = sys.argv[3] if len(sys.argv) > 3 else "mgs"
 N = 10000
 t = inputs.chirp_grid(N)
 w = inputs.simpson_weights(N)
 q, chi, psi = inputs.chirp_params(M, 2, spin=True)
 S = torch.empty((M, N), dtype=torch.complex128, device="cuda")
 rbg.gen_chirp(S, t, w, q, chi, psi, spin=True)
-ctx = rbg.Context(S, w, 0.0, K)
+ctx = rbg.Context(S, w, 0.0, K, ortho=ORTHO)
 ctx.set_timing(True)
 ctx.run()
 k = ctx.info()[0]

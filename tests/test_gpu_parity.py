@@ -230,3 +230,27 @@ def test_nccl_exchange_path_world1(rbg, orc):
             rbg.emulate_allgather([ctx])
             ctx.iter_finish()
         compare(ctx.result(), o)
+
+
+@pytest.mark.parametrize("case", ["cfg0", "cfg1", "cfg2", "cfg4", "ragged_real", "ragged_cplx"])
+def test_cgs_variant_parity(rbg, orc, case):
+    """Hoffmann CGSCI orthogonalisation (rbg_desc.ortho = CGS) against the oracle's CGS mode
+    (lanes (32, 256)): bit for bit."""
+    rng = np.random.default_rng(77)
+    if case == "cfg0":
+        S, w, tol, k_max = inputs.config0()
+    elif case == "cfg1":
+        S, w, tol, k_max = inputs.config1(M=3000, N=2000)
+    elif case == "cfg2":
+        S, w, tol, k_max = inputs.config2(M=2000, N=10000)
+        k_max = 60
+    elif case == "cfg4":
+        S, w, tol, k_max, _ = inputs.config4(M=4096, N=1024, r=256)
+    elif case == "ragged_real":
+        S, w, tol, k_max = rng.standard_normal((300, 257)), rng.uniform(0.5, 1.5, 257), 0.0, 40
+    else:
+        S = rng.standard_normal((200, 4097)) + 1j * rng.standard_normal((200, 4097))
+        w, tol, k_max = rng.uniform(0.5, 1.5, 4097), 0.0, 40
+    g = rbg.greedy(S, w, tol, k_max, ortho="cgs")
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL_CGS, ortho="cgs")
+    compare(g, o)

@@ -353,3 +353,31 @@ def test_canonical_vs_plain_agree_while_separated(orc):
     # ... and the squared residuals (the recurrence's own variable) to ~1e4 eps * max ||s||^2
     np.testing.assert_allclose(a.errors[:d] ** 2, b.errors[:d] ** 2, rtol=0,
                                atol=1e-12 * a.errors[0] ** 2)
+
+
+# ---------------------------------------------------------------- CGSCI variant
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_cgs_variant_equivalence_and_orthogonality(orc, cplx):
+    """Iterated classical GS gives the same pivots as LAPACK xGEQP3 / Algorithm 2 on
+    separated inputs, |diag R| = err_k, and an orthonormal basis."""
+    rng = np.random.default_rng(200)
+    N, M, K = 30, 80, 20
+    S = rand_matrix(rng, N, M, cplx)
+    w = rng.uniform(0.5, 1.5, N)
+    r = orc.greedy(S, w, 0.0, K, lanes=orc.CANONICAL_CGS, ortho="cgs")
+    St = brute.weighted(S, w)
+    Ql, Rl, P = scipy.linalg.qr(St, pivoting=True, mode="economic")
+    np.testing.assert_array_equal(r.pivots, P[:K])
+    np.testing.assert_allclose(r.errors[:K], np.abs(np.diag(Rl))[:K], rtol=1e-12)
+    G = (r.Q.conj() * w[None, :]) @ r.Q.T
+    assert np.max(np.abs(G - np.eye(K))) <= 1e-13
+
+
+def test_cgs_variant_closed_forms_and_rank(orc):
+    r = orc.greedy(np.eye(3), np.ones(3), 0.0, 3, lanes=orc.CANONICAL_CGS, ortho="cgs")
+    assert list(r.pivots) == [0, 1, 2] and list(r.errors) == [1.0, 1.0, 1.0, 0.0]
+    rng = np.random.default_rng(201)
+    S = rand_matrix(rng, 50, 90, True, rank=9)
+    res = orc.greedy(S, np.ones(50), 0.0, 50, lanes=orc.CANONICAL_CGS, ortho="cgs")
+    assert res.k == 9 and res.stop == "RANK"
