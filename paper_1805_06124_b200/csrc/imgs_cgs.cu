@@ -40,42 +40,87 @@ __device__ __forceinline__ double2 cta_sum256(double re, double im, double2 *s_w
     return make_double2(x, y);
 }
 
+// x - c q (CAC rule 9 pattern; real: both components by the real c)
+template <bool CPLX>
+__device__ __forceinline__ double2 cgs_msub(double2 x, double2 c, double2 q) {
+    if (CPLX) {
+        x.x = fma(-c.x, q.x, x.x);
+        x.x = fma(c.y, q.y, x.x);
+        x.y = fma(-c.x, q.y, x.y);
+        x.y = fma(-c.y, q.x, x.y);
+    } else {
+        x.x = fma(-c.x, q.x, x.x);
+        x.y = fma(-c.x, q.y, x.y);
+    }
+    return x;
+}
+
+template <bool CPLX>
+__device__ __forceinline__ void nrm_acc(double &acc, double2 x, double2 wv) {
+    // wv = (w_u, w_u) complex, (w_2u, w_2u+1) real -- CAC rule 4
+    double t = wv.x * x.x;
+    acc = fma(t, x.x, acc);
+    t = wv.y * x.y;
+    acc = fma(t, x.y, acc);
+}
+
+template <bool CPLX>
+__device__ __forceinline__ double2 wvec(const double *w, long long u) {
+    if (CPLX) {
+        const double wu = w[u];
+        return make_double2(wu, wu);
+    }
+    return reinterpret_cast<const double2 *>(w)[u];
+}
+
 template <bool CPLX>
 __device__ double nrm256(const double2 *v, const double *w, long long nvec, double2 *s_w) {
+    constexpr int U = 8;  // independent loads in flight ahead of the sequential chain
     double acc = 0.0;
-    for (long long u = threadIdx.x; u < nvec; u += kCgsThreads) {  // CAC rule 4
-        const double2 x = v[u];
-        if (CPLX) {
-            const double wu = w[u];
-            double t = wu * x.x;
-            acc = fma(t, x.x, acc);
-            t = wu * x.y;
-            acc = fma(t, x.y, acc);
-        } else {
-            double t = w[2 * u] * x.x;
-            acc = fma(t, x.x, acc);
-            t = w[2 * u + 1] * x.y;
-            acc = fma(t, x.y, acc);
+    long long u = threadIdx.x;
+    for (; u + (U - 1) * kCgsThreads < nvec; u += U * kCgsThreads) {
+        double2 x[U], wv[U];
+#pragma unroll
+        for (int t = 0; t < U; t++) {
+            x[t] = v[u + t * kCgsThreads];
+            wv[t] = wvec<CPLX>(w, u + t * kCgsThreads);
         }
+#pragma unroll
+        for (int t = 0; t < U; t++) nrm_acc<CPLX>(acc, x[t], wv[t]);
     }
+    for (; u < nvec; u += kCgsThreads) nrm_acc<CPLX>(acc, v[u], wvec<CPLX>(w, u));
     return cta_sum256(acc, 0.0, s_w).x;
 }
 
 template <bool CPLX>
-__device__ double2 dot256(const double2 *wq, const double2 *v, long long nvec, double2 *s_w) {
-    double pr = 0.0, pi = 0.0;
-    for (long long u = threadIdx.x; u < nvec; u += kCgsThreads) {  // CAC rule 2
-        const double2 e = wq[u], x = v[u];
-        if (CPLX) {
-            pr = fma(e.x, x.x, pr);
-            pr = fma(e.y, x.y, pr);
-            pi = fma(e.x, x.y, pi);
-            pi = fma(-e.y, x.x, pi);
-        } else {
-            pr = fma(e.x, x.x, pr);
-            pr = fma(e.y, x.y, pr);
-        }
+__device__ __forceinline__ void dot_acc(double &pr, double &pi, double2 e, double2 x) {
+    if (CPLX) {
+        pr = fma(e.x, x.x, pr);
+        pr = fma(e.y, x.y, pr);
+        pi = fma(e.x, x.y, pi);
+        pi = fma(-e.y, x.x, pi);
+    } else {
+        pr = fma(e.x, x.x, pr);
+        pr = fma(e.y, x.y, pr);
     }
+}
+
+template <bool CPLX>
+__device__ double2 dot256(const double2 *wq, const double2 *v, long long nvec, double2 *s_w) {
+    constexpr int U = 8;  // independent 16-byte loads in flight per operand
+    double pr = 0.0, pi = 0.0;
+    long long u = threadIdx.x;
+    for (; u + (U - 1) * kCgsThreads < nvec; u += U * kCgsThreads) {  // CAC rule 2, in order
+        double2 e[U], x[U];
+#pragma unroll
+        for (int t = 0; t < U; t++) {
+            e[t] = wq[u + t * kCgsThreads];
+            x[t] = v[u + t * kCgsThreads];
+        }
+#pragma unroll
+        for (int t = 0; t < U; t++) dot_acc<CPLX>(pr, pi, e[t], x[t]);
+    }
+    for (; u < nvec; u += kCgsThreads) dot_acc<CPLX>(pr, pi, wq[u], v[u]);
     return cta_sum256(pr, pi, s_w);
 }
 
@@ -146,18 +191,16 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
         // v <- v - Q c, each element sequentially over i
         for (long long u = gtid; u < nvec; u += nthr) {
             double2 x = vbuf[u];
-            for (long long i = 0; i < k; i++) {
-                const double2 c = cbuf[i], q = a.Q[i * a.ldq_v + u];
-                if (CPLX) {
-                    x.x = fma(-c.x, q.x, x.x);
-                    x.x = fma(c.y, q.y, x.x);
-                    x.y = fma(-c.x, q.y, x.y);
-                    x.y = fma(-c.y, q.x, x.y);
-                } else {
-                    x.x = fma(-c.x, q.x, x.x);
-                    x.y = fma(-c.x, q.y, x.y);
-                }
+            constexpr int U = 16;  // basis loads in flight ahead of the sequential fma chain
+            long long i = 0;
+            for (; i + U <= k; i += U) {
+                double2 q[U];
+#pragma unroll
+                for (int t = 0; t < U; t++) q[t] = a.Q[(i + t) * a.ldq_v + u];
+#pragma unroll
+                for (int t = 0; t < U; t++) x = cgs_msub<CPLX>(x, cbuf[i + t], q[t]);
             }
+            for (; i < k; i++) x = cgs_msub<CPLX>(x, cbuf[i], a.Q[i * a.ldq_v + u]);
             vbuf[u] = x;
         }
         grid.sync();
@@ -199,11 +242,16 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
 }
 
 int cgs_grid(int num_sms) {
+    // one CTA per SM (measured: grid barriers over 592 CTAs cost more than the extra waves)
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_imgs_cgs<true>, kCgsThreads, 0) != cudaSuccess)
         return num_sms;
-    int g = per_sm * num_sms;
-    return g > num_sms ? num_sms : (g < 1 ? 1 : g);
+    int p2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_imgs_cgs<false>, kCgsThreads, 0) == cudaSuccess && p2 < per_sm)
+        per_sm = p2;
+    if (per_sm > 1) per_sm = 1;  // one CTA per SM: the cheapest grid barrier
+    const int g = per_sm * num_sms;
+    return g < 1 ? 1 : g;
 }
 
 cudaError_t launch_imgs_cgs(const ImgsArgs &a, bool cplx, double2 *vbuf, double2 *cbuf, int grid, cudaStream_t s) {
