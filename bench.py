@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--graph-batch", type=int, default=0)
     p.add_argument("--ortho", default="mgs", choices=["mgs", "cgs"],
                    help="IMGS variant: the paper's MGSCI (default) or Hoffmann CGSCI")
+    p.add_argument("--residual", default="recurrence", choices=["recurrence", "explicit"],
+                   help="column residuals: the paper's recurrence (default) or Algorithm 2 updates")
     return p.parse_args()
 
 
@@ -168,7 +170,7 @@ def config_dict(a, world):
             "rows": a.rows, "cols_per_gpu": a.cols_per_gpu, "cols_global": a.cols_per_gpu * world,
             "k_window": [a.warmup, a.warmup + a.steps], "parallelism": f"column-sharded x{world}",
             "l2": "inputs (65.5 GB/GPU) >> 126 MB L2; no flush",
-            "ortho": getattr(a, "ortho", "mgs"),
+            "ortho": getattr(a, "ortho", "mgs"), "residual": getattr(a, "residual", "recurrence"),
             "value_unit": "greedy iterations/s x (cols_global / 409,600) -- plain it/s at 1 GPU"}
 
 
@@ -217,7 +219,8 @@ def run_ours(a):
     stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
     torch.cuda.set_stream(stream)
     ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
-                      world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id, ortho=a.ortho)
+                      world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id, ortho=a.ortho,
+                      residual=a.residual)
     ctx.set_timing(True)
     if a.graph_batch:
         ctx.set_graph_batch(a.graph_batch)
@@ -254,6 +257,8 @@ def run_ours(a):
     it_s = K / (ms / 1e3)
     value = it_s * (M_glob / M_PER_GPU)
     bytes_sweep = N * M_loc * 16 + M_loc * (8 + 8 + 16)      # DESIGN.md "Roofline" per launch
+    if a.residual == "explicit":
+        bytes_sweep += 2 * N * M_loc * 16                     # + re-read and write-back of V
     sweep_avg_s = float(np.mean(sw)) / 1e3
     achieved = bytes_sweep / sweep_avg_s / 1e9
     pk = peaks()

@@ -76,6 +76,14 @@ typedef enum { RBG_COMM_NONE = 0, RBG_COMM_NCCL = 1, RBG_COMM_EXTERNAL = 2 } rbg
  * 2 grid-wide phases per pass instead of k dependent reductions). */
 typedef enum { RBG_ORTHO_MGS = 0, RBG_ORTHO_CGS = 1 } rbg_ortho;
 
+/* Column residuals: RECURRENCE = the paper's Eq. (Residual), r2_j <- r2_j - |c_kj|^2 with one
+ * read of S per iteration (accuracy floor ~sqrt(eps) max||s||, reading R8);
+ * EXPLICIT = Algorithm 2's in-place column updates v_j <- v_j - c_kj q_k with r2_j recomputed
+ * from the updated column: floor ~eps max||s||, a read and a write of the
+ * (library-owned, W^{1/2}-scaled) columns per iteration.  NEXT-row calls (validate, add_columns,
+ * gram, reconstruct, eim) need RECURRENCE.  (DESIGN.md CAC rule 12.)          */
+typedef enum { RBG_RESIDUAL_RECURRENCE = 0, RBG_RESIDUAL_EXPLICIT = 1 } rbg_residual;
+
 typedef struct rbg_desc {
     const void *S;        /* N x M_loc snapshot block, column-major                      */
     rbg_mem S_mem;        /* where S lives                                               */
@@ -99,6 +107,7 @@ typedef struct rbg_desc {
     int64_t M_global;     /* total columns over all ranks (0 => M)                       */
     uint8_t nccl_id[128]; /* ncclUniqueId from rbg_get_unique_id on rank 0 (comm = NCCL) */
     rbg_ortho ortho;      /* orthogonalisation of the pivot column (default MGS)         */
+    rbg_residual residual;/* how the column residuals are kept (default RECURRENCE)       */
 } rbg_desc;
 
 typedef struct rbg_stats {
@@ -113,7 +122,8 @@ typedef struct rbg_stats {
 } rbg_stats;
 
 /* Fill *d with defaults: ld = 0, borrow = 0, w = NULL, device = -1, check_finite = 1,
- * comm = NONE, rank = 0, world = 1, col_offset = 0, M_global = 0, ortho = MGS. */
+ * comm = NONE, rank = 0, world = 1, col_offset = 0, M_global = 0, ortho = MGS,
+ * residual = RECURRENCE. */
 void rbg_desc_init(rbg_desc *d);
 
 /* North-star entry point: host S (N x M, ld = N) and host w (NULL => ones).  The matrix

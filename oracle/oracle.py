@@ -74,7 +74,7 @@ def lib():
                                d, d, d, d, ctypes.POINTER(ctypes.c_int)]
         L.orc_imgs.restype = ctypes.c_int
         L.orc_greedy.argtypes = [d, i64, i64, i64, d, ctypes.c_int, ctypes.c_double, i64,
-                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, i64, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, i64, ctypes.c_int, ctypes.c_int,
                                  ctypes.POINTER(i64), d, d, d, d,
                                  ctypes.POINTER(ctypes.c_int), d, d,
                                  ctypes.POINTER(ctypes.c_int), d, d, d]
@@ -165,12 +165,13 @@ class GreedyResult:
 def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
            lanes: tuple[int, int] = CANONICAL, threads: int = 0,
            max_iters: int = -1, resume: "GreedyResult | None" = None,
-           ortho: str = "mgs") -> GreedyResult:
+           ortho: str = "mgs", residual: str = "recurrence") -> GreedyResult:
     """RB-greedy (Algorithm 3) on S given as an (M, N) C-order array (column-major N x M).
 
     ``lanes=(L_S, L_I)``; ``threads=0`` lets OpenMP choose.  ``resume`` continues from a
     previous state whose R / r2 already cover all M columns (enrichment).  ``ortho="cgs"``
     uses Hoffmann's iterated classical GS (pass lanes=CANONICAL_CGS for GPU parity).
+    ``residual="explicit"`` keeps Algorithm 2's explicitly updated columns (CAC rule 12).
     """
     Sf, cplx = _flat(S)
     M, N = S.shape
@@ -188,6 +189,7 @@ def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
     r2 = np.zeros(M)
     k0 = -1
     if resume is not None:
+        assert residual == "recurrence"
         k0 = resume.k
         assert resume.R.shape == (k0, M) and resume.r2.shape == (M,)
         piv[:k0] = resume.pivots
@@ -204,7 +206,7 @@ def greedy(S: np.ndarray, w: np.ndarray, tol: float, k_max: int,
     tt = np.zeros(k_max)
     k = lib().orc_greedy(
         _p(Sf), N, M, N * nv, _p(w), cplx, float(tol), int(k_max), lanes[0], lanes[1],
-        threads, int(max_iters), int(k0), 1 if ortho == "cgs" else 0,
+        threads, int(max_iters), int(k0), 1 if ortho == "cgs" else 0, 1 if residual == "explicit" else 0,
         piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _p(Q.view(np.float64)),
         _p(WQ.view(np.float64)), _p(R.view(np.float64)), _p(err),
         nu.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _p(rdiag), _p(r2),

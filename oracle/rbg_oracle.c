@@ -274,7 +274,7 @@ static double now_s(void)
  */
 int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const double *w,
                    int cplx, double tol, int64_t k_max, int L_S, int L_I, int nthreads,
-                   int64_t max_iters, int64_t k0, int ortho,
+                   int64_t max_iters, int64_t k0, int ortho, int explicit_mode,
                    int64_t *piv, double *Q, double *WQ, double *R, double *err, int *nu,
                    double *rdiag, double *r2, int *stop_out,
                    double *t_sweep, double *t_imgs, double *t_iter)
@@ -288,6 +288,25 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
     (void)nthreads;
 #endif
     double *v = (double *)malloc(sizeof(double) * (size_t)ldq);
+    /* explicit residuals (Algorithm 2 in-place updates; DESIGN.md CAC rule
+     * 12): work on V = W^{1/2} S (sqrt(w_i) rounded once) with unit weights; the basis handed
+     * back is Q = Q~ / W^{1/2}. */
+    const double *w_true = w;
+    double *V = NULL, *ones = NULL;
+    if (explicit_mode) {
+        V = (double *)malloc(sizeof(double) * (size_t)(ldq * M));
+        ones = (double *)malloc(sizeof(double) * (size_t)N);
+        for (int64_t i = 0; i < N; i++) ones[i] = 1.0;
+        for (int64_t j = 0; j < M; j++)
+            for (int64_t i = 0; i < N; i++) {
+                double r = sqrt(w[i]);
+                V[j * ldq + i * nv] = r * S[j * lds + i * nv];
+                if (cplx) V[j * ldq + i * nv + 1] = r * S[j * lds + i * nv + 1];
+            }
+        S = V;
+        lds = ldq;
+        w = ones;
+    }
 
     int64_t k = 0;
     if (k0 >= 0) {
@@ -339,12 +358,43 @@ int64_t orc_greedy(const double *S, int64_t N, int64_t M, int64_t lds, const dou
             orc_dot(wq, S + j * lds, N, cplx, L_S, &cr, &ci);
             Rrow[j * nv] = cr;
             if (cplx) Rrow[j * nv + 1] = ci;
-            if (r2[j] != -INFINITY) r2[j] = r2[j] - abs2(cr, ci, cplx);
+            if (r2[j] == -INFINITY) continue;
+            if (!explicit_mode) {
+                r2[j] = r2[j] - abs2(cr, ci, cplx);
+            } else {
+                /* v_j <- v_j - c q~_k (CAC rule 9 pattern), then r2_j = ||v_j||^2 */
+                double *vj = V + j * lds;
+                const double *q = Q + (k - 1) * ldq;
+                if (cplx) {
+                    for (int64_t e = 0; e < N; e++) {
+                        double xr = vj[2 * e], xi = vj[2 * e + 1];
+                        xr = fma(-cr, q[2 * e], xr);
+                        xr = fma(ci, q[2 * e + 1], xr);
+                        xi = fma(-cr, q[2 * e + 1], xi);
+                        xi = fma(-ci, q[2 * e], xi);
+                        vj[2 * e] = xr;
+                        vj[2 * e + 1] = xi;
+                    }
+                } else {
+                    for (int64_t e = 0; e < N; e++) vj[e] = fma(-cr, q[e], vj[e]);
+                }
+                r2[j] = orc_nrm(vj, w, N, cplx, L_S);
+            }
         }
         if (t_sweep) t_sweep[k - 1] = now_s() - ts;
         if (t_iter) t_iter[k - 1] = now_s() - t_it;
     }
     free(v);
+    if (explicit_mode) {
+        for (int64_t i = 0; i < k; i++)
+            for (int64_t e = 0; e < N; e++) {
+                double r = sqrt(w_true[e]);
+                Q[i * ldq + e * nv] = Q[i * ldq + e * nv] / r;
+                if (cplx) Q[i * ldq + e * nv + 1] = Q[i * ldq + e * nv + 1] / r;
+            }
+        free(V);
+        free(ones);
+    }
     *stop_out = stop;
     return k;
 }

@@ -96,6 +96,8 @@ struct rbg_ctx {
     int graph_batch = 0;
     cudaGraphExec_t graph = nullptr;
     rbg_ortho ortho = RBG_ORTHO_MGS;
+    bool xmode = false;          // explicit residuals (Algorithm 2 updates)
+    double *w_true = nullptr;    // explicit mode: the caller's weights (w holds ones)
     double2 *cgs_v = nullptr, *cgs_c = nullptr;
     int cgs_grid = 0;
 };
@@ -125,6 +127,7 @@ void free_ctx(rbg_ctx *c) {
     cudaFree(c->send);
     cudaFree(c->recv);
     cudaFree(c->cgs_v);
+    cudaFree(c->w_true);
     cudaFree(c->cgs_c);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -143,6 +146,7 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.R = c->R;
     a.ldr = c->M;
     a.qi = -1;
+    a.V = c->xmode ? c->S : nullptr;
     a.r2 = c->r2;
     a.st = c->st;
     a.recs = c->recs;
@@ -361,6 +365,7 @@ void rbg_desc_init(rbg_desc *d) {
     d->comm = RBG_COMM_NONE;
     d->world = 1;
     d->ortho = RBG_ORTHO_MGS;
+    d->residual = RBG_RESIDUAL_RECURRENCE;
 }
 
 const char *rbg_last_error(void) { return g_err.c_str(); }
@@ -400,6 +405,8 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         return fail(RBG_EINVAL, "k_max=%lld outside [1, N=%lld]", (long long)d->k_max, (long long)d->N);
     if (world > 1 && d->comm == RBG_COMM_NONE) return fail(RBG_EINVAL, "world > 1 needs comm NCCL or EXTERNAL");
     if (d->ortho != RBG_ORTHO_MGS && d->ortho != RBG_ORTHO_CGS) return fail(RBG_EINVAL, "unknown ortho %d", (int)d->ortho);
+    if (d->residual != RBG_RESIDUAL_RECURRENCE && d->residual != RBG_RESIDUAL_EXPLICIT)
+        return fail(RBG_EINVAL, "unknown residual mode %d", (int)d->residual);
     const bool cplx = d->dtype == RBG_COMPLEX_F64;
     const long long nvec = cplx ? d->N : (d->N + 1) / 2;
     if (imgs_maxv(nvec) == 0) return fail(RBG_EINVAL, "N=%lld exceeds the IMGS register tile (max %d vectors)", (long long)d->N, 16 * kLaneImgs);
@@ -492,6 +499,23 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     // weights (zero padded), basis, coefficients, state
     std::vector<double> wpad(2 * nvec + 2, 0.0);
     std::memcpy(wpad.data(), wh.data(), sizeof(double) * d->N);
+    c->xmode = d->residual == RBG_RESIDUAL_EXPLICIT;
+    if (c->xmode) {
+        // the kernels see V = W^{1/2} S with unit weights; w_true keeps the caller's weights
+        CUB(cudaMalloc(&c->w_true, sizeof(double) * wpad.size()));
+        CUB(cudaMemcpyAsync(c->w_true, wpad.data(), sizeof(double) * wpad.size(), cudaMemcpyHostToDevice, c->stream));
+        double2 *V = nullptr;
+        if (c->own_S) V = c->S;                               // scale the private copy in place
+        else CUB(cudaMalloc(&V, (size_t)nvec * 16 * c->M));
+        CUB(launch_scale_sqrtw(V, nvec, c->S, c->ldv, c->M, nvec, c->N, c->w_true, cplx, c->stream));
+        c->S = V;
+        c->own_S = true;
+        c->ldv = nvec;
+        CUB(cudaStreamSynchronize(c->stream));
+        std::vector<double> ones(2 * nvec + 2, 0.0);
+        for (long long i = 0; i < d->N; i++) ones[i] = 1.0;
+        wpad.swap(ones);
+    }
     CUB(cudaMalloc(&c->w, sizeof(double) * wpad.size()));
     CUB(cudaMemcpyAsync(c->w, wpad.data(), sizeof(double) * wpad.size(), cudaMemcpyHostToDevice, c->stream));
     const size_t qbytes = (size_t)c->k_max * nvec * 16;
@@ -646,9 +670,23 @@ rbg_status rbg_get_basis(rbg_ctx *c, void *out, int64_t ldq, int on_device) {
     if (!out || ldq < c->N) return fail(RBG_EINVAL, "null output or ldq < N");
     DevState h;
     TRY(read_state(c, &h));
-    if (h.k)
-        CU(cudaMemcpy2D(out, (size_t)ldq * c->se, c->Q, (size_t)c->ldq_v * 16, (size_t)c->N * c->se, h.k,
-                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    if (!h.k) return RBG_OK;
+    const double2 *src = c->Q;
+    double2 *tmp = nullptr;
+    if (c->xmode) {  // Q = Q~ / W^{1/2}: the W-orthonormal basis of S
+        CU(cudaMalloc(&tmp, (size_t)h.k * c->ldq_v * 16));
+        cudaError_t e = launch_unscale_sqrtw(tmp, c->Q, h.k, c->ldq_v, c->w_true, c->cplx, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) {
+            cudaFree(tmp);
+            return fail(RBG_ECUDA, "basis unscale: %s", cudaGetErrorString(e));
+        }
+        src = tmp;
+    }
+    cudaError_t e = cudaMemcpy2D(out, (size_t)ldq * c->se, src, (size_t)c->ldq_v * 16, (size_t)c->N * c->se, h.k,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(RBG_ECUDA, "get_basis: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
 
@@ -786,6 +824,7 @@ rbg_status rbg_emulate_allgather(rbg_ctx **ctxs, int world) {
 rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg_mem V_mem, double *err, void *C,
                         int64_t ldc, int out_on_device) {
     TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
     if (C && ldc < M_v) return fail(RBG_EINVAL, "ldc < M_v");
     if (c->local_pending) return fail(RBG_ESTATE, "validate inside an EXTERNAL iteration");
     DevState h;
@@ -819,6 +858,7 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
 
 rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem) {
     TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
     if (c->world != 1 || c->comm != RBG_COMM_NONE) return fail(RBG_ESTATE, "add_columns needs a single-GPU context");
     DevState h;
     TRY(read_state(c, &h));
@@ -912,6 +952,7 @@ rbg_status gram_device(rbg_ctx *c, int k, int kp, double2 *G) {
 
 rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
     if (c->world != 1) return fail(RBG_ESTATE, "gram needs a single-GPU context");
     DevState h;
     TRY(read_state(c, &h));
@@ -934,6 +975,7 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
 rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_out, double *sigma, void *X,
                            int64_t ldx, int on_device) {
     TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
     if (c->world != 1) return fail(RBG_ESTATE, "reconstruct needs a single-GPU context");
     if (!(tau2 >= 0.0) || kr_max < 0) return fail(RBG_EINVAL, "tau2 < 0 or kr_max < 0");
     if (X && ldx < c->N) return fail(RBG_EINVAL, "ldx < N");
@@ -997,6 +1039,7 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
 
 rbg_status rbg_eim(rbg_ctx *c, int64_t *nodes, void *B, int64_t ldb, int on_device) {
     TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
     DevState h;
     TRY(read_state(c, &h));
     const int k = (int)h.k;

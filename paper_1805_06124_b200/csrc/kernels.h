@@ -21,6 +21,7 @@ struct SweepArgs {
     double *R;             // k_max rows of ldr elements (16 B complex / 8 B real), row-major
     long long ldr;         // R row stride in elements (>= M)
     long long qi;          // >= 0: use basis vector qi and R row qi (validation); -1: q_{k-1}
+    double2 *V;            // explicit mode: the columns updated in place (== S), else NULL
     double *r2;            // M
     DevState *st;
     Rec *recs;             // one record per CTA
@@ -67,6 +68,11 @@ int imgs_maxv(long long nvec);  // 0 if unsupported
 int cgs_grid(int num_sms);
 cudaError_t launch_imgs_cgs(const ImgsArgs &a, bool cplx, double2 *vbuf, double2 *cbuf, int grid, cudaStream_t s);
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s);
+// Explicit mode: V = W^{1/2} S and Q = Q~ / W^{1/2} (sweep.cu).
+cudaError_t launch_scale_sqrtw(double2 *V, long long ldv, const double2 *S, long long lds, long long M, long long nvec,
+                               long long N, const double *w, bool cplx, cudaStream_t s);
+cudaError_t launch_unscale_sqrtw(double2 *Q, const double2 *Qt, long long k, long long nvec, const double *w, bool cplx,
+                                 cudaStream_t s);
 // Deterministic maxloc of r2[0..M) (value desc, index asc) into st->m_loc / st->j_loc.
 cudaError_t launch_maxloc(const double *r2, long long M, long long col_offset, DevState *st,
                           cudaStream_t s);

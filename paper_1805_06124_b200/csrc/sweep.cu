@@ -156,6 +156,54 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
         if (INIT) {
             r2n = re;
             if (lane == 0) a.r2[c] = r2n;
+        } else if (a.V) {
+            // explicit residuals (Algorithm 2, DESIGN.md CAC rule 12): v_j <- v_j - c q~_k in
+            // place and r2_j = ||v_j||^2 recomputed from the updated column (second pass)
+            const double old = a.r2[c];
+            if (lane == 0) {
+                if (CPLX) reinterpret_cast<double2 *>(a.R)[(k - 1) * a.ldr + c] = make_double2(re, im);
+                else a.R[(k - 1) * a.ldr + c] = re;
+            }
+            r2n = old;
+            if (old != -INFINITY) {
+                double2 *vcol = a.V + c * a.ldv;
+                double acc = 0.0;
+                for (long long base = 0; base < nvec; base += 32 * 8) {
+                    double2 xv[8];
+#pragma unroll
+                    for (int t = 0; t < 8; t++) {
+                        const long long u = base + (long long)t * 32 + lane;
+                        xv[t] = (u < nvec) ? vcol[u] : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; t++) {
+                        const long long u = base + (long long)t * 32 + lane;
+                        if (u < nvec) {
+                            double2 x = xv[t];
+                            const double2 e = load_e<CPLX, false, ESMEM>(E, Ew, u);  // q~_k (w = 1)
+                            if (CPLX) {
+                                double xr = x.x, xi = x.y;
+                                xr = fma(-re, e.x, xr);
+                                xr = fma(im, e.y, xr);
+                                xi = fma(-re, e.y, xi);
+                                xi = fma(-im, e.x, xi);
+                                x = make_double2(xr, xi);
+                            } else {
+                                x.x = fma(-re, e.x, x.x);
+                                x.y = fma(-re, e.y, x.y);
+                            }
+                            if (odd_tail && u == nvec - 1) x.y = 0.0;
+                            vcol[u] = x;
+                            acc = fma(x.x, x.x, acc);
+                            acc = fma(x.y, x.y, acc);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 1; h < 32; h <<= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, h);
+                r2n = acc;
+            }
+            if (lane == 0) a.r2[c] = r2n;
         } else {
             const double cc = CPLX ? fma(re, re, im * im) : re * re;  // CAC rule 5
             const double old = a.r2[c];
@@ -292,6 +340,55 @@ cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepCo
     }
     if (init) return cfg.esmem ? launch_t<false, true, true>(a, cfg, s) : launch_t<false, true, false>(a, cfg, s);
     return cfg.esmem ? launch_t<false, false, true>(a, cfg, s) : launch_t<false, false, false>(a, cfg, s);
+}
+
+// ------------------------------------------------------------------ explicit-mode helpers
+// V = W^{1/2} S (per real component, sqrt(w_i) rounded once): the explicit mode works on the
+// unweighted problem for S~ (reading R6).  V, S: M columns of nvec vectors (strides ldv, lds).
+__global__ void k_scale_sqrtw(double2 *V, long long ldv, const double2 *S, long long lds, long long M,
+                              long long nvec, long long N, const double *w, bool cplx) {
+    const long long total = M * nvec;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const long long c = t / nvec, u = t - c * nvec;
+        const double2 x = S[c * lds + u];
+        double2 y;
+        if (cplx) {
+            const double r = sqrt(w[u]);
+            y = make_double2(r * x.x, r * x.y);
+        } else {
+            y = make_double2(sqrt(w[2 * u]) * x.x, 2 * u + 1 < N ? sqrt(w[2 * u + 1]) * x.y : 0.0);
+        }
+        V[c * ldv + u] = y;
+    }
+}
+
+cudaError_t launch_scale_sqrtw(double2 *V, long long ldv, const double2 *S, long long lds, long long M, long long nvec,
+                               long long N, const double *w, bool cplx, cudaStream_t s) {
+    k_scale_sqrtw<<<148 * 8, 256, 0, s>>>(V, ldv, S, lds, M, nvec, N, w, cplx);
+    return cudaGetLastError();
+}
+
+// Q = Q~ / sqrt(w) per real component (the W-orthonormal basis of the explicit mode).
+__global__ void k_unscale_sqrtw(double2 *Q, const double2 *Qt, long long k, long long nvec, const double *w, bool cplx) {
+    const long long total = k * nvec;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const long long u = t % nvec;
+        const double2 x = Qt[t];
+        if (cplx) {
+            const double r = sqrt(w[u]);
+            Q[t] = make_double2(x.x / r, x.y / r);
+        } else {
+            // padding rows carry w = 0: keep them zero
+            const double r0 = sqrt(w[2 * u]), r1 = sqrt(w[2 * u + 1]);
+            Q[t] = make_double2(x.x / r0, r1 > 0.0 ? x.y / r1 : 0.0);
+        }
+    }
+}
+
+cudaError_t launch_unscale_sqrtw(double2 *Q, const double2 *Qt, long long k, long long nvec, const double *w, bool cplx,
+                                 cudaStream_t s) {
+    k_unscale_sqrtw<<<148 * 4, 256, 0, s>>>(Q, Qt, k, nvec, w, cplx);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ maxloc / sqrt helpers

@@ -27,6 +27,7 @@ REAL_F64, COMPLEX_F64 = 1, 2
 MEM_HOST, MEM_DEVICE = 0, 1
 COMM_NONE, COMM_NCCL, COMM_EXTERNAL = 0, 1, 2
 ORTHO = {"mgs": 0, "cgs": 1}
+RESIDUAL = {"recurrence": 0, "explicit": 1}
 
 
 class RbgError(RuntimeError):
@@ -44,6 +45,7 @@ class Desc(ctypes.Structure):
         ("device", ctypes.c_int), ("check_finite", ctypes.c_int), ("comm", ctypes.c_int),
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("col_offset", ctypes.c_int64),
         ("M_global", ctypes.c_int64), ("nccl_id", ctypes.c_uint8 * 128), ("ortho", ctypes.c_int),
+        ("residual", ctypes.c_int),
     ]
 
 
@@ -157,7 +159,7 @@ class Context:
     def __init__(self, S, w=None, tol: float = 0.0, k_max: int = 1, *, stream=None,
                  comm: int = COMM_NONE, rank: int = 0, world: int = 1, col_offset: int = 0,
                  M_global: int = 0, nccl_id: bytes | None = None, check_finite: bool = True,
-                 borrow: bool = True, ortho: str = "mgs"):
+                 borrow: bool = True, ortho: str = "mgs", residual: str = "recurrence"):
         L = lib()
         d = Desc()
         L.rbg_desc_init(ctypes.byref(d))
@@ -212,6 +214,7 @@ class Context:
         d.stream = None if stream is None else (1 if int(stream) == 0 else int(stream))
         d.check_finite = 1 if check_finite else 0
         d.ortho = ORTHO[ortho]
+        d.residual = RESIDUAL[residual]
         d.comm = comm
         d.rank = rank
         d.world = world

@@ -254,3 +254,36 @@ def test_cgs_variant_parity(rbg, orc, case):
     g = rbg.greedy(S, w, tol, k_max, ortho="cgs")
     o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL_CGS, ortho="cgs")
     compare(g, o)
+
+
+@pytest.mark.parametrize("case", ["cfg0", "cfg1", "cfg4", "odd_real_borrowed", "cplx_strided", "cgs"])
+def test_explicit_residual_parity(rbg, orc, case):
+    """Explicit residuals (Algorithm 2 in-place updates, rbg_desc.residual = EXPLICIT) against
+    the oracle's explicit mode: bit for bit, and the paper's tolerances are reached."""
+    import torch
+    rng = np.random.default_rng(88)
+    kw, okw = {}, {}
+    if case == "cfg0":
+        S, w, tol, k_max = inputs.config0()
+    elif case == "cfg1":
+        S, w, tol, k_max = inputs.config1(M=3000, N=2000)
+    elif case == "cfg4":
+        S, w, tol, k_max, _ = inputs.config4(M=4096, N=1024, r=256)
+    elif case == "odd_real_borrowed":
+        S, w, tol, k_max = rng.standard_normal((300, 257)), rng.uniform(0.5, 1.5, 257), 0.0, 60
+        big = torch.full((300, 258), float("nan"), dtype=torch.float64, device="cuda")
+        big[:, :257] = torch.as_tensor(S, device="cuda")
+        kw["_S"] = big[:, :257]                   # padding row holds NaN: must never be read
+    elif case == "cplx_strided":
+        S = rng.standard_normal((200, 1000)) + 1j * rng.standard_normal((200, 1000))
+        w, tol, k_max = rng.uniform(0.5, 1.5, 1000), 0.0, 50
+    else:
+        S, w, tol, k_max = inputs.config1(M=2000, N=800)
+        kw["ortho"], okw["ortho"] = "cgs", "cgs"
+    src = kw.pop("_S", S)
+    lanes = orc.CANONICAL_CGS if okw.get("ortho") == "cgs" else orc.CANONICAL
+    g = rbg.greedy(src, w, tol, k_max, residual="explicit", check_finite=False, **kw)
+    o = orc.greedy(S, w, tol, k_max, lanes=lanes, residual="explicit", **okw)
+    compare(g, o)
+    if case in ("cfg0", "cfg1"):
+        assert g.stop == "TOL"

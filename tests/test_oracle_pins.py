@@ -381,3 +381,46 @@ def test_cgs_variant_closed_forms_and_rank(orc):
     S = rand_matrix(rng, 50, 90, True, rank=9)
     res = orc.greedy(S, np.ones(50), 0.0, 50, lanes=orc.CANONICAL_CGS, ortho="cgs")
     assert res.k == 9 and res.stop == "RANK"
+
+
+# ---------------------------------------------------------------- explicit residuals (8f-4)
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_explicit_mode_is_algorithm2(orc, cplx):
+    """Explicit residuals = Algorithm 2 (MGS with pivoting, in-place updates) + IMGS of the
+    updated pivot column: same pivots as the independent Algorithm 2 and xGEQP3, |diag R|."""
+    rng = np.random.default_rng(300)
+    N, M, K = 30, 80, 25
+    S = rand_matrix(rng, N, M, cplx)
+    w = rng.uniform(0.5, 1.5, N)
+    r = orc.greedy(S, w, 0.0, K, residual="explicit")
+    St = brute.weighted(S, w)
+    piv2, rd2, _, _ = brute.mgs_pivoting(St, K)
+    np.testing.assert_array_equal(r.pivots, piv2)
+    np.testing.assert_allclose(r.errors[:K], rd2, rtol=1e-12)
+    Ql, Rl, P = scipy.linalg.qr(St, pivoting=True, mode="economic")
+    np.testing.assert_array_equal(r.pivots, P[:K])
+    G = (r.Q.conj() * w[None, :]) @ r.Q.T
+    assert np.max(np.abs(G - np.eye(K))) <= 1e-13
+    # R is Algorithm 2's factor: upper triangular in pivoted order, diagonal = residual norms
+    R11 = r.R[:, r.pivots]
+    scale = np.abs(R11).max()
+    assert np.max(np.abs(np.tril(R11, -1))) <= 1e-14 * scale
+    np.testing.assert_allclose(np.abs(np.diag(R11)), r.errors[:K], rtol=1e-12)
+
+
+def test_explicit_mode_beats_the_recurrence_floor(orc):
+    """Reading R8: the recurrence stalls near sqrt(eps) max||s|| and stops RANK on config 0;
+    explicit residuals reach the paper's tolerance (Cor. 5.6 holds to ~eps, checked by direct
+    projection)."""
+    S, w, tol, k_max = inputs.config0()
+    a = orc.greedy(S, w, tol, k_max)
+    b = orc.greedy(S, w, tol, k_max, residual="explicit")
+    assert a.stop == "RANK" and a.errors[-1] > 1e-9
+    assert b.stop == "TOL" and b.errors[-1] < tol
+    St = brute.weighted(S, w)
+    scale = np.sqrt(np.max(np.sum(w * S * S, axis=1)))
+    for k in (10, 40, b.k - 1, b.k):
+        Qt = (np.sqrt(w)[None, :] * b.Q[:k]).T
+        d = brute.direct_residuals(St, Qt)
+        assert abs(d.max() - b.errors[k]) <= 1e-13 * scale
