@@ -283,8 +283,25 @@ def run_ours(a):
 
     # ---- end to end through the C ABI with host buffers (pinned), all iterations
     if not a.no_e2e:
-        line["e2e"] = e2e(a, S, w, k_max, W + K, stream, rank, world, M_loc, M_glob, nccl_id, dev)
-    del S
+        # the host copy needs |S| of pinned RAM per rank on this node: all ranks agree first
+        need = S.numel() * S.element_size() * int(os.environ.get("LOCAL_WORLD_SIZE", "1")) * 1.15
+        ok = host_mem_available() > need
+        if world > 1:
+            t = torch.tensor([1 if ok else 0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok = bool(t.item())
+        if ok:
+            host = torch.empty(S.shape, dtype=S.dtype, pin_memory=True)
+            host.copy_(S)
+            del S
+            torch.cuda.empty_cache()
+            line["e2e"] = e2e(a, host, w, k_max, W + K, stream, rank, world, M_loc, M_glob, dev)
+            del host
+        else:
+            line["e2e"] = {"value": None, "unit": "it/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                           "note": f"not run: host RAM available {host_mem_available() / 1e9:.0f} GB < "
+                                   f"{need / 1e9:.0f} GB needed for pinned host copies of the input"}
+    S = None
     torch.cuda.empty_cache()
 
     # ---- CPU oracle baseline (rank 0, one GPU only)
@@ -305,19 +322,27 @@ def run_ours(a):
     return 0
 
 
-def e2e(a, S, w, k_max, iters, stream, rank, world, M_loc, M_glob, nccl_id, dev):
-    """Same metric through the public API with HOST buffers: H2D of S inside the timed
-    region (create), all iterations, and the D2H read of pivots, errors and basis."""
+def host_mem_available() -> float:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return float(line.split()[1]) * 1024.0
+    except OSError:
+        pass
+    return 0.0
+
+
+def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev):
+    """Same metric through the public API with HOST buffers: H2D of S (pinned host copy)
+    inside the timed region (create), all iterations, and the D2H read of pivots, errors
+    and basis."""
     import torch
     import torch.distributed as dist
     from paper_1805_06124_b200 import rbg
 
-    host = torch.empty(S.shape, dtype=S.dtype, pin_memory=True)
-    host.copy_(S)
-    S_cols = S.shape
-    del S
-    torch.cuda.empty_cache()
+    S_cols = host.shape
     Sh = host.numpy()
+    nccl_id = None
     from paper_1805_06124_b200 import dist as D
     if world > 1:
         dist.barrier()
@@ -334,7 +359,7 @@ def e2e(a, S, w, k_max, iters, stream, rank, world, M_loc, M_glob, nccl_id, dev)
     t1 = time.perf_counter()
     wall = D.max_over_ranks(t1 - t0, device=dev)
     ctx.close()
-    del host, Sh
+    del Sh
     h2d = S_cols[0] * S_cols[1] * 16
     d2h = piv.nbytes + err.nbytes + Q.nbytes
     return {"value": iters / wall * (M_glob / M_PER_GPU), "unit": "it/s",
