@@ -73,13 +73,88 @@ __device__ __forceinline__ double2 load_e(const double2 *E, const double *Ew, lo
     return ESMEM ? E[u] : __ldg(E + u);
 }
 
+// CTA maxloc of the warps' bests, then the last CTA to finish (atomic ticket) reduces the
+// per-CTA records with the total order into the device state and, on a sharded run, packs
+// the local candidate column into the exchange slot.
+template <bool CPLX>
+__device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, long long best_j, bool odd_tail) {
+    __shared__ double s_m[kSweepWarps];
+    __shared__ long long s_j[kSweepWarps];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long nvec = a.nvec;
+    if (lane == 0) {
+        s_m[warp] = best_m;
+        s_j[warp] = best_j;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double bm = s_m[0];
+        long long bj = s_j[0];
+        for (int w = 1; w < kSweepWarps; w++)
+            if (rec_better(s_m[w], s_j[w], bm, bj)) {
+                bm = s_m[w];
+                bj = s_j[w];
+            }
+        a.recs[blockIdx.x].m = bm;
+        a.recs[blockIdx.x].j = bj;
+        __threadfence();
+        const unsigned t = atomicAdd(a.ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp == 0) {
+        double bm = -INFINITY;
+        long long bj = 0x7fffffffffffffffLL;
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+            const double m = __ldcg(&a.recs[b].m);
+            const long long j = __ldcg(&a.recs[b].j);
+            if (rec_better(m, j, bm, bj)) {
+                bm = m;
+                bj = j;
+            }
+        }
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {  // exact: total order, any combine order
+            const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+            const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+            if (rec_better(om, oj, bm, bj)) {
+                bm = om;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            const long long jg = (bj == 0x7fffffffffffffffLL) ? bj : bj + a.col_offset;
+            a.st->m_loc = bm;
+            a.st->j_loc = jg;
+            *a.ticket = 0u;
+            if (a.send) {
+                Rec *h = reinterpret_cast<Rec *>(a.send);
+                h->m = bm;
+                h->j = jg;
+            }
+        }
+        if (a.send) s_j[0] = bj;
+    }
+    if (a.send) {  // pack the local candidate column for the all-gather
+        __syncthreads();
+        const long long bj = s_j[0];
+        double2 *dst = reinterpret_cast<double2 *>(a.send + sizeof(Rec));
+        const bool valid = bj >= 0 && bj < a.M;
+        for (long long u = tid; u < nvec; u += kSweepThreads) {
+            double2 x = valid ? a.S[bj * a.ldv + u] : make_double2(0.0, 0.0);
+            if (odd_tail && u == nvec - 1) x.y = 0.0;
+            dst[u] = x;
+        }
+    }
+}
+
 template <bool CPLX, bool INIT, bool ESMEM, int U>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar;
-    __shared__ double s_m[kSweepWarps];
-    __shared__ long long s_j[kSweepWarps];
-    __shared__ int s_last;
 
     const int stop = a.st->stop;
     if (stop) return;
@@ -224,73 +299,122 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     }
     if (!waited) mbar_wait(&mbar, 0);  // never leave with a bulk copy in flight
 
-    // ---- CTA maxloc, then last-CTA-done global maxloc ---------------------------------
-    if (lane == 0) {
-        s_m[warp] = best_m;
-        s_j[warp] = best_j;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double bm = s_m[0];
-        long long bj = s_j[0];
-        for (int w = 1; w < kSweepWarps; w++)
-            if (rec_better(s_m[w], s_j[w], bm, bj)) {
-                bm = s_m[w];
-                bj = s_j[w];
-            }
-        a.recs[blockIdx.x].m = bm;
-        a.recs[blockIdx.x].j = bj;
-        __threadfence();
-        const unsigned t = atomicAdd(a.ticket, 1u);
-        s_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (warp == 0) {
-        double bm = -INFINITY;
-        long long bj = 0x7fffffffffffffffLL;
-        for (int b = lane; b < (int)gridDim.x; b += 32) {
-            const double m = __ldcg(&a.recs[b].m);
-            const long long j = __ldcg(&a.recs[b].j);
-            if (rec_better(m, j, bm, bj)) {
-                bm = m;
-                bj = j;
-            }
-        }
-#pragma unroll
-        for (int h = 16; h >= 1; h >>= 1) {  // exact: total order, any combine order
-            const double om = __shfl_xor_sync(0xffffffffu, bm, h);
-            const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
-            if (rec_better(om, oj, bm, bj)) {
-                bm = om;
-                bj = oj;
+    sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
+}
+
+// Continuous-ring variant of k_sweep for the recurrence (a0/a2): a warp's columns form one
+// stream of 16-byte trips (column c0, c0+16, ...; ceil(nvec/32) trips each), and the ring of
+// U loads in flight runs across column boundaries, so the next column's first vectors are
+// already in flight while the current column is reduced (xor-butterfly), its r2 updated and
+// its R entry stored.  The per-lane chains, the lane tree and the visiting order are those
+// of k_sweep: results are bit-identical.  r2 of the next column is prefetched one column
+// ahead so its load latency never stalls the warp.
+template <bool CPLX, bool INIT, bool ESMEM, int U>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_ring(const SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t mbar;
+
+    if (a.st->stop) return;
+    const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long nvec = a.nvec;
+    const bool odd_tail = !CPLX && (a.N & 1);
+
+    const double2 *Eg = INIT ? reinterpret_cast<const double2 *>(a.w) : a.WQ + (k - 1) * a.ldq_v;
+    const double2 *E = Eg;
+    const double *Ew = a.w;
+    if (ESMEM) {
+        const size_t bytes = (INIT && CPLX) ? ((size_t)nvec * 8 + 15) / 16 * 16 : (size_t)nvec * 16;
+        if (tid == 0) {
+            mbar_init(&mbar, 1);
+            mbar_arrive_expect_tx(&mbar, (uint32_t)bytes);
+            const unsigned char *src = reinterpret_cast<const unsigned char *>(Eg);
+            for (size_t off = 0; off < bytes; off += kBulkChunk) {
+                uint32_t n = (uint32_t)((bytes - off) < kBulkChunk ? (bytes - off) : kBulkChunk);
+                bulk_g2s(smem + off, src + off, n, &mbar);
             }
         }
-        if (lane == 0) {
-            const long long jg = (bj == 0x7fffffffffffffffLL) ? bj : bj + a.col_offset;
-            a.st->m_loc = bm;
-            a.st->j_loc = jg;
-            *a.ticket = 0u;
-            if (a.send) {
-                Rec *h = reinterpret_cast<Rec *>(a.send);
-                h->m = bm;
-                h->j = jg;
-            }
-        }
-        if (a.send) s_j[0] = bj;
-    }
-    if (a.send) {  // pack the local candidate column for the all-gather
         __syncthreads();
-        const long long bj = s_j[0];
-        double2 *dst = reinterpret_cast<double2 *>(a.send + sizeof(Rec));
-        const bool valid = bj >= 0 && bj < a.M;
-        for (long long u = tid; u < nvec; u += kSweepThreads) {
-            double2 x = valid ? a.S[bj * a.ldv + u] : make_double2(0.0, 0.0);
-            if (odd_tail && u == nvec - 1) x.y = 0.0;
-            dst[u] = x;
+        E = reinterpret_cast<const double2 *>(smem);
+        Ew = reinterpret_cast<const double *>(smem);
+    }
+
+    const long long c_begin = (long long)blockIdx.x * a.M / gridDim.x;
+    const long long c_end = (long long)(blockIdx.x + 1) * a.M / gridDim.x;
+    const uint64_t pol = policy_evict_first();
+    // a column is gpc groups of U trips (32 vectors per trip); the last group is ragged
+    const int nv = (int)nvec;
+    const int gpc = (int)((nvec + 32 * U - 1) / (32 * U));
+    const long long c0 = c_begin + warp;
+    const long long ncols = c0 < c_end ? (c_end - c0 + kSweepWarps - 1) / kSweepWarps : 0;
+    const long long G = ncols * gpc;  // groups of this warp
+
+    // load cursor: group lg of the column whose first vector (+ lane) is lcol
+    const double2 *lcol = a.S + c0 * a.ldv + lane;
+    int lg = 0;
+    double2 xr[U];
+#pragma unroll
+    for (int t = 0; t < U; t++)
+        xr[t] = (G > 0 && t * 32 + lane < nv) ? ld_stream(lcol + t * 32, pol) : make_double2(0.0, 0.0);
+    if (++lg == gpc) { lg = 0; lcol += (long long)kSweepWarps * a.ldv; }
+    if (ESMEM) mbar_wait(&mbar, 0);  // loads are in flight; now e~ must have landed
+
+    double best_m = -INFINITY;
+    long long best_j = 0x7fffffffffffffffLL;
+    double re = 0.0, im = 0.0;
+    long long c = c0;
+    int cg = 0;  // group of column c being consumed
+    double old = (!INIT && ncols > 0) ? a.r2[c0] : 0.0;  // r2 of the current column
+
+    for (long long g = 0; g < G; g++) {
+        const bool more = g + 1 < G;
+        const int lu0 = lg * 32 * U + lane;  // first vector of the group being issued
+        const int cu0 = cg * 32 * U + lane;  // first vector of the group being consumed
+        const double2 *lp = lcol + lg * 32 * U;
+#pragma unroll
+        for (int t = 0; t < U; t++) {
+            double2 x = xr[t];
+            // refill slot t with the same slot of the next group (possibly the next column)
+            xr[t] = (more && lu0 + t * 32 < nv) ? ld_stream(lp + t * 32, pol) : make_double2(0.0, 0.0);
+            const int u = cu0 + t * 32;
+            if (u < nv) {
+                if (odd_tail && u == nv - 1) x.y = 0.0;  // row N is padding
+                accum<CPLX, INIT>(re, im, x, load_e<CPLX, INIT, ESMEM>(E, Ew, u));
+            }
+        }
+        if (++lg == gpc) { lg = 0; lcol += (long long)kSweepWarps * a.ldv; }
+        if (++cg == gpc) {  // column c complete (warp-uniform)
+            cg = 0;
+#pragma unroll
+            for (int h = 1; h < 32; h <<= 1) {  // CAC rule 3
+                re = re + __shfl_xor_sync(0xffffffffu, re, h);
+                if (CPLX && !INIT) im = im + __shfl_xor_sync(0xffffffffu, im, h);
+            }
+            double r2n;
+            if (INIT) {
+                r2n = re;
+                if (lane == 0) a.r2[c] = r2n;
+            } else {
+                const double cc = CPLX ? fma(re, re, im * im) : re * re;  // CAC rule 5
+                r2n = old - cc;                                            // CAC rule 6
+                if (lane == 0) {
+                    if (CPLX) reinterpret_cast<double2 *>(a.R)[(k - 1) * a.ldr + c] = make_double2(re, im);
+                    else a.R[(k - 1) * a.ldr + c] = re;
+                    a.r2[c] = r2n;
+                }
+                const long long cn = c + kSweepWarps;
+                old = cn < c_end ? a.r2[cn] : 0.0;
+            }
+            if (r2n > best_m) {  // columns visited in increasing order: first max wins
+                best_m = r2n;
+                best_j = c;
+            }
+            c += kSweepWarps;
+            re = 0.0;
+            im = 0.0;
         }
     }
+    sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
 }
 
 SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int device) {
@@ -314,13 +438,22 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
     return c;
 }
 
+using SweepKernel = void (*)(const SweepArgs);
+
+template <bool CPLX, bool INIT, bool ESMEM, int U>
+static SweepKernel pick_kernel(bool ring) {
+    // the explicit mode (a.V) re-reads and rewrites each column: per-column loop of k_sweep
+    return ring ? k_sweep_ring<CPLX, INIT, ESMEM, U> : k_sweep<CPLX, INIT, ESMEM, U>;
+}
+
 template <bool CPLX, bool INIT, bool ESMEM>
 static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStream_t s) {
-    auto kern = k_sweep<CPLX, INIT, ESMEM, 4>;
+    const bool ring = a.V == nullptr && getenv("RBG_SWEEP_PERCOL") == nullptr;
+    auto kern = pick_kernel<CPLX, INIT, ESMEM, 4>(ring);
     switch (cfg.unroll) {
-        case 8: kern = k_sweep<CPLX, INIT, ESMEM, 8>; break;
-        case 12: kern = k_sweep<CPLX, INIT, ESMEM, 12>; break;
-        case 16: kern = k_sweep<CPLX, INIT, ESMEM, 16>; break;
+        case 8: kern = pick_kernel<CPLX, INIT, ESMEM, 8>(ring); break;
+        case 12: kern = pick_kernel<CPLX, INIT, ESMEM, 12>(ring); break;
+        case 16: kern = pick_kernel<CPLX, INIT, ESMEM, 16>(ring); break;
         default: break;
     }
     if (cfg.smem > 48 * 1024) {
