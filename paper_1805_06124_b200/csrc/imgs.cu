@@ -16,6 +16,7 @@
 // (L2 evict-last) before the reduction so their latency overlaps it.  The kernel is
 // replicated on every GPU of a sharded run (no broadcast of q needed).
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -31,7 +32,9 @@ namespace rbg {
 // Slots and mbarriers are double-buffered by reduction parity: a CTA can only receive the
 // data of reduction n+2 after all of its own warps have sent reduction n+1, i.e. after
 // they finished reading the buffers of reduction n.
+template <int CTAS>
 struct ClusterReducer {
+    static constexpr int WPC = kLaneImgs / CTAS / 32;  // warps per CTA; CTAS * WPC = 64 leaves
     double2 (*slots)[64];
     uint64_t *bars;
     uint32_t rank;
@@ -44,8 +47,8 @@ struct ClusterReducer {
             re = re + __shfl_xor_sync(0xffffffffu, re, h);
             im = im + __shfl_xor_sync(0xffffffffu, im, h);
         }
-        if (lane < kImgsCtas) {
-            const uint32_t dst = map_dsmem(smem_u32(&slots[par][rank * 8 + warp]), (uint32_t)lane);
+        if (lane < CTAS) {
+            const uint32_t dst = map_dsmem(smem_u32(&slots[par][rank * WPC + warp]), (uint32_t)lane);
             const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
             st_async_v2(dst, re, im, bar);
         }
@@ -137,7 +140,7 @@ __device__ __forceinline__ void axpy(double2 (&v)[MAXV], const double2 *q, int s
 // full-mbarrier (TMA bytes) and one empty-mbarrier (8 consumer warps) per stage, so issuing
 // copies never delays a warp on the reduction's critical path.  D = 0: the slices are loaded
 // straight from global memory one step ahead (large N only).
-template <int MAXV, int D>
+template <int MAXV, int D, int THREADS>
 struct BasisPipe {
     unsigned char *smem;
     uint64_t *full, *empty;
@@ -145,12 +148,12 @@ struct BasisPipe {
     long long ldq_v;
     int k, rank, nvec;
 
-    static constexpr int kStageBytes = 2 * MAXV * kImgsThreads * 16;
+    static constexpr int kStageBytes = 2 * MAXV * THREADS * 16;
 
     __device__ __forceinline__ double2 *wq_stage(long long s) const {
         return reinterpret_cast<double2 *>(smem + (size_t)(s % D) * kStageBytes);
     }
-    __device__ __forceinline__ double2 *q_stage(long long s) const { return wq_stage(s) + MAXV * kImgsThreads; }
+    __device__ __forceinline__ double2 *q_stage(long long s) const { return wq_stage(s) + MAXV * THREADS; }
 
     __device__ void issue(long long s) const {  // one producer thread
         const int b = (int)(s % k);
@@ -158,9 +161,9 @@ struct BasisPipe {
         int len[MAXV];
 #pragma unroll
         for (int m = 0; m < MAXV; m++) {
-            const int u0 = m * kLaneImgs + rank * kImgsThreads;
+            const int u0 = m * kLaneImgs + rank * THREADS;
             const int l = nvec - u0;
-            len[m] = l < 0 ? 0 : (l > kImgsThreads ? kImgsThreads : l);
+            len[m] = l < 0 ? 0 : (l > THREADS ? THREADS : l);
             bytes += 2u * (uint32_t)len[m] * 16u;
         }
         uint64_t *bar = &full[s % D];
@@ -170,9 +173,9 @@ struct BasisPipe {
 #pragma unroll
         for (int m = 0; m < MAXV; m++) {
             if (len[m] > 0) {
-                const int u0 = m * kLaneImgs + rank * kImgsThreads;
-                bulk_g2s(dw + m * kImgsThreads, wq + u0, (uint32_t)len[m] * 16u, bar);
-                bulk_g2s(dq + m * kImgsThreads, q + u0, (uint32_t)len[m] * 16u, bar);
+                const int u0 = m * kLaneImgs + rank * THREADS;
+                bulk_g2s(dw + m * THREADS, wq + u0, (uint32_t)len[m] * 16u, bar);
+                bulk_g2s(dq + m * THREADS, q + u0, (uint32_t)len[m] * 16u, bar);
             }
         }
     }
@@ -195,9 +198,9 @@ struct BasisPipe {
     }
 };
 
-template <bool CPLX, int MAXV, int D>
-__global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads + 32, 1)
-    k_imgs(const ImgsArgs a) {
+template <bool CPLX, int MAXV, int D, int CTAS>
+__global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArgs a) {
+    constexpr int THREADS = kLaneImgs / CTAS;  // consumer threads per CTA (one lane each)
     constexpr int DD = D > 0 ? D : 1;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double2 s_slots[2][64];
@@ -210,9 +213,9 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     const long long k = a.st->k;
     const uint32_t rank = cluster_ctarank();
     const int tid = threadIdx.x;
-    const bool producer = tid >= kImgsThreads;   // warp 8 (D > 0 only)
+    const bool producer = tid >= THREADS;   // the last warp (D > 0 only)
     const int nvec = (int)a.nvec;
-    const int u0 = (int)rank * kImgsThreads + tid;             // this lane's first vector
+    const int u0 = (int)rank * THREADS + tid;                  // this lane's first vector
     const int nm = (!producer && u0 < nvec) ? (nvec - u0 + kLaneImgs - 1) / kLaneImgs : 0;
     const bool odd_tail = !CPLX && (a.N & 1);
 
@@ -241,7 +244,7 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     else if (err < a.tol) why = kStopTol;
     else if (k == a.k_max) why = kStopKmax;
 
-    const BasisPipe<MAXV, DD> pipe{dsm, s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec};
+    const BasisPipe<MAXV, DD, THREADS> pipe{dsm, s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec};
     const long long limit = (long long)kNuMax * k;  // MGS steps that can ever be needed
     if (tid == 0) {
         mbar_init(&s_bars[0], 1);
@@ -250,10 +253,10 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
         mbar_arrive_expect_tx(&s_bars[1], 64 * 16);
         s_done = -1;
     }
-    if (D > 0 && tid == kImgsThreads) {
+    if (D > 0 && tid == THREADS) {
         for (int i = 0; i < DD; i++) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], kImgsThreads / 32);
+            mbar_init(&s_empty[i], THREADS / 32);
         }
         if (why == kStopNone)
             for (long long s = 0; s < DD && s < limit; s++) pipe.issue(s);
@@ -268,7 +271,7 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
         return;
     }
     if (producer) {
-        if (D > 0 && tid == kImgsThreads) pipe.produce(DD < limit ? DD : limit, limit, &s_done);
+        if (D > 0 && tid == THREADS) pipe.produce(DD < limit ? DD : limit, limit, &s_done);
         return;
     }
 
@@ -286,7 +289,7 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     }
 
     const int warp = tid >> 5, lane = tid & 31;
-    ClusterReducer red{s_slots, s_bars, rank, warp, lane, 0, 0u};
+    ClusterReducer<CTAS> red{s_slots, s_bars, rank, warp, lane, 0, 0u};
     const uint64_t keep = policy_evict_last();
     const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
     double n_prev = n0, nn = 0.0;
@@ -309,9 +312,9 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
             double2 c;
             if (D > 0) {
                 mbar_wait(&s_full[s % DD], (uint32_t)((s / DD) & 1));
-                dot_partial<CPLX, MAXV>(v, pipe.wq_stage(s) + tid, kImgsThreads, nm, pr, pi);
+                dot_partial<CPLX, MAXV>(v, pipe.wq_stage(s) + tid, THREADS, nm, pr, pi);
                 c = red.sum(pr, pi);
-                axpy<CPLX, MAXV>(v, pipe.q_stage(s) + tid, kImgsThreads, nm, c);
+                axpy<CPLX, MAXV>(v, pipe.q_stage(s) + tid, THREADS, nm, c);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[s % DD]);  // this warp is done with the stage
             } else {
@@ -377,7 +380,7 @@ __global__ void __cluster_dims__(kImgsCtas, 1, 1) __launch_bounds__(kImgsThreads
     }
 }
 
-// (MAXV, D): vectors per lane and prefetch depth, D * MAXV * 8 KB of shared memory.
+// (MAXV, D): vectors per lane and prefetch depth, D * MAXV * 32 KB / CTAS of shared memory.
 int imgs_maxv(long long nvec) {
     const long long per = (nvec + kLaneImgs - 1) / kLaneImgs;
     if (per <= 6) return (int)(per < 1 ? 1 : per);
@@ -387,36 +390,71 @@ int imgs_maxv(long long nvec) {
     return 0;
 }
 
-template <bool CPLX, int MAXV, int D>
+// Cluster size: 16 CTAs x 128 lanes (non-portable cluster) halves each SM's share of the
+// per-step FP64 work and basis bytes against 8 x 256; L_I = 2048 and the reduction tree are
+// the same, so the result bits are identical.  RBG_IMGS_CTAS=8 selects the portable size.
+static int imgs_ctas() {
+    static int c = 0;
+    if (c == 0) {
+        c = 16;
+        if (const char *e = getenv("RBG_IMGS_CTAS"))
+            if (atoi(e) == 8) c = 8;
+    }
+    return c;
+}
+
+template <bool CPLX, int MAXV, int D, int CTAS>
 static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
-    auto kern = k_imgs<CPLX, MAXV, D>;
-    const size_t smem = D > 0 ? (size_t)D * 2 * MAXV * kImgsThreads * 16 : 0;
+    auto kern = k_imgs<CPLX, MAXV, D, CTAS>;
+    constexpr int THREADS = kLaneImgs / CTAS;
+    const size_t smem = D > 0 ? (size_t)D * 2 * MAXV * THREADS * 16 : 0;
+    cudaError_t e;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<kImgsCtas, kImgsThreads + 32, smem, s>>>(a);
+    if (CTAS > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CTAS, 1, 1);
+    cfg.blockDim = dim3(THREADS + 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CTAS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-template <bool CPLX>
+template <bool CPLX, int CTAS>
 static cudaError_t launch_c(const ImgsArgs &a, cudaStream_t s) {
+    // prefetch depth: the same shared-memory budget per CTA at either cluster size
+    constexpr int X = CTAS / 8;
     switch (imgs_maxv(a.nvec)) {
-        case 1: return launch_md<CPLX, 1, 8>(a, s);
-        case 2: return launch_md<CPLX, 2, 6>(a, s);
-        case 3: return launch_md<CPLX, 3, 6>(a, s);
-        case 4: return launch_md<CPLX, 4, 5>(a, s);
-        case 5: return launch_md<CPLX, 5, 4>(a, s);
-        case 6: return launch_md<CPLX, 6, 4>(a, s);
-        case 8: return launch_md<CPLX, 8, 3>(a, s);
-        case 12: return launch_md<CPLX, 12, 0>(a, s);
-        case 16: return launch_md<CPLX, 16, 0>(a, s);
+        case 1: return launch_md<CPLX, 1, 8 * X, CTAS>(a, s);
+        case 2: return launch_md<CPLX, 2, 6 * X, CTAS>(a, s);
+        case 3: return launch_md<CPLX, 3, 6 * X, CTAS>(a, s);
+        case 4: return launch_md<CPLX, 4, 5 * X, CTAS>(a, s);
+        case 5: return launch_md<CPLX, 5, 4 * X, CTAS>(a, s);
+        case 6: return launch_md<CPLX, 6, 4 * X, CTAS>(a, s);
+        case 8: return launch_md<CPLX, 8, 3 * X, CTAS>(a, s);
+        case 12: return launch_md<CPLX, 12, 0, CTAS>(a, s);
+        case 16: return launch_md<CPLX, 16, 0, CTAS>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s) {
-    return cplx ? launch_c<true>(a, s) : launch_c<false>(a, s);
+    if (imgs_ctas() == 16) return cplx ? launch_c<true, 16>(a, s) : launch_c<false, 16>(a, s);
+    return cplx ? launch_c<true, 8>(a, s) : launch_c<false, 8>(a, s);
 }
 
 }  // namespace rbg
