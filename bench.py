@@ -55,6 +55,9 @@ def parse():
                    help="IMGS variant: the paper's MGSCI (default) or Hoffmann CGSCI")
     p.add_argument("--residual", default="recurrence", choices=["recurrence", "explicit"],
                    help="column residuals: the paper's recurrence (default) or Algorithm 2 updates")
+    p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                   help="N > 1 exchange: records/pivot column over NVLink inside the kernels (default) "
+                        "or one ncclAllGather per iteration")
     return p.parse_args()
 
 
@@ -171,6 +174,7 @@ def config_dict(a, world):
             "k_window": [a.warmup, a.warmup + a.steps], "parallelism": f"column-sharded x{world}",
             "l2": "inputs (65.5 GB/GPU) >> 126 MB L2; no flush",
             "ortho": getattr(a, "ortho", "mgs"), "residual": getattr(a, "residual", "recurrence"),
+            "exchange": (getattr(a, "comm", "peer") if world > 1 else "none"),
             "value_unit": "greedy iterations/s x (cols_global / 409,600) -- plain it/s at 1 GPU"}
 
 
@@ -214,13 +218,16 @@ def run_ours(a):
     nccl_id = None
     comm = rbg.COMM_NONE
     if world > 1:
-        nccl_id = D.nccl_unique_id()
-        comm = rbg.COMM_NCCL
+        comm = rbg.COMM_PEER if a.comm == "peer" else rbg.COMM_NCCL
+        if comm == rbg.COMM_NCCL:
+            nccl_id = D.nccl_unique_id()
     stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
     torch.cuda.set_stream(stream)
     ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
                       world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id, ortho=a.ortho,
                       residual=a.residual)
+    if comm == rbg.COMM_PEER:
+        D.connect_peers(ctx)
     ctx.set_timing(True)
     if a.graph_batch:
         ctx.set_graph_batch(a.graph_batch)
@@ -278,7 +285,9 @@ def run_ours(a):
         "hbm_gbs_per_gpu": achieved, "hbm_gbs_total": achieved * world,
         "phase_ms_avg": {"sweep": float(np.mean(sw)), "xchg": float(np.mean(xc)), "imgs": float(np.mean(im))},
         "final_err": float(errs[-1]) if len(errs) else None,
-        "roofline": roof, "clocks": clocks, "gpu_launches": 2 * K,
+        "roofline": roof, "clocks": clocks,
+        # ours per iteration: sweep + IMGS (+ the PEER wait kernel); NCCL's own kernel not counted
+        "gpu_launches": (3 if comm == rbg.COMM_PEER else 2) * K,
     }
 
     # ---- end to end through the C ABI with host buffers (pinned), all iterations
@@ -344,14 +353,18 @@ def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev):
     Sh = host.numpy()
     nccl_id = None
     from paper_1805_06124_b200 import dist as D
+    comm = rbg.COMM_NONE
     if world > 1:
         dist.barrier()
-        nccl_id = D.nccl_unique_id()
+        comm = rbg.COMM_PEER if a.comm == "peer" else rbg.COMM_NCCL
+        if comm == rbg.COMM_NCCL:
+            nccl_id = D.nccl_unique_id()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ctx = rbg.Context(Sh, w, 0.0, k_max, stream=stream.cuda_stream,
-                      comm=rbg.COMM_NCCL if world > 1 else rbg.COMM_NONE, rank=rank, world=world,
+    ctx = rbg.Context(Sh, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank, world=world,
                       col_offset=D.partition(M_glob, world, rank)[0], M_global=M_glob, nccl_id=nccl_id)
+    if comm == rbg.COMM_PEER:
+        D.connect_peers(ctx)
     ctx.step(iters)
     piv = ctx.pivots()
     err = ctx.errors()

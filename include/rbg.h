@@ -59,16 +59,26 @@ typedef enum {
     RBG_STOP_TOL = 1,           /* err_k < tol (Algorithm 3 loop test)      */
     RBG_STOP_KMAX = 2,          /* k = k_max basis vectors                                */
     RBG_STOP_RANK = 3,          /* IMGS found the pivot numerically in span(Q) (R7, R17)   */
-    RBG_STOP_ALL_SELECTED = 4   /* every column already selected                          */
+    RBG_STOP_ALL_SELECTED = 4,  /* every column already selected                          */
+    RBG_STOP_PEER_TIMEOUT = 5   /* comm = PEER: a rank's record did not arrive within
+                                   rbg_desc.peer_timeout_ms; the outputs are incomplete     */
 } rbg_stop;
 
 typedef enum { RBG_MEM_HOST = 0, RBG_MEM_DEVICE = 1 } rbg_mem;
 
-/* Column-sharded execution: NONE = one GPU owns all columns;
+/* Column-sharded execution (the paper's MPI exchange):
+ * NONE = one GPU owns all columns;
  * NCCL = ncclAllGather of {maxloc record, candidate column} per iteration;
  * EXTERNAL = the caller moves the exchange buffers itself between rbg_iter_local and
- * rbg_iter_finish (used to run the sharded path on one GPU in tests). */
-typedef enum { RBG_COMM_NONE = 0, RBG_COMM_NCCL = 1, RBG_COMM_EXTERNAL = 2 } rbg_comm;
+ *   rbg_iter_finish (used to run the sharded path on one GPU in tests);
+ * PEER = no collective library: each rank's sweep kernel stores its 16-byte maxloc record into
+ *   every rank's memory over NVLink (CUDA IPC mappings, release/acquire tags) and the
+ *   replicated IMGS reads the winner's column from the owner's send slot over NVLink.  Needs
+ *   rbg_peer_export + rbg_peer_connect (all ranks on one node, P2P-capable GPUs, world <= 8). */
+typedef enum { RBG_COMM_NONE = 0, RBG_COMM_NCCL = 1, RBG_COMM_EXTERNAL = 2, RBG_COMM_PEER = 3 } rbg_comm;
+
+/* Bytes of one rank's PEER handle blob (two cudaIpcMemHandle_t). */
+#define RBG_PEER_HANDLE_BYTES 128
 
 /* Orthogonalisation of each new basis vector: Hoffmann's iterated MODIFIED Gram-Schmidt
  * ("MGSCI", kappa = 2; the paper's choice) or iterated CLASSICAL
@@ -108,6 +118,8 @@ typedef struct rbg_desc {
     uint8_t nccl_id[128]; /* ncclUniqueId from rbg_get_unique_id on rank 0 (comm = NCCL) */
     rbg_ortho ortho;      /* orthogonalisation of the pivot column (default MGS)         */
     rbg_residual residual;/* how the column residuals are kept (default RECURRENCE)       */
+    int64_t peer_timeout_ms; /* comm = PEER: stop PEER_TIMEOUT when a peer's record is this
+                             late (0 => 60,000 ms)                                       */
 } rbg_desc;
 
 typedef struct rbg_stats {
@@ -226,6 +238,20 @@ rbg_status rbg_xchg_buffers(rbg_ctx *ctx, void **send, void **recv, size_t *byte
 /* Convenience for tests: all-gather the send buffers of `world` EXTERNAL contexts on the
  * same device (device-to-device copies), ctxs[p] holding rank p. */
 rbg_status rbg_emulate_allgather(rbg_ctx **ctxs, int world);
+
+/* PEER exchange setup.  Every rank exports RBG_PEER_HANDLE_BYTES of CUDA-IPC handles (its
+ * record array and send slots), the caller all-gathers them (rank order) and every rank
+ * connects: peer buffers are mapped with cudaIpcOpenMemHandle (own buffers used directly).
+ * Until connected, rbg_run / rbg_step return ESTATE (a one-rank PEER context is connected at
+ * create).  ESTATE on a non-PEER context; ECUDA if a mapping fails.  The PEER iteration can
+ * also be driven by rbg_iter_local / rbg_iter_finish (finish = wait for the records + IMGS). */
+rbg_status rbg_peer_export(rbg_ctx *ctx, uint8_t out[RBG_PEER_HANDLE_BYTES]);
+rbg_status rbg_peer_connect(rbg_ctx *ctx, const uint8_t *all_handles);
+/* Tests on one GPU: wire `world` PEER contexts of this process (ctxs[p] = rank p, same
+ * device and the same stream, else EINVAL) to each other's buffers directly.  Drive them with rbg_iter_local on every rank,
+ * then rbg_iter_finish on every rank (stream order puts every record in place before any
+ * rank waits: no kernel ever waits for one that has not been launched). */
+rbg_status rbg_peer_connect_local(rbg_ctx **ctxs, int world);
 
 /* Lane counts of the canonical arithmetic contract this build implements. */
 void rbg_lanes(int *L_S, int *L_I);

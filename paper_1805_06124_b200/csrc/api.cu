@@ -100,6 +100,14 @@ struct rbg_ctx {
     double *w_true = nullptr;    // explicit mode: the caller's weights (w holds ones)
     double2 *cgs_v = nullptr, *cgs_c = nullptr;
     int cgs_grid = 0;
+    // PEER exchange: this rank's record array, every rank's record array and send slots
+    // (own pointers or CUDA-IPC mappings), which of them were opened through IPC
+    PeerRec *peer_in = nullptr;
+    PeerRec *peer_rec[kMaxPeers] = {};
+    unsigned char *peer_send[kMaxPeers] = {};
+    bool peer_ipc[kMaxPeers] = {};
+    bool peer_connected = false;
+    long long peer_timeout_ns = 0;
 };
 
 namespace {
@@ -111,6 +119,12 @@ void free_ctx(rbg_ctx *c) {
     for (auto &p : c->ev)
         for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
     if (c->nccl) nccl_destroy(c->nccl);
+    for (int q = 0; q < kMaxPeers; q++)
+        if (c->peer_ipc[q]) {
+            cudaIpcCloseMemHandle(c->peer_rec[q]);
+            cudaIpcCloseMemHandle(c->peer_send[q]);
+        }
+    cudaFree(c->peer_in);
     if (c->own_S) cudaFree(c->S);
     cudaFree(c->w);
     cudaFree(c->Q);
@@ -153,6 +167,14 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.ticket = c->ticket;
     a.col_offset = c->col_offset;
     a.send = c->comm != RBG_COMM_NONE ? c->send : nullptr;
+    a.peer_world = 0;
+    a.peer_rank = c->rank;
+    a.peer_slot = c->slot;
+    for (int q = 0; q < kMaxPeers; q++) a.peer_in[q] = nullptr;
+    if (c->comm == RBG_COMM_PEER) {
+        a.peer_world = c->world;
+        for (int q = 0; q < c->world; q++) a.peer_in[q] = c->peer_rec[q];
+    }
     return a;
 }
 
@@ -180,6 +202,9 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.xchg = c->comm != RBG_COMM_NONE;
     a.recv = c->recv;
     a.slot_bytes = c->slot;
+    a.peer_mine = c->comm == RBG_COMM_PEER ? c->peer_in : nullptr;
+    a.peer_slot = c->slot;
+    for (int q = 0; q < kMaxPeers; q++) a.peer_send[q] = q < c->world ? c->peer_send[q] : nullptr;
     return a;
 }
 
@@ -195,6 +220,10 @@ rbg_status enqueue_local(rbg_ctx *c) {
 }
 
 rbg_status enqueue_xchg(rbg_ctx *c) {
+    if (c->comm == RBG_COMM_PEER) {
+        CU(launch_peer_wait(c->peer_in, c->world, c->st, c->peer_timeout_ns, c->stream));
+        return RBG_OK;
+    }
     if (c->comm == RBG_COMM_NCCL) {
         const char *msg = nullptr;
         if (nccl_allgather_bytes(c->send, c->recv, c->slot, c->nccl, c->stream, &msg))
@@ -403,7 +432,10 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     // continues after rbg_add_columns)
     if (d->k_max < 1 || d->k_max > d->N)
         return fail(RBG_EINVAL, "k_max=%lld outside [1, N=%lld]", (long long)d->k_max, (long long)d->N);
-    if (world > 1 && d->comm == RBG_COMM_NONE) return fail(RBG_EINVAL, "world > 1 needs comm NCCL or EXTERNAL");
+    if (world > 1 && d->comm == RBG_COMM_NONE) return fail(RBG_EINVAL, "world > 1 needs comm NCCL, EXTERNAL or PEER");
+    if (d->comm < RBG_COMM_NONE || d->comm > RBG_COMM_PEER) return fail(RBG_EINVAL, "unknown comm %d", (int)d->comm);
+    if (d->comm == RBG_COMM_PEER && world > kMaxPeers)
+        return fail(RBG_EINVAL, "PEER exchange supports at most %d ranks", kMaxPeers);
     if (d->ortho != RBG_ORTHO_MGS && d->ortho != RBG_ORTHO_CGS) return fail(RBG_EINVAL, "unknown ortho %d", (int)d->ortho);
     if (d->residual != RBG_RESIDUAL_RECURRENCE && d->residual != RBG_RESIDUAL_EXPLICIT)
         return fail(RBG_EINVAL, "unknown residual mode %d", (int)d->residual);
@@ -547,7 +579,17 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(cudaMalloc(&c->ticket, sizeof(unsigned)));
     CUB(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
 
-    if (d->comm != RBG_COMM_NONE) {  // (world = 1 runs the same exchange path, e.g. in tests)
+    if (d->comm == RBG_COMM_PEER) {  // two send slots (by tag parity) + 2 x world records
+        c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;
+        CUB(cudaMalloc(&c->send, 2 * c->slot));
+        CUB(cudaMemsetAsync(c->send, 0, 2 * c->slot, c->stream));
+        CUB(cudaMalloc(&c->peer_in, sizeof(PeerRec) * 2 * world));
+        CUB(cudaMemsetAsync(c->peer_in, 0, sizeof(PeerRec) * 2 * world, c->stream));  // tag 0: none yet
+        c->peer_rec[c->rank] = c->peer_in;
+        c->peer_send[c->rank] = c->send;
+        c->peer_timeout_ns = (d->peer_timeout_ms > 0 ? d->peer_timeout_ms : 60000) * 1000000LL;
+        c->peer_connected = world == 1;
+    } else if (d->comm != RBG_COMM_NONE) {  // (world = 1 runs the same exchange path, e.g. in tests)
         c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;
         CUB(cudaMalloc(&c->send, c->slot));
         CUB(cudaMalloc(&c->recv, c->slot * world));
@@ -582,6 +624,7 @@ rbg_status rbg_create(rbg_ctx **ctx, const void *S, int64_t N, int64_t M, const 
 rbg_status rbg_step(rbg_ctx *c, int64_t n) {
     TRY(check_ctx(c));
     if (c->comm == RBG_COMM_EXTERNAL) return fail(RBG_ESTATE, "EXTERNAL contexts use rbg_iter_local/finish");
+    if (c->comm == RBG_COMM_PEER && !c->peer_connected) return fail(RBG_ESTATE, "PEER context not connected (rbg_peer_connect)");
     if (n < 0) return fail(RBG_EINVAL, "n < 0");
     return enqueue_n(c, n);
 }
@@ -589,6 +632,7 @@ rbg_status rbg_step(rbg_ctx *c, int64_t n) {
 rbg_status rbg_run(rbg_ctx *c) {
     TRY(check_ctx(c));
     if (c->comm == RBG_COMM_EXTERNAL) return fail(RBG_ESTATE, "EXTERNAL contexts use rbg_iter_local/finish");
+    if (c->comm == RBG_COMM_PEER && !c->peer_connected) return fail(RBG_ESTATE, "PEER context not connected (rbg_peer_connect)");
     const long long need = c->k_max + 1 - c->iters;
     if (need > 0) TRY(enqueue_n(c, need));
     CU(cudaStreamSynchronize(c->stream));
@@ -783,7 +827,9 @@ rbg_status rbg_get_stats(rbg_ctx *c, rbg_stats *o) {
 
 rbg_status rbg_iter_local(rbg_ctx *c) {
     TRY(check_ctx(c));
-    if (c->comm != RBG_COMM_EXTERNAL || c->local_pending) return fail(RBG_ESTATE, "iter_local out of order");
+    if ((c->comm != RBG_COMM_EXTERNAL && c->comm != RBG_COMM_PEER) || c->local_pending)
+        return fail(RBG_ESTATE, "iter_local out of order");
+    if (c->comm == RBG_COMM_PEER && !c->peer_connected) return fail(RBG_ESTATE, "PEER context not connected");
     TRY(enqueue_local(c));
     c->local_pending = true;
     return RBG_OK;
@@ -791,7 +837,9 @@ rbg_status rbg_iter_local(rbg_ctx *c) {
 
 rbg_status rbg_iter_finish(rbg_ctx *c) {
     TRY(check_ctx(c));
-    if (c->comm != RBG_COMM_EXTERNAL || !c->local_pending) return fail(RBG_ESTATE, "iter_finish out of order");
+    if ((c->comm != RBG_COMM_EXTERNAL && c->comm != RBG_COMM_PEER) || !c->local_pending)
+        return fail(RBG_ESTATE, "iter_finish out of order");
+    if (c->comm == RBG_COMM_PEER) TRY(enqueue_xchg(c));  // wait for the peers' records
     TRY(enqueue_finish(c));
     c->local_pending = false;
     c->iters++;
@@ -818,6 +866,61 @@ rbg_status rbg_emulate_allgather(rbg_ctx **ctxs, int world) {
         for (int r = 0; r < world; r++)
             CU(cudaMemcpy(ctxs[p]->recv + (size_t)r * ctxs[p]->slot, ctxs[r]->send, ctxs[r]->slot,
                           cudaMemcpyDeviceToDevice));
+    return RBG_OK;
+}
+
+rbg_status rbg_peer_export(rbg_ctx *c, uint8_t out[RBG_PEER_HANDLE_BYTES]) {
+    TRY(check_ctx(c));
+    if (!out) return fail(RBG_EINVAL, "null output");
+    if (c->comm != RBG_COMM_PEER) return fail(RBG_ESTATE, "not a PEER context");
+    cudaIpcMemHandle_t h[2];
+    CU(cudaIpcGetMemHandle(&h[0], c->peer_in));
+    CU(cudaIpcGetMemHandle(&h[1], c->send));
+    static_assert(sizeof(cudaIpcMemHandle_t) * 2 == RBG_PEER_HANDLE_BYTES, "handle size");
+    std::memcpy(out, h, sizeof h);
+    return RBG_OK;
+}
+
+rbg_status rbg_peer_connect(rbg_ctx *c, const uint8_t *all) {
+    TRY(check_ctx(c));
+    if (!all) return fail(RBG_EINVAL, "null handle list");
+    if (c->comm != RBG_COMM_PEER) return fail(RBG_ESTATE, "not a PEER context");
+    if (c->peer_connected) return fail(RBG_ESTATE, "already connected");
+    for (int q = 0; q < c->world; q++) {
+        if (q == c->rank) continue;  // own buffers: direct pointers
+        cudaIpcMemHandle_t h[2];
+        std::memcpy(h, all + (size_t)q * RBG_PEER_HANDLE_BYTES, sizeof h);
+        void *rec = nullptr, *snd = nullptr;
+        CU(cudaIpcOpenMemHandle(&rec, h[0], cudaIpcMemLazyEnablePeerAccess));
+        cudaError_t e = cudaIpcOpenMemHandle(&snd, h[1], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaIpcCloseMemHandle(rec);
+            return fail(RBG_ECUDA, "cudaIpcOpenMemHandle (rank %d send slots): %s", q, cudaGetErrorString(e));
+        }
+        c->peer_rec[q] = static_cast<PeerRec *>(rec);
+        c->peer_send[q] = static_cast<unsigned char *>(snd);
+        c->peer_ipc[q] = true;
+    }
+    c->peer_connected = true;
+    return RBG_OK;
+}
+
+rbg_status rbg_peer_connect_local(rbg_ctx **ctxs, int world) {
+    if (!ctxs || world < 1 || world > kMaxPeers) return fail(RBG_EINVAL, "bad context list");
+    for (int p = 0; p < world; p++)
+        if (!ctxs[p] || ctxs[p]->comm != RBG_COMM_PEER || ctxs[p]->world != world || ctxs[p]->rank != p ||
+            ctxs[p]->peer_connected && world > 1)
+            return fail(RBG_EINVAL, "context %d is not an unconnected rank %d of a %d-rank PEER group", p, p, world);
+    for (int p = 1; p < world; p++)  // one stream: rank p's wait never runs beside a sweep it waits for
+        if (ctxs[p]->stream != ctxs[0]->stream || ctxs[p]->device != ctxs[0]->device)
+            return fail(RBG_EINVAL, "local PEER contexts must share one device and one stream");
+    for (int p = 0; p < world; p++) {
+        for (int q = 0; q < world; q++) {
+            ctxs[p]->peer_rec[q] = ctxs[q]->peer_in;
+            ctxs[p]->peer_send[q] = ctxs[q]->send;
+        }
+        ctxs[p]->peer_connected = true;
+    }
     return RBG_OK;
 }
 

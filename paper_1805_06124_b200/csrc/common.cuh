@@ -15,7 +15,8 @@ constexpr int kImgsThreads = 256;   // threads per IMGS CTA
 constexpr int kLaneImgs = kImgsCtas * kImgsThreads;  // L_I = 2048
 constexpr int kNuMax = 5;           // IMGS sweep cap (R7)
 
-constexpr int kStopNone = 0, kStopTol = 1, kStopKmax = 2, kStopRank = 3, kStopAll = 4;
+constexpr int kStopNone = 0, kStopTol = 1, kStopKmax = 2, kStopRank = 3, kStopAll = 4, kStopPeer = 5;
+constexpr int kMaxPeers = 8;        // ranks of a PEER exchange (one NVSwitch box)
 
 // One maxloc record: 16 bytes, total order (m descending, j ascending).
 struct __align__(16) Rec {
@@ -26,6 +27,17 @@ struct __align__(16) Rec {
 __device__ __forceinline__ bool rec_better(double m1, long long j1, double m2, long long j2) {
     return (m1 > m2) || (m1 == m2 && j1 < j2);
 }
+
+// PEER exchange: rank p's sweep writes its local maxloc into slot
+// (parity, p) of EVERY rank's record array over NVLink (P2P stores), then the tag with release
+// semantics; tag = st->k + 1 of the sweep (unique per iteration), parity = tag & 1 (records of
+// consecutive iterations never share a slot).
+struct __align__(32) PeerRec {
+    double m;
+    long long j;                  // global column index
+    unsigned long long tag;
+    long long pad;
+};
 
 // Device-resident loop state (one per context).
 struct DevState {
@@ -143,6 +155,43 @@ __device__ __forceinline__ double2 ld_stream(const double2 *p, uint64_t pol) {
                  : "=d"(r.x), "=d"(r.y)
                  : "l"(p), "l"(pol));
     return r;
+}
+
+// System-scope release store / acquire load (flags written and polled across GPUs).
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_f64(double *p, double v) {
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_s64(long long *p, long long v) {
+    asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_sys_f64(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ long long ld_relaxed_sys_s64(const long long *p) {
+    long long v;
+    asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// 16-byte load that bypasses L1 (data written by another GPU since the last kernel).
+__device__ __forceinline__ double2 ld_cv(const double2 *p) {
+    double2 r;
+    asm volatile("ld.global.cv.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {

@@ -222,22 +222,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     // ---- a3: pivot decision (identical in every CTA and on every rank) ------------------
     double m;
     long long J;
-    int owner = 0;
-    if (!a.xchg) {
-        m = a.st->m_loc;
-        J = a.st->j_loc;
-    } else {
-        m = -INFINITY;
-        J = 0x7fffffffffffffffLL;
-        for (int p = 0; p < a.world; p++) {
-            const Rec *r = reinterpret_cast<const Rec *>(a.recv + (size_t)p * a.slot_bytes);
-            if (rec_better(r->m, r->j, m, J)) {
-                m = r->m;
-                J = r->j;
-                owner = p;
-            }
-        }
-    }
+    const double2 *src;
+    pivot_decision(a, k, m, J, src);
     const double err = sqrt(fmax(m, 0.0));  // CAC rule 8
     int why = kStopNone;
     if (m == -INFINITY) why = kStopAll;
@@ -276,15 +262,11 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     }
 
     // ---- a5: Hoffmann IMGS (CAC rule 9) ---------------------------------------------
-    const double2 *src = !a.xchg
-                             ? a.S + (J - a.col_offset) * a.ldv
-                             : reinterpret_cast<const double2 *>(a.recv + (size_t)owner * a.slot_bytes +
-                                                                 sizeof(Rec));
     double2 v[MAXV];
 #pragma unroll
     for (int mm = 0; mm < MAXV; mm++) {
         const int u = u0 + mm * kLaneImgs;
-        v[mm] = (mm < nm) ? src[u] : make_double2(0.0, 0.0);
+        v[mm] = (mm < nm) ? (a.peer_mine ? ld_cv(src + u) : src[u]) : make_double2(0.0, 0.0);
         if (odd_tail && u == nvec - 1) v[mm].y = 0.0;
     }
 

@@ -139,22 +139,8 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
     // ---- pivot decision (identical in every CTA) ------------------------------------
     double m;
     long long J;
-    int owner = 0;
-    if (!a.xchg) {
-        m = a.st->m_loc;
-        J = a.st->j_loc;
-    } else {
-        m = -INFINITY;
-        J = 0x7fffffffffffffffLL;
-        for (int p = 0; p < a.world; p++) {
-            const Rec *r = reinterpret_cast<const Rec *>(a.recv + (size_t)p * a.slot_bytes);
-            if (rec_better(r->m, r->j, m, J)) {
-                m = r->m;
-                J = r->j;
-                owner = p;
-            }
-        }
-    }
+    const double2 *src;
+    pivot_decision(a, k, m, J, src);
     const double err = sqrt(fmax(m, 0.0));
     int why = kStopNone;
     if (m == -INFINITY) why = kStopAll;
@@ -168,10 +154,8 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
         return;
     }
 
-    const double2 *src = !a.xchg ? a.S + (J - a.col_offset) * a.ldv
-                                 : reinterpret_cast<const double2 *>(a.recv + (size_t)owner * a.slot_bytes + sizeof(Rec));
     for (long long u = gtid; u < nvec; u += nthr) {
-        double2 x = src[u];
+        double2 x = a.peer_mine ? ld_cv(src + u) : src[u];
         if (odd_tail && u == nvec - 1) x.y = 0.0;
         vbuf[u] = x;
     }

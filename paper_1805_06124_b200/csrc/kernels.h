@@ -1,5 +1,6 @@
 // kernels.h -- host-visible launch interface of the rbg device kernels (internal).
 #pragma once
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -28,6 +29,11 @@ struct SweepArgs {
     unsigned *ticket;      // last-CTA-done counter (returns to 0)
     long long col_offset;  // global index of local column 0
     unsigned char *send;   // exchange slot of this rank (NULL on one GPU)
+    // PEER exchange (peer_world > 0): every rank's record array, this rank's index, and the
+    // byte size of one of the two send slots (the candidate goes to slot tag & 1)
+    PeerRec *peer_in[kMaxPeers];
+    int peer_world, peer_rank;
+    size_t peer_slot;
 };
 
 // Pivot decision + iterated MGS (a3 finalize, a5, a6).
@@ -51,7 +57,57 @@ struct ImgsArgs {
     bool xchg;                  // decision from the exchanged records (any world size)
     const unsigned char *recv;  // world slots of xchg_slot_bytes(nvec)
     size_t slot_bytes;
+    // PEER exchange: this rank's record array (written by every rank's sweep) and every
+    // rank's two send slots (P2P-mapped); NULL otherwise
+    const PeerRec *peer_mine;
+    const unsigned char *peer_send[kMaxPeers];
+    size_t peer_slot;
 };
+
+// Pivot decision (a3) from this rank's maxloc, the all-gathered slots (NCCL / EXTERNAL) or the
+// PEER records; `src` = the pivot column (local S, a received slot, or the owner's send slot
+// over NVLink, read with ld_cv).  Identical bits on every CTA and every rank.
+__device__ __forceinline__ void pivot_decision(const ImgsArgs &a, long long k, double &m, long long &J,
+                                               const double2 *&src) {
+    if (a.peer_mine) {
+        const int par = (int)((k + 1) & 1);
+        m = -INFINITY;
+        J = 0x7fffffffffffffffLL;
+        int owner = 0;
+        for (int p = 0; p < a.world; p++) {
+            const PeerRec *r = a.peer_mine + par * a.world + p;
+            const double rm = ld_relaxed_sys_f64(&r->m);
+            const long long rj = ld_relaxed_sys_s64(&r->j);
+            if (rec_better(rm, rj, m, J)) {
+                m = rm;
+                J = rj;
+                owner = p;
+            }
+        }
+        src = reinterpret_cast<const double2 *>(a.peer_send[owner] + (size_t)par * a.peer_slot + sizeof(Rec));
+    } else if (!a.xchg) {
+        m = a.st->m_loc;
+        J = a.st->j_loc;
+        src = a.S + (J - a.col_offset) * a.ldv;
+    } else {
+        m = -INFINITY;
+        J = 0x7fffffffffffffffLL;
+        int owner = 0;
+        for (int p = 0; p < a.world; p++) {
+            const Rec *r = reinterpret_cast<const Rec *>(a.recv + (size_t)p * a.slot_bytes);
+            if (rec_better(r->m, r->j, m, J)) {
+                m = r->m;
+                J = r->j;
+                owner = p;
+            }
+        }
+        src = reinterpret_cast<const double2 *>(a.recv + (size_t)owner * a.slot_bytes + sizeof(Rec));
+    }
+}
+
+// PEER exchange wait (a4): until every rank's record of this iteration has arrived (tag), or
+// timeout_ns passed (then stop = PEER_TIMEOUT).  One warp; no-op once stopped.
+cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, long long timeout_ns, cudaStream_t s);
 
 struct SweepConfig {
     int grid, threads;

@@ -73,6 +73,13 @@ __device__ __forceinline__ double2 load_e(const double2 *E, const double *Ew, lo
     return ESMEM ? E[u] : __ldg(E + u);
 }
 
+// This sweep's send slot: PEER keeps two (by the parity of the record tag st->k + 1), so a
+// slot is rewritten only after every peer has consumed it.
+__device__ __forceinline__ unsigned char *send_slot(const SweepArgs &a) {
+    if (a.peer_world == 0) return a.send;
+    return a.send + (size_t)((a.st->k + 1) & 1) * a.peer_slot;
+}
+
 // CTA maxloc of the warps' bests, then the last CTA to finish (atomic ticket) reduces the
 // per-CTA records with the total order into the device state and, on a sharded run, packs
 // the local candidate column into the exchange slot.
@@ -131,22 +138,40 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
             a.st->j_loc = jg;
             *a.ticket = 0u;
             if (a.send) {
-                Rec *h = reinterpret_cast<Rec *>(a.send);
+                Rec *h = reinterpret_cast<Rec *>(send_slot(a));
                 h->m = bm;
                 h->j = jg;
             }
+            s_m[1] = bm;
+            s_j[1] = jg;
         }
         if (a.send) s_j[0] = bj;
     }
-    if (a.send) {  // pack the local candidate column for the all-gather
+    if (a.send) {  // pack the local candidate column for the all-gather / the peers
         __syncthreads();
         const long long bj = s_j[0];
-        double2 *dst = reinterpret_cast<double2 *>(a.send + sizeof(Rec));
+        double2 *dst = reinterpret_cast<double2 *>(send_slot(a) + sizeof(Rec));
         const bool valid = bj >= 0 && bj < a.M;
         for (long long u = tid; u < nvec; u += kSweepThreads) {
             double2 x = valid ? a.S[bj * a.ldv + u] : make_double2(0.0, 0.0);
             if (odd_tail && u == nvec - 1) x.y = 0.0;
             dst[u] = x;
+        }
+        if (a.peer_world > 0) {
+            // PEER: the column is in place (CTA barrier), make it and the record visible to
+            // every GPU, then publish the record in every rank's array and release the tag
+            __syncthreads();
+            if (tid == 0) {
+                const unsigned long long tag = (unsigned long long)a.st->k + 1;
+                const int par = (int)(tag & 1);
+                __threadfence_system();
+                for (int q = 0; q < a.peer_world; q++) {
+                    PeerRec *r = a.peer_in[q] + par * a.peer_world + a.peer_rank;
+                    st_relaxed_sys_f64(&r->m, s_m[1]);
+                    st_relaxed_sys_s64(&r->j, s_j[1]);
+                    st_release_sys(&r->tag, tag);
+                }
+            }
         }
     }
 }

@@ -3,8 +3,10 @@
 One process per GPU; torch.distributed supplies the process group (NCCL on GPUs, gloo in
 the CPU tests) and is used only for setup: the column partition, the broadcast of the
 NCCL unique id that the library's own communicator is built from, and max-over-ranks
-timing.  The per-iteration exchange (one ncclAllGather of a {maxloc record, candidate
-column} slot per rank) happens inside librbg.so on the library's stream.
+timing, and (PEER mode) the one-time all-gather of every rank's CUDA-IPC handles.  The
+per-iteration exchange happens inside librbg.so on the library's stream: PEER = P2P stores
+of the maxloc records from the sweep kernel and NVLink reads of the pivot column by IMGS;
+NCCL = one ncclAllGather of a {maxloc record, candidate column} slot per rank.
 
 The paper distributes columns over "pivot cores" ("distributing N/P
 columns" read as M/P, reading R11); here contiguous blocks, the last ranks taking the
@@ -50,9 +52,25 @@ def max_over_ranks(x: float, group=None, device=None) -> float:
     return float(t.item())
 
 
-def sharded_context(S_local, w, tol: float, k_max: int, M_global: int, group=None, **kw):
-    """rbg.Context for this rank's column block, wired to an NCCL communicator shared by the
-    ranks of `group`.  S_local must be this rank's partition(M_global, world, rank) block."""
+def all_gather_bytes(payload: bytes, group=None) -> list[bytes]:
+    """Every rank's `payload` (e.g. its PEER CUDA-IPC handles), in rank order."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, payload, group=group)
+    return out
+
+
+def connect_peers(ctx, group=None):
+    """PEER exchange setup: all-gather every rank's IPC handles and map them."""
+    ctx.peer_connect(all_gather_bytes(ctx.peer_export(), group))
+    return ctx
+
+
+def sharded_context(S_local, w, tol: float, k_max: int, M_global: int, group=None, comm: str = "peer", **kw):
+    """rbg.Context for this rank's column block of a `group`-wide sharded greedy.  comm="peer":
+    records and the pivot column move over NVLink inside the kernels (CUDA IPC); "nccl": one
+    ncclAllGather per iteration on a communicator shared by the ranks.  S_local must be this
+    rank's partition(M_global, world, rank) block."""
     import torch.distributed as dist
     from . import rbg
     world = dist.get_world_size(group)
@@ -62,6 +80,12 @@ def sharded_context(S_local, w, tol: float, k_max: int, M_global: int, group=Non
         raise ValueError(f"rank {rank} holds {S_local.shape[0]} columns, partition says {m_loc}")
     if world == 1:
         return rbg.Context(S_local, w, tol, k_max, **kw)
+    if comm == "peer":
+        ctx = rbg.Context(S_local, w, tol, k_max, comm=rbg.COMM_PEER, rank=rank, world=world,
+                          col_offset=off, M_global=M_global, **kw)
+        return connect_peers(ctx, group)
+    if comm != "nccl":
+        raise ValueError(f"comm must be 'peer' or 'nccl', not {comm!r}")
     uid = nccl_unique_id(group)
     return rbg.Context(S_local, w, tol, k_max, comm=rbg.COMM_NCCL, rank=rank, world=world,
                        col_offset=off, M_global=M_global, nccl_id=uid, **kw)

@@ -22,10 +22,11 @@ LIB_PATH = os.path.join(PKG, "librbg.so")
 
 OK, EINVAL, ENONFINITE, ENOMEM, ECUDA, ENCCL, ESTATE = range(7)
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENONFINITE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
-STOP = {0: "NONE", 1: "TOL", 2: "KMAX", 3: "RANK", 4: "ALL_SELECTED"}
+STOP = {0: "NONE", 1: "TOL", 2: "KMAX", 3: "RANK", 4: "ALL_SELECTED", 5: "PEER_TIMEOUT"}
 REAL_F64, COMPLEX_F64 = 1, 2
 MEM_HOST, MEM_DEVICE = 0, 1
-COMM_NONE, COMM_NCCL, COMM_EXTERNAL = 0, 1, 2
+COMM_NONE, COMM_NCCL, COMM_EXTERNAL, COMM_PEER = 0, 1, 2, 3
+PEER_HANDLE_BYTES = 128
 ORTHO = {"mgs": 0, "cgs": 1}
 RESIDUAL = {"recurrence": 0, "explicit": 1}
 
@@ -45,7 +46,7 @@ class Desc(ctypes.Structure):
         ("device", ctypes.c_int), ("check_finite", ctypes.c_int), ("comm", ctypes.c_int),
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("col_offset", ctypes.c_int64),
         ("M_global", ctypes.c_int64), ("nccl_id", ctypes.c_uint8 * 128), ("ortho", ctypes.c_int),
-        ("residual", ctypes.c_int),
+        ("residual", ctypes.c_int), ("peer_timeout_ms", ctypes.c_int64),
     ]
 
 
@@ -83,6 +84,9 @@ SYMBOLS = {
     "rbg_iter_finish": ([_P], ctypes.c_int),
     "rbg_xchg_buffers": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "rbg_emulate_allgather": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
+    "rbg_peer_export": ([_P, ctypes.POINTER(ctypes.c_uint8)], ctypes.c_int),
+    "rbg_peer_connect": ([_P, ctypes.POINTER(ctypes.c_uint8)], ctypes.c_int),
+    "rbg_peer_connect_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
     "rbg_lanes": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], None),
     "rbg_version": ([], ctypes.c_char_p),
     "rbg_last_error": ([], ctypes.c_char_p),
@@ -159,7 +163,8 @@ class Context:
     def __init__(self, S, w=None, tol: float = 0.0, k_max: int = 1, *, stream=None,
                  comm: int = COMM_NONE, rank: int = 0, world: int = 1, col_offset: int = 0,
                  M_global: int = 0, nccl_id: bytes | None = None, check_finite: bool = True,
-                 borrow: bool = True, ortho: str = "mgs", residual: str = "recurrence"):
+                 borrow: bool = True, ortho: str = "mgs", residual: str = "recurrence",
+                 peer_timeout_ms: int = 0):
         L = lib()
         d = Desc()
         L.rbg_desc_init(ctypes.byref(d))
@@ -216,6 +221,7 @@ class Context:
         d.ortho = ORTHO[ortho]
         d.residual = RESIDUAL[residual]
         d.comm = comm
+        d.peer_timeout_ms = int(peer_timeout_ms)
         d.rank = rank
         d.world = world
         d.col_offset = col_offset
@@ -388,6 +394,20 @@ class Context:
         B = buf[:k * k].reshape((k, k), order="F")
         return nodes[:k], (B if self.cplx else B.real.copy())
 
+    def peer_export(self) -> bytes:
+        """This rank's CUDA-IPC handles for the PEER exchange (rbg_peer_export)."""
+        buf = (ctypes.c_uint8 * PEER_HANDLE_BYTES)()
+        _check(lib().rbg_peer_export(self.h, buf))
+        return bytes(buf)
+
+    def peer_connect(self, handles: list[bytes]):
+        """Map every rank's PEER buffers; ``handles[p]`` = rank p's peer_export()."""
+        blob = b"".join(handles)
+        if len(blob) != PEER_HANDLE_BYTES * len(handles):
+            raise ValueError("each handle blob must be PEER_HANDLE_BYTES long")
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(lib().rbg_peer_connect(self.h, buf))
+
     def xchg_buffers(self):
         s, r, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().rbg_xchg_buffers(self.h, ctypes.byref(s), ctypes.byref(r), ctypes.byref(n)))
@@ -419,6 +439,12 @@ def enrich(ctx: Context, V, tol: float, rounds: int = 3):
     err = ctx.validate(Vh)
     history.append(float(err.max()) if err.size else 0.0)
     return history, bool(np.all(err < tol))
+
+
+def peer_connect_local(ctxs: list[Context]):
+    """Wire PEER contexts of this process (one device, one stream) to each other (tests)."""
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.h for c in ctxs])
+    _check(lib().rbg_peer_connect_local(arr, len(ctxs)))
 
 
 def emulate_allgather(ctxs: list[Context]):

@@ -232,6 +232,99 @@ def test_nccl_exchange_path_world1(rbg, orc):
         compare(ctx.result(), o)
 
 
+def _peer_group(rbg, S, w, tol, k_max, world, stream, **kw):
+    M = S.shape[0]
+    bounds = [M * p // world for p in range(world + 1)]
+    ctxs = [rbg.Context(S[bounds[p]:bounds[p + 1]], w, tol, k_max, stream=stream, comm=rbg.COMM_PEER,
+                        rank=p, world=world, col_offset=bounds[p], M_global=M, peer_timeout_ms=20000, **kw)
+            for p in range(world)]
+    if world > 1:
+        rbg.peer_connect_local(ctxs)
+    return ctxs
+
+
+@pytest.mark.parametrize("world,ortho", [(1, "mgs"), (2, "mgs"), (3, "mgs"), (4, "mgs"), (2, "cgs")])
+def test_peer_exchange_on_one_gpu(rbg, orc, world, ortho):
+    """comm = PEER (no collective library): each rank's sweep stores its maxloc record into
+    every rank's record array with release-tagged stores, the wait kernel acquires the tags,
+    the replicated IMGS reads the winner's column from the owner's send slot (two slots by
+    tag parity).  The ranks share one stream and are driven local-on-all then finish-on-all,
+    so no kernel ever waits for one that has not been launched.  Bit-identical to the oracle."""
+    import torch
+    S, w, tol, k_max = inputs.config1(M=3001, N=700)
+    lanes = orc.CANONICAL_CGS if ortho == "cgs" else orc.CANONICAL
+    o = orc.greedy(S, w, tol, k_max, lanes=lanes, ortho=ortho)
+    stream = torch.cuda.Stream()
+    ctxs = _peer_group(rbg, S, w, tol, k_max, world, stream.cuda_stream, ortho=ortho)
+    for _ in range(k_max + 1):
+        for c in ctxs:
+            c.iter_local()
+        for c in ctxs:
+            c.iter_finish()
+    res = [c.result() for c in ctxs]
+    for r in res:
+        assert (r.k, r.stop) == (o.k, o.stop)
+        np.testing.assert_array_equal(r.pivots, o.pivots)
+        np.testing.assert_array_equal(r.errors, o.errors)
+        np.testing.assert_array_equal(r.nu, o.nu)
+        np.testing.assert_array_equal(r.Q, o.Q)
+    np.testing.assert_array_equal(np.concatenate([r.R for r in res], axis=1), o.R)
+    np.testing.assert_array_equal(np.concatenate([r.r2 for r in res]), o.r2)
+    for c in ctxs:
+        c.close()
+
+
+def test_peer_world1_run_and_graphs(rbg, orc):
+    """A one-rank PEER context is connected at create: rbg_run and CUDA-graph batches (the
+    wait kernel captured with the sweep and IMGS) give the oracle's bits; the exchange phase
+    is timed as C_j."""
+    S, w, tol, k_max = inputs.config1(M=2500, N=800)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    with rbg.Context(S, w, tol, k_max, comm=rbg.COMM_PEER, rank=0, world=1) as ctx:
+        ctx.set_timing(True)
+        ctx.run()
+        compare(ctx.result(), o)
+        assert ctx.stats().t_xchg_ms > 0.0
+    with rbg.Context(S, w, tol, k_max, comm=rbg.COMM_PEER, rank=0, world=1) as ctx:
+        ctx.set_graph_batch(8)
+        ctx.run()
+        compare(ctx.result(), o)
+
+
+def test_peer_setup_errors_and_timeout(rbg):
+    """Unconnected PEER ranks refuse to run; local wiring needs one stream; a rank whose
+    peer never publishes its record stops PEER_TIMEOUT after peer_timeout_ms instead of
+    hanging (the wait kernel is bounded)."""
+    import torch
+    S, w, tol, k_max = inputs.config1(M=400, N=300)
+    a = rbg.Context(S[:200], w, tol, 10, comm=rbg.COMM_PEER, rank=0, world=2, col_offset=0, M_global=400)
+    b = rbg.Context(S[200:], w, tol, 10, comm=rbg.COMM_PEER, rank=1, world=2, col_offset=200, M_global=400)
+    with pytest.raises(rbg.RbgError) as e:
+        a.step(1)
+    assert e.value.status == rbg.ESTATE
+    with pytest.raises(rbg.RbgError) as e:
+        rbg.peer_connect_local([a, b])          # two library-owned streams
+    assert e.value.status == rbg.EINVAL
+    assert len(a.peer_export()) == rbg.PEER_HANDLE_BYTES
+    a.close()
+    b.close()
+    stream = torch.cuda.Stream()
+    ctxs = _peer_group(rbg, S, w, tol, 10, 2, stream.cuda_stream)
+    for c in ctxs:
+        c.close()
+    a = rbg.Context(S[:200], w, tol, 10, stream=stream.cuda_stream, comm=rbg.COMM_PEER, rank=0, world=2,
+                    col_offset=0, M_global=400, peer_timeout_ms=200)
+    b = rbg.Context(S[200:], w, tol, 10, stream=stream.cuda_stream, comm=rbg.COMM_PEER, rank=1, world=2,
+                    col_offset=200, M_global=400, peer_timeout_ms=200)
+    rbg.peer_connect_local([a, b])
+    a.iter_local()                               # rank 1 never sweeps
+    a.iter_finish()
+    k, _, why = a.info()
+    assert (k, why) == (0, "PEER_TIMEOUT")
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("case", ["cfg0", "cfg1", "cfg2", "cfg4", "ragged_real", "ragged_cplx"])
 def test_cgs_variant_parity(rbg, orc, case):
     """Hoffmann CGSCI orthogonalisation (rbg_desc.ortho = CGS) against the oracle's CGS mode
