@@ -830,7 +830,17 @@ rbg_status rbg_iter_local(rbg_ctx *c) {
     if ((c->comm != RBG_COMM_EXTERNAL && c->comm != RBG_COMM_PEER) || c->local_pending)
         return fail(RBG_ESTATE, "iter_local out of order");
     if (c->comm == RBG_COMM_PEER && !c->peer_connected) return fail(RBG_ESTATE, "PEER context not connected");
+    PhaseEvents *pe = nullptr;
+    if (c->timing) {  // the same per-phase events as enqueue_iteration
+        PhaseEvents p;
+        for (int i = 0; i < 4; i++) CU(cudaEventCreate(&p.e[i]));
+        c->ev.push_back(p);
+        c->ev_iter.push_back(c->iters);
+        pe = &c->ev.back();
+        CU(cudaEventRecord(pe->e[0], c->stream));
+    }
     TRY(enqueue_local(c));
+    if (pe) CU(cudaEventRecord(pe->e[1], c->stream));
     c->local_pending = true;
     return RBG_OK;
 }
@@ -839,8 +849,11 @@ rbg_status rbg_iter_finish(rbg_ctx *c) {
     TRY(check_ctx(c));
     if ((c->comm != RBG_COMM_EXTERNAL && c->comm != RBG_COMM_PEER) || !c->local_pending)
         return fail(RBG_ESTATE, "iter_finish out of order");
+    const bool timed = c->timing && !c->ev.empty() && c->ev_iter.back() == c->iters;
     if (c->comm == RBG_COMM_PEER) TRY(enqueue_xchg(c));  // wait for the peers' records
+    if (timed) CU(cudaEventRecord(c->ev.back().e[2], c->stream));
     TRY(enqueue_finish(c));
+    if (timed) CU(cudaEventRecord(c->ev.back().e[3], c->stream));
     c->local_pending = false;
     c->iters++;
     return RBG_OK;

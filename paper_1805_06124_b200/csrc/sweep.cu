@@ -98,7 +98,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
     if (tid == 0) {
         double bm = s_m[0];
         long long bj = s_j[0];
-        for (int w = 1; w < kSweepWarps; w++)
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
             if (rec_better(s_m[w], s_j[w], bm, bj)) {
                 bm = s_m[w];
                 bj = s_j[w];
@@ -152,7 +152,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
         const long long bj = s_j[0];
         double2 *dst = reinterpret_cast<double2 *>(send_slot(a) + sizeof(Rec));
         const bool valid = bj >= 0 && bj < a.M;
-        for (long long u = tid; u < nvec; u += kSweepThreads) {
+        for (long long u = tid; u < nvec; u += blockDim.x) {
             double2 x = valid ? a.S[bj * a.ldv + u] : make_double2(0.0, 0.0);
             if (odd_tail && u == nvec - 1) x.y = 0.0;
             dst[u] = x;
