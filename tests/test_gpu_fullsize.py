@@ -74,3 +74,91 @@ def test_config2_full_size_sampled(orc):
         assert out[3] == nu[kk]
     del S
     torch.cuda.empty_cache()
+
+
+def test_config4_full_size_bit_exact(orc):
+    """Config 4 at full size (real 4,096 x 65,536, exact rank 512, sigma_i = 10^(-i/25),
+    nonuniform weights, tol 1e-13, k_max 512): the whole greedy against the canonical-mode
+    oracle -- pivots, stop reason, errors, Q, R, r2, nu bit for bit (BASELINE.json: pivots
+    bit-exact on all five configs)."""
+    from paper_1805_06124_b200 import inputs, rbg
+
+    S, w, tol, k_max, _ = inputs.config4()
+    g = rbg.greedy(S, w, tol, k_max)
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    assert (g.k, g.stop) == (o.k, o.stop)
+    assert g.stop == "RANK"                                  # the recurrence floor (R8, R17)
+    np.testing.assert_array_equal(g.pivots, o.pivots)
+    np.testing.assert_array_equal(g.nu, o.nu)
+    np.testing.assert_array_equal(g.errors, o.errors)
+    np.testing.assert_array_equal(g.Q, o.Q)
+    np.testing.assert_array_equal(g.R, o.R)
+    np.testing.assert_array_equal(g.r2, o.r2)
+
+
+def test_config3_two_shards_full_size_on_one_gpu(orc):
+    """Config 3's per-GPU shard size at P = 2 (10,000 x 819,200 complex, 131 GB, k_max 300),
+    run on one GPU: the two PEER ranks (one process, one stream, local wiring; each rank's
+    kernels are the ones a 2-GPU run launches) against one P = 1 context over the same
+    131 GB -- pivots, errors, nu, Q, and the concatenated R and r2 bit for bit -- plus
+    oracle-sampled R entries and IMGS vectors."""
+    import torch
+
+    from paper_1805_06124_b200 import dist as D
+    from paper_1805_06124_b200 import inputs, rbg
+
+    N, M_loc, P, k_max = 10000, 409600, 2, 300
+    M = M_loc * P
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info()
+    if free < 138e9:
+        pytest.skip(f"needs ~136 GB of device memory ({free / 1e9:.0f} of {total / 1e9:.0f} GB free)")
+    t = inputs.chirp_grid(N)
+    w = inputs.simpson_weights(N)
+    q, chi, psi = inputs.chirp_params(M, 3, spin=True)
+    S = torch.empty((M, N), dtype=torch.complex128, device="cuda")
+    for a in range(0, M, M_loc):                               # generator call per shard
+        rbg.gen_chirp(S[a:a + M_loc], t, w, q[a:a + M_loc], chi[a:a + M_loc], psi[a:a + M_loc], spin=True)
+    with rbg.Context(S, w, 0.0, k_max) as ctx:
+        ctx.run()
+        ref = ctx.result()
+    assert (ref.k, ref.stop) == (k_max, "KMAX")
+    stream = torch.cuda.Stream()
+    ctxs = []
+    for p in range(P):
+        off, m = D.partition(M, P, p)
+        ctxs.append(rbg.Context(S[off:off + m], w, 0.0, k_max, stream=stream.cuda_stream, comm=rbg.COMM_PEER,
+                                rank=p, world=P, col_offset=off, M_global=M))
+    rbg.peer_connect_local(ctxs)
+    for _ in range(k_max + 1):
+        for c in ctxs:
+            c.iter_local()
+        for c in ctxs:
+            c.iter_finish()
+    res = [c.result() for c in ctxs]
+    for c in ctxs:
+        c.close()
+    for r in res:
+        assert (r.k, r.stop) == (ref.k, ref.stop)
+        np.testing.assert_array_equal(r.pivots, ref.pivots)
+        np.testing.assert_array_equal(r.errors, ref.errors)
+        np.testing.assert_array_equal(r.nu, ref.nu)
+        np.testing.assert_array_equal(r.Q, ref.Q)
+    np.testing.assert_array_equal(np.concatenate([r.R for r in res], axis=1), ref.R)
+    np.testing.assert_array_equal(np.concatenate([r.r2 for r in res]), ref.r2)
+    assert (ref.pivots >= M_loc).any() and (ref.pivots < M_loc).any()   # both ranks win pivots
+
+    L_S, L_I = orc.CANONICAL
+    rng = np.random.default_rng(11)
+    cols = np.unique(np.concatenate([rng.choice(M, 8, replace=False), [M_loc - 1, M_loc]]))
+    Sh = S[torch.as_tensor(cols, device="cuda")].cpu().numpy()
+    WQ = ref.Q * w[None, :]
+    for a, j in enumerate(cols):
+        for i in (0, 1, 150, k_max - 1):
+            assert orc.dot(WQ[i], Sh[a], L_S) == ref.R[i, j]
+    for kk in (0, 5, 299):
+        v = S[int(ref.pivots[kk])].cpu().numpy()
+        out = orc.imgs(ref.Q[:kk], v, w, L_I)
+        np.testing.assert_array_equal(out[0], ref.Q[kk])
+    del S
+    torch.cuda.empty_cache()
