@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     // ---- columns of this CTA ------------------------------------------------------
     const long long c_begin = (long long)blockIdx.x * a.M / gridDim.x;
     const long long c_end = (long long)(blockIdx.x + 1) * a.M / gridDim.x;
-    const uint64_t pol = policy_evict_first();
+    // explicit mode re-reads each column right after its first pass: keep the first pass's
+    // lines in L2 (evict-last) and demote them on the re-read and the write-back (evict-first)
+    const uint64_t pol = a.V ? policy_evict_last() : policy_evict_first();
+    const uint64_t pol_done = policy_evict_first();
 
     double best_m = -INFINITY;
     long long best_j = 0x7fffffffffffffffLL;
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
 #pragma unroll
                     for (int t = 0; t < 8; t++) {
                         const long long u = base + (long long)t * 32 + lane;
-                        xv[t] = (u < nvec) ? vcol[u] : make_double2(0.0, 0.0);
+                        xv[t] = (u < nvec) ? ld_keep(vcol + u, pol_done) : make_double2(0.0, 0.0);
                     }
 #pragma unroll
                     for (int t = 0; t < 8; t++) {
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
                                 x.y = fma(-re, e.y, x.y);
                             }
                             if (odd_tail && u == nvec - 1) x.y = 0.0;
-                            vcol[u] = x;
+                            st_keep(vcol + u, x, pol_done);
                             acc = fma(x.x, x.x, acc);
                             acc = fma(x.y, x.y, acc);
                         }
