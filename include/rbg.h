@@ -253,6 +253,14 @@ rbg_status rbg_peer_connect(rbg_ctx *ctx, const uint8_t *all_handles);
  * rank waits: no kernel ever waits for one that has not been launched). */
 rbg_status rbg_peer_connect_local(rbg_ctx **ctxs, int world);
 
+/* Out-of-bounds write detection (compute-sanitizer is closed on the GPU pool): while on, every
+ * device buffer the library allocates gets a 256-byte canary tail (0xA5), checked when the
+ * buffer is freed; buffers allocated while off are unaffected. */
+void rbg_debug_set_canary(int on);
+/* Canary violations so far, after checking every live canaried buffer now (synchronises the
+ * devices); if > 0, rbg_last_error() describes the first. */
+int64_t rbg_debug_canary_violations(void);
+
 /* Lane counts of the canonical arithmetic contract this build implements. */
 void rbg_lanes(int *L_S, int *L_I);
 const char *rbg_version(void);

@@ -124,25 +124,25 @@ void free_ctx(rbg_ctx *c) {
             cudaIpcCloseMemHandle(c->peer_rec[q]);
             cudaIpcCloseMemHandle(c->peer_send[q]);
         }
-    cudaFree(c->peer_in);
-    if (c->own_S) cudaFree(c->S);
-    cudaFree(c->w);
-    cudaFree(c->Q);
-    cudaFree(c->WQ);
-    cudaFree(c->R);
-    cudaFree(c->r2);
-    cudaFree(c->st);
-    cudaFree(c->errors);
-    cudaFree(c->rdiag);
-    cudaFree(c->piv);
-    cudaFree(c->nu);
-    cudaFree(c->recs);
-    cudaFree(c->ticket);
-    cudaFree(c->send);
-    cudaFree(c->recv);
-    cudaFree(c->cgs_v);
-    cudaFree(c->w_true);
-    cudaFree(c->cgs_c);
+    dfree(c->peer_in);
+    if (c->own_S) dfree(c->S);
+    dfree(c->w);
+    dfree(c->Q);
+    dfree(c->WQ);
+    dfree(c->R);
+    dfree(c->r2);
+    dfree(c->st);
+    dfree(c->errors);
+    dfree(c->rdiag);
+    dfree(c->piv);
+    dfree(c->nu);
+    dfree(c->recs);
+    dfree(c->ticket);
+    dfree(c->send);
+    dfree(c->recv);
+    dfree(c->cgs_v);
+    dfree(c->w_true);
+    dfree(c->cgs_c);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -315,24 +315,24 @@ rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld,
     if (ld < c->N) return fail(RBG_EINVAL, "ld=%lld < N=%lld", ld, c->N);
     const size_t pitch = (size_t)c->nvec * 16, col_bytes = (size_t)c->N * c->se;
     double2 *d = nullptr;
-    CU(cudaMalloc(&d, pitch * Mb));
+    CU(dmalloc(&d, pitch * Mb));
     const cudaMemcpyKind kind = mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     cudaError_t e = cudaSuccess;
     if (pitch != col_bytes) e = cudaMemsetAsync(d, 0, pitch * Mb, c->stream);
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(d, pitch, src, (size_t)ld * c->se, col_bytes, Mb, kind, c->stream);
     unsigned long long *bad = nullptr, hbad = ~0ull;
-    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof *bad);
+    if (e == cudaSuccess) e = dmalloc(&bad, sizeof *bad);
     if (e == cudaSuccess) e = cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = launch_check_finite(d, c->nvec, Mb, c->N, c->nvec, c->cplx, bad, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(bad);
+    dfree(bad);
     if (e != cudaSuccess) {
-        cudaFree(d);
+        dfree(d);
         return fail(RBG_ECUDA, "uploading a column block: %s", cudaGetErrorString(e));
     }
     if (hbad != ~0ull) {
-        cudaFree(d);
+        dfree(d);
         return fail(RBG_ENONFINITE, "non-finite entry at (row %lld, col %lld)", (long long)(hbad % c->N),
                     (long long)(hbad / c->N));
     }
@@ -348,9 +348,9 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     Rec *recs = nullptr;
     unsigned *ticket = nullptr;
     const int grid = std::max(c->cfg_init.grid, c->cfg_sweep.grid);
-    cudaError_t e = cudaMalloc(&vst, sizeof(DevState));
-    if (e == cudaSuccess) e = cudaMalloc(&recs, sizeof(Rec) * grid);
-    if (e == cudaSuccess) e = cudaMalloc(&ticket, sizeof(unsigned));
+    cudaError_t e = dmalloc(&vst, sizeof(DevState));
+    if (e == cudaSuccess) e = dmalloc(&recs, sizeof(Rec) * grid);
+    if (e == cudaSuccess) e = dmalloc(&ticket, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemsetAsync(vst, 0, sizeof(DevState), c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned), c->stream);
     SweepArgs a = sweep_args(c);
@@ -372,9 +372,9 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
         e = launch_sweep(a, c->cplx, false, c->cfg_sweep, c->stream);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(vst);
-    cudaFree(recs);
-    cudaFree(ticket);
+    dfree(vst);
+    dfree(recs);
+    dfree(ticket);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "coefficient passes: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
@@ -398,6 +398,15 @@ void rbg_desc_init(rbg_desc *d) {
 }
 
 const char *rbg_last_error(void) { return g_err.c_str(); }
+
+void rbg_debug_set_canary(int on) { debug_set_canary(on != 0); }
+
+int64_t rbg_debug_canary_violations(void) {
+    std::string msg;
+    const long long n = debug_canary_violations(&msg);
+    if (n) g_err = msg;
+    return n;
+}
 
 void rbg_lanes(int *L_S, int *L_I) {
     if (L_S) *L_S = kLaneSweep;
@@ -506,7 +515,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     } else {
         c->ldv = nvec;
         const size_t dst_pitch = (size_t)nvec * 16;
-        CUB(cudaMalloc(&c->S, dst_pitch * d->M));
+        CUB(dmalloc(&c->S, dst_pitch * d->M));
         c->own_S = true;
         if (dst_pitch != col_bytes) CUB(cudaMemsetAsync(c->S, 0, dst_pitch * d->M, c->stream));
         const cudaMemcpyKind kind = d->S_mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -517,12 +526,12 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     }
     if (d->check_finite) {  // first non-finite entry in column-major order, on the device
         unsigned long long *bad = nullptr, hbad = ~0ull;
-        CUB(cudaMalloc(&bad, sizeof *bad));
+        CUB(dmalloc(&bad, sizeof *bad));
         CUB(cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream));
         CUB(launch_check_finite(c->S, c->ldv, c->M, c->N, nvec, cplx, bad, c->stream));
         CUB(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, c->stream));
         CUB(cudaStreamSynchronize(c->stream));
-        cudaFree(bad);
+        dfree(bad);
         if (hbad != ~0ull)
             return bail(fail(RBG_ENONFINITE, "non-finite S entry at (row %lld, col %lld)", (long long)(hbad % d->N),
                              (long long)(hbad / d->N) + d->col_offset));
@@ -534,11 +543,11 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     c->xmode = d->residual == RBG_RESIDUAL_EXPLICIT;
     if (c->xmode) {
         // the kernels see V = W^{1/2} S with unit weights; w_true keeps the caller's weights
-        CUB(cudaMalloc(&c->w_true, sizeof(double) * wpad.size()));
+        CUB(dmalloc(&c->w_true, sizeof(double) * wpad.size()));
         CUB(cudaMemcpyAsync(c->w_true, wpad.data(), sizeof(double) * wpad.size(), cudaMemcpyHostToDevice, c->stream));
         double2 *V = nullptr;
         if (c->own_S) V = c->S;                               // scale the private copy in place
-        else CUB(cudaMalloc(&V, (size_t)nvec * 16 * c->M));
+        else CUB(dmalloc(&V, (size_t)nvec * 16 * c->M));
         CUB(launch_scale_sqrtw(V, nvec, c->S, c->ldv, c->M, nvec, c->N, c->w_true, cplx, c->stream));
         c->S = V;
         c->own_S = true;
@@ -548,42 +557,42 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         for (long long i = 0; i < d->N; i++) ones[i] = 1.0;
         wpad.swap(ones);
     }
-    CUB(cudaMalloc(&c->w, sizeof(double) * wpad.size()));
+    CUB(dmalloc(&c->w, sizeof(double) * wpad.size()));
     CUB(cudaMemcpyAsync(c->w, wpad.data(), sizeof(double) * wpad.size(), cudaMemcpyHostToDevice, c->stream));
     const size_t qbytes = (size_t)c->k_max * nvec * 16;
-    CUB(cudaMalloc(&c->Q, qbytes));
-    CUB(cudaMalloc(&c->WQ, qbytes));
+    CUB(dmalloc(&c->Q, qbytes));
+    CUB(dmalloc(&c->WQ, qbytes));
     CUB(cudaMemsetAsync(c->Q, 0, qbytes, c->stream));
     CUB(cudaMemsetAsync(c->WQ, 0, qbytes, c->stream));
-    CUB(cudaMalloc(&c->R, (size_t)c->k_max * c->M * c->se));
+    CUB(dmalloc(&c->R, (size_t)c->k_max * c->M * c->se));
     CUB(cudaMemsetAsync(c->R, 0, (size_t)c->k_max * c->M * c->se, c->stream));
-    CUB(cudaMalloc(&c->r2, sizeof(double) * c->M));
-    CUB(cudaMalloc(&c->st, sizeof(DevState)));
+    CUB(dmalloc(&c->r2, sizeof(double) * c->M));
+    CUB(dmalloc(&c->st, sizeof(DevState)));
     CUB(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
-    CUB(cudaMalloc(&c->errors, sizeof(double) * (c->k_max + 1)));
+    CUB(dmalloc(&c->errors, sizeof(double) * (c->k_max + 1)));
     CUB(cudaMemsetAsync(c->errors, 0, sizeof(double) * (c->k_max + 1), c->stream));
-    CUB(cudaMalloc(&c->rdiag, sizeof(double) * c->k_max));
-    CUB(cudaMalloc(&c->piv, sizeof(long long) * c->k_max));
-    CUB(cudaMalloc(&c->nu, sizeof(int) * c->k_max));
+    CUB(dmalloc(&c->rdiag, sizeof(double) * c->k_max));
+    CUB(dmalloc(&c->piv, sizeof(long long) * c->k_max));
+    CUB(dmalloc(&c->nu, sizeof(int) * c->k_max));
     CUB(cudaMemsetAsync(c->nu, 0, sizeof(int) * c->k_max, c->stream));
     c->ortho = d->ortho;
     if (c->ortho == RBG_ORTHO_CGS) {
-        CUB(cudaMalloc(&c->cgs_v, (size_t)nvec * 16));
-        CUB(cudaMalloc(&c->cgs_c, sizeof(double2) * (size_t)c->k_max));
+        CUB(dmalloc(&c->cgs_v, (size_t)nvec * 16));
+        CUB(dmalloc(&c->cgs_c, sizeof(double2) * (size_t)c->k_max));
         c->cgs_grid = cgs_grid(c->num_sms);
     }
     c->cfg_init = sweep_config(cplx, true, nvec, c->num_sms, c->device);
     c->cfg_sweep = sweep_config(cplx, false, nvec, c->num_sms, c->device);
     const int max_grid = std::max(c->cfg_init.grid, c->cfg_sweep.grid);
-    CUB(cudaMalloc(&c->recs, sizeof(Rec) * max_grid));
-    CUB(cudaMalloc(&c->ticket, sizeof(unsigned)));
+    CUB(dmalloc(&c->recs, sizeof(Rec) * max_grid));
+    CUB(dmalloc(&c->ticket, sizeof(unsigned)));
     CUB(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
 
     if (d->comm == RBG_COMM_PEER) {  // two send slots (by tag parity) + 2 x world records
         c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;
-        CUB(cudaMalloc(&c->send, 2 * c->slot));
+        CUB(dmalloc(&c->send, 2 * c->slot));
         CUB(cudaMemsetAsync(c->send, 0, 2 * c->slot, c->stream));
-        CUB(cudaMalloc(&c->peer_in, sizeof(PeerRec) * 2 * world));
+        CUB(dmalloc(&c->peer_in, sizeof(PeerRec) * 2 * world));
         CUB(cudaMemsetAsync(c->peer_in, 0, sizeof(PeerRec) * 2 * world, c->stream));  // tag 0: none yet
         c->peer_rec[c->rank] = c->peer_in;
         c->peer_send[c->rank] = c->send;
@@ -591,8 +600,8 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         c->peer_connected = world == 1;
     } else if (d->comm != RBG_COMM_NONE) {  // (world = 1 runs the same exchange path, e.g. in tests)
         c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;
-        CUB(cudaMalloc(&c->send, c->slot));
-        CUB(cudaMalloc(&c->recv, c->slot * world));
+        CUB(dmalloc(&c->send, c->slot));
+        CUB(dmalloc(&c->recv, c->slot * world));
         CUB(cudaMemsetAsync(c->send, 0, c->slot, c->stream));
         CUB(cudaMemsetAsync(c->recv, 0, c->slot * world, c->stream));
         if (d->comm == RBG_COMM_NCCL) {
@@ -718,18 +727,18 @@ rbg_status rbg_get_basis(rbg_ctx *c, void *out, int64_t ldq, int on_device) {
     const double2 *src = c->Q;
     double2 *tmp = nullptr;
     if (c->xmode) {  // Q = Q~ / W^{1/2}: the W-orthonormal basis of S
-        CU(cudaMalloc(&tmp, (size_t)h.k * c->ldq_v * 16));
+        CU(dmalloc(&tmp, (size_t)h.k * c->ldq_v * 16));
         cudaError_t e = launch_unscale_sqrtw(tmp, c->Q, h.k, c->ldq_v, c->w_true, c->cplx, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e != cudaSuccess) {
-            cudaFree(tmp);
+            dfree(tmp);
             return fail(RBG_ECUDA, "basis unscale: %s", cudaGetErrorString(e));
         }
         src = tmp;
     }
     cudaError_t e = cudaMemcpy2D(out, (size_t)ldq * c->se, src, (size_t)c->ldq_v * 16, (size_t)c->N * c->se, h.k,
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
-    cudaFree(tmp);
+    dfree(tmp);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "get_basis: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
@@ -949,9 +958,9 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
     TRY(upload_block(c, V, M_v, ldv, V_mem, &Vd));
     const long long k = h.k;
     double *Rv = nullptr, *e2 = nullptr, *ed = nullptr;
-    cudaError_t e = cudaMalloc(&Rv, (size_t)std::max<long long>(k, 1) * M_v * c->se);
-    if (e == cudaSuccess) e = cudaMalloc(&e2, sizeof(double) * M_v);
-    if (e == cudaSuccess) e = cudaMalloc(&ed, sizeof(double) * M_v);
+    cudaError_t e = dmalloc(&Rv, (size_t)std::max<long long>(k, 1) * M_v * c->se);
+    if (e == cudaSuccess) e = dmalloc(&e2, sizeof(double) * M_v);
+    if (e == cudaSuccess) e = dmalloc(&ed, sizeof(double) * M_v);
     rbg_status st = e == cudaSuccess ? coeff_passes(c, Vd, M_v, Rv, M_v, e2, k)
                                      : fail(RBG_ENOMEM, "validation buffers: %s", cudaGetErrorString(e));
     const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -965,10 +974,10 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "validation coefficients: %s", cudaGetErrorString(e));
     }
     cudaStreamSynchronize(c->stream);
-    cudaFree(Vd);
-    cudaFree(Rv);
-    cudaFree(e2);
-    cudaFree(ed);
+    dfree(Vd);
+    dfree(Rv);
+    dfree(e2);
+    dfree(ed);
     return st;
 }
 
@@ -984,9 +993,9 @@ rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, 
     const size_t pitch = (size_t)c->nvec * 16;
     double2 *S1 = nullptr;
     double *R1 = nullptr, *r21 = nullptr;
-    cudaError_t e = cudaMalloc(&S1, pitch * M1);
-    if (e == cudaSuccess) e = cudaMalloc(&R1, (size_t)c->k_max * M1 * c->se);
-    if (e == cudaSuccess) e = cudaMalloc(&r21, sizeof(double) * M1);
+    cudaError_t e = dmalloc(&S1, pitch * M1);
+    if (e == cudaSuccess) e = dmalloc(&R1, (size_t)c->k_max * M1 * c->se);
+    if (e == cudaSuccess) e = dmalloc(&r21, sizeof(double) * M1);
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(S1, pitch, c->S, (size_t)c->ldv * 16, pitch, M0, cudaMemcpyDeviceToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(S1 + M0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(R1, 0, (size_t)c->k_max * M1 * c->se, c->stream);
@@ -995,11 +1004,11 @@ rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, 
                               cudaMemcpyDeviceToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(r21, c->r2, sizeof(double) * M0, cudaMemcpyDeviceToDevice, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(Fd);
+    dfree(Fd);
     if (e != cudaSuccess) {
-        cudaFree(S1);
-        cudaFree(R1);
-        cudaFree(r21);
+        dfree(S1);
+        dfree(R1);
+        dfree(r21);
         return fail(e == cudaErrorMemoryAllocation ? RBG_ENOMEM : RBG_ECUDA, "add_columns: %s", cudaGetErrorString(e));
     }
     if (c->started) {
@@ -1007,15 +1016,15 @@ rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, 
         // search restarts over all columns and the next iteration begins at the decision
         rbg_status st = coeff_passes(c, S1 + M0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), M1, r21 + M0, h.k);
         if (st != RBG_OK) {
-            cudaFree(S1);
-            cudaFree(R1);
-            cudaFree(r21);
+            dfree(S1);
+            dfree(R1);
+            dfree(r21);
             return st;
         }
     }
-    if (c->own_S) cudaFree(c->S);
-    cudaFree(c->R);
-    cudaFree(c->r2);
+    if (c->own_S) dfree(c->S);
+    dfree(c->R);
+    dfree(c->r2);
     c->S = S1;
     c->own_S = true;
     c->ldv = c->nvec;
@@ -1051,16 +1060,16 @@ rbg_status gram_device(rbg_ctx *c, int k, int kp, double2 *G) {
         for (int b = a; b < nt; b++) tiles.push_back(make_int2(a, b));
     int2 *tiles_d = nullptr;
     double2 *P = nullptr;
-    cudaError_t e = cudaMalloc(&tiles_d, sizeof(int2) * tiles.size());
-    if (e == cudaSuccess) e = cudaMalloc(&P, sizeof(double2) * (size_t)nchunks * k * k);
+    cudaError_t e = dmalloc(&tiles_d, sizeof(int2) * tiles.size());
+    if (e == cudaSuccess) e = dmalloc(&P, sizeof(double2) * (size_t)nchunks * k * k);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(tiles_d, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess)
         e = launch_gram(c->R, c->M, k, c->M, c->cplx, P, kGramChunk, nchunks, tiles_d, (int)tiles.size(), c->stream);
     if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(tiles_d);
-    cudaFree(P);
+    dfree(tiles_d);
+    dfree(P);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "gram: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
@@ -1077,14 +1086,14 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     if (k == 0) return RBG_OK;
     const int kp = k + (k & 1);
     double2 *Gd = nullptr;
-    CU(cudaMalloc(&Gd, sizeof(double2) * (size_t)kp * kp));
+    CU(dmalloc(&Gd, sizeof(double2) * (size_t)kp * kp));
     rbg_status st = gram_device(c, k, kp, Gd);
     if (st == RBG_OK) {
         cudaError_t e = cudaMemcpy2D(G, (size_t)ldg * 16, Gd, (size_t)kp * 16, (size_t)k * 16, k,
                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "gram copy: %s", cudaGetErrorString(e));
     }
-    cudaFree(Gd);
+    dfree(Gd);
     return st;
 }
 
@@ -1106,14 +1115,14 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     unsigned long long *flags = nullptr;
     int *sweeps = nullptr, *order = nullptr, *krd = nullptr;
     double *sig = nullptr;
-    cudaError_t e = cudaMalloc(&G, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = cudaMalloc(&V, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = cudaMalloc(&rots, rot_bytes(kp));
-    if (e == cudaSuccess) e = cudaMalloc(&flags, 2 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMalloc(&sweeps, sizeof(int));
-    if (e == cudaSuccess) e = cudaMalloc(&order, sizeof(int) * kp);
-    if (e == cudaSuccess) e = cudaMalloc(&krd, sizeof(int));
-    if (e == cudaSuccess) e = cudaMalloc(&sig, sizeof(double) * kp);
+    cudaError_t e = dmalloc(&G, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = dmalloc(&V, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = dmalloc(&rots, rot_bytes(kp));
+    if (e == cudaSuccess) e = dmalloc(&flags, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = dmalloc(&sweeps, sizeof(int));
+    if (e == cudaSuccess) e = dmalloc(&order, sizeof(int) * kp);
+    if (e == cudaSuccess) e = dmalloc(&krd, sizeof(int));
+    if (e == cudaSuccess) e = dmalloc(&sig, sizeof(double) * kp);
     rbg_status st = e == cudaSuccess ? RBG_OK : fail(RBG_ENOMEM, "reconstruct buffers: %s", cudaGetErrorString(e));
     if (st == RBG_OK) st = gram_device(c, k, kp, G);
     if (st == RBG_OK) {
@@ -1130,7 +1139,7 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && sigma) e = cudaMemcpy(sigma, sig, sizeof(double) * k, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && X && kr > 0) {
-            e = cudaMalloc(&Xd, (size_t)kr * c->nvec * 16);
+            e = dmalloc(&Xd, (size_t)kr * c->nvec * 16);
             if (e == cudaSuccess)
                 e = launch_recon_x(c->Q, c->ldq_v, c->nvec, k, V, kp, order, kr, Xd, c->nvec, c->cplx, c->stream);
             if (e == cudaSuccess)
@@ -1141,15 +1150,15 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "reconstruct: %s", cudaGetErrorString(e));
         else if (kr_out) *kr_out = kr;
     }
-    cudaFree(G);
-    cudaFree(V);
-    cudaFree(Xd);
-    cudaFree(rots);
-    cudaFree(flags);
-    cudaFree(sweeps);
-    cudaFree(order);
-    cudaFree(krd);
-    cudaFree(sig);
+    dfree(G);
+    dfree(V);
+    dfree(Xd);
+    dfree(rots);
+    dfree(flags);
+    dfree(sweeps);
+    dfree(order);
+    dfree(krd);
+    dfree(sig);
     return st;
 }
 
@@ -1165,17 +1174,17 @@ rbg_status rbg_eim(rbg_ctx *c, int64_t *nodes, void *B, int64_t ldb, int on_devi
     long long *nd = nullptr;
     double2 *Bd = nullptr;
     int *status = nullptr, hs = 0;
-    cudaError_t e = cudaMalloc(&nd, sizeof(long long) * k);
-    if (e == cudaSuccess) e = cudaMalloc(&Bd, sizeof(double2) * (size_t)k * k);
-    if (e == cudaSuccess) e = cudaMalloc(&status, sizeof(int));
+    cudaError_t e = dmalloc(&nd, sizeof(long long) * k);
+    if (e == cudaSuccess) e = dmalloc(&Bd, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = dmalloc(&status, sizeof(int));
     if (e == cudaSuccess) e = run_eim(c->Q, c->ldq_v, c->N, c->cplx, k, nd, Bd, status, c->stream);
     if (e == cudaSuccess) e = cudaMemcpy(&hs, status, sizeof(int), cudaMemcpyDeviceToHost);
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (e == cudaSuccess && nodes) e = cudaMemcpy(nodes, nd, sizeof(long long) * k, kind);
     if (e == cudaSuccess && B) e = cudaMemcpy2D(B, (size_t)ldb * 16, Bd, (size_t)k * 16, (size_t)k * 16, k, kind);
-    cudaFree(nd);
-    cudaFree(Bd);
-    cudaFree(status);
+    dfree(nd);
+    dfree(Bd);
+    dfree(status);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "eim: %s", cudaGetErrorString(e));
     if (hs) return fail(RBG_ESTATE, "EIM residual vanished: the basis is numerically degenerate");
     return RBG_OK;

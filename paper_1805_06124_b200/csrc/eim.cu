@@ -164,12 +164,12 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     a.k = k;
     a.nodes = nodes_d;
     a.status = status_d;
-    cudaError_t e = cudaMalloc(&a.Xi, sizeof(double2) * (size_t)k * N);
-    if (e == cudaSuccess) e = cudaMalloc(&a.T, sizeof(double2) * (size_t)k * k);
-    if (e == cudaSuccess) e = cudaMalloc(&a.c, sizeof(double2) * k);
-    if (e == cudaSuccess) e = cudaMalloc(&a.bm, sizeof(double) * blocks);
-    if (e == cudaSuccess) e = cudaMalloc(&a.bj, sizeof(long long) * blocks);
-    if (e == cudaSuccess) e = cudaMalloc(&a.ticket, sizeof(unsigned));
+    cudaError_t e = dmalloc(&a.Xi, sizeof(double2) * (size_t)k * N);
+    if (e == cudaSuccess) e = dmalloc(&a.T, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = dmalloc(&a.c, sizeof(double2) * k);
+    if (e == cudaSuccess) e = dmalloc(&a.bm, sizeof(double) * blocks);
+    if (e == cudaSuccess) e = dmalloc(&a.bj, sizeof(long long) * blocks);
+    if (e == cudaSuccess) e = dmalloc(&a.ticket, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(status_d, 0, sizeof(int), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.c, 0, sizeof(double2) * k, s);
@@ -188,12 +188,12 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(a.Xi);
-    cudaFree(a.T);
-    cudaFree(a.c);
-    cudaFree(a.bm);
-    cudaFree(a.bj);
-    cudaFree(a.ticket);
+    dfree(a.Xi);
+    dfree(a.T);
+    dfree(a.c);
+    dfree(a.bm);
+    dfree(a.bj);
+    dfree(a.ticket);
     return e;
 }
 

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -151,6 +152,17 @@ size_t rot_bytes(int kp);
 // Greedy EIM nodes (eim.cu): nodes_d[k], B_d = Q(P, :) k x k column-major complex.
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
                     int *status_d, cudaStream_t s);
+
+// Device allocations of the library (devmem.cu): cudaMalloc / cudaFree, with a checked
+// 256-byte canary tail per buffer while canaries are on (rbg_debug_set_canary).
+cudaError_t dmalloc(void **p, size_t bytes);
+cudaError_t dfree(void *p);
+template <class T>
+inline cudaError_t dmalloc(T **p, size_t bytes) {
+    return dmalloc(reinterpret_cast<void **>(p), bytes);
+}
+void debug_set_canary(bool on);
+long long debug_canary_violations(std::string *msg);
 
 // First non-finite entry of a device block: writes min(col * N + row) (or -1) to *out.
 cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,

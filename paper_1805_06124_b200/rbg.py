@@ -88,6 +88,8 @@ SYMBOLS = {
     "rbg_peer_connect": ([_P, ctypes.POINTER(ctypes.c_uint8)], ctypes.c_int),
     "rbg_peer_connect_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
     "rbg_lanes": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], None),
+    "rbg_debug_set_canary": ([ctypes.c_int], None),
+    "rbg_debug_canary_violations": ([], ctypes.c_int64),
     "rbg_version": ([], ctypes.c_char_p),
     "rbg_last_error": ([], ctypes.c_char_p),
     "rbg_destroy": ([_P], None),
@@ -121,6 +123,17 @@ def lib():
 def _check(status: int):
     if status != OK:
         raise RbgError(status, lib().rbg_last_error().decode())
+
+
+def set_canary(on: bool):
+    """Canary tails on every device buffer allocated from now on (rbg_debug_set_canary)."""
+    lib().rbg_debug_set_canary(1 if on else 0)
+
+
+def canary_violations() -> tuple[int, str]:
+    """(violations so far, first message) after checking every live canaried buffer."""
+    n = int(lib().rbg_debug_canary_violations())
+    return n, (lib().rbg_last_error().decode() if n else "")
 
 
 def lanes() -> tuple[int, int]:

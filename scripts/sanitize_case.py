@@ -30,3 +30,15 @@ for _ in range(21):
     for c in ctxs:
         c.iter_finish()
 print("ok", [c.info() for c in ctxs])
+import torch  # noqa: E402
+
+st = torch.cuda.Stream()
+pctx = [rbg.Context(S[p * 350:(p + 1) * 350], w, tol, 20, stream=st.cuda_stream, comm=rbg.COMM_PEER, rank=p,
+                    world=2, col_offset=p * 350, M_global=700) for p in range(2)]
+rbg.peer_connect_local(pctx)
+for _ in range(21):
+    for c in pctx:
+        c.iter_local()
+    for c in pctx:
+        c.iter_finish()
+print("peer ok", [c.info() for c in pctx])
