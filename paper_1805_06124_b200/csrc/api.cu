@@ -1054,7 +1054,7 @@ namespace {
 // G = R(0:k, :) R(0:k, :)^H into a zero-padded kp x kp column-major device buffer.
 rbg_status gram_device(rbg_ctx *c, int k, int kp, double2 *G) {
     const long long nchunks = std::max<long long>(1, (c->M + kGramChunk - 1) / kGramChunk);
-    const int nt = (k + 31) / 32;
+    const int nt = (k + gram_tile() - 1) / gram_tile();
     std::vector<int2> tiles;
     for (int a = 0; a < nt; a++)
         for (int b = a; b < nt; b++) tiles.push_back(make_int2(a, b));
@@ -1117,8 +1117,8 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     double *sig = nullptr;
     cudaError_t e = dmalloc(&G, sizeof(double2) * (size_t)kp * kp);
     if (e == cudaSuccess) e = dmalloc(&V, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = dmalloc(&rots, rot_bytes(kp));
-    if (e == cudaSuccess) e = dmalloc(&flags, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = dmalloc(&rots, jacobi_scratch_bytes(kp));  // k_jacobi scratch
+    if (e == cudaSuccess) e = dmalloc(&flags, 3 * sizeof(unsigned long long));  // ratios + barrier
     if (e == cudaSuccess) e = dmalloc(&sweeps, sizeof(int));
     if (e == cudaSuccess) e = dmalloc(&order, sizeof(int) * kp);
     if (e == cudaSuccess) e = dmalloc(&krd, sizeof(int));
@@ -1129,7 +1129,7 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
         std::vector<double2> I((size_t)kp * kp, make_double2(0.0, 0.0));
         for (int i = 0; i < kp; i++) I[(size_t)i * kp + i] = make_double2(1.0, 0.0);
         e = cudaMemcpyAsync(V, I.data(), sizeof(double2) * I.size(), cudaMemcpyHostToDevice, c->stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), c->stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned long long), c->stream);
         if (e == cudaSuccess) e = launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
         if (e == cudaSuccess)
             e = launch_eig_sort(G, k, kp, tau2, (int)std::min<int64_t>(kr_max ? kr_max : k, k), order, sig, krd,

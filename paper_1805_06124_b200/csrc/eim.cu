@@ -56,35 +56,73 @@ struct EimArgs {
     int *status;     // 0 ok, 1 degenerate (zero residual)
 };
 
-// Forward substitution for step l (l >= 1): c_a for a < l.
+// Forward substitution for step l (l >= 1): c_a for a < l.  One thread per row r; the row's
+// entries T[r][b] are loaded 4 columns at a time, one batch ahead of use, so no step waits on
+// memory; c_b is broadcast through a two-slot shared buffer (one barrier per column: slot
+// b & 1 is rewritten at column b + 2, after every thread passed the barrier of b + 1).
+constexpr int kEimBatch = 4;
+
 __global__ void __launch_bounds__(1024) k_eim_solve(EimArgs a, int l) {
-    __shared__ double2 cb;
-    // one thread per row a (k <= 1024 enforced on the host); rhs a = q_l(p_a)
+    __shared__ double2 cb[2];
     const int r = threadIdx.x;
-    double2 v = make_double2(0.0, 0.0);
-    if (r < l) v = load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]);
-    for (int b = 0; b < l; b++) {
-        if (r == b) {
-            cb = cdiv(v, a.T[(long long)b * a.k + b]);
-            a.c[b] = cb;
+    const bool mine = r < l;
+    double2 v = make_double2(0.0, 0.0), tdiag = make_double2(1.0, 0.0);
+    if (mine) {
+        v = load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]);   // rhs q_l(p_r)
+        tdiag = a.T[(long long)r * a.k + r];
+    }
+    const double2 *trow = a.T + (long long)r * a.k;
+    double2 tn[kEimBatch];
+#pragma unroll
+    for (int j = 0; j < kEimBatch; j++) tn[j] = (mine && j < r) ? trow[j] : make_double2(0.0, 0.0);
+    for (int b0 = 0; b0 < l; b0 += kEimBatch) {
+        double2 t[kEimBatch];
+#pragma unroll
+        for (int j = 0; j < kEimBatch; j++) {
+            t[j] = tn[j];
+            const int bn = b0 + kEimBatch + j;
+            tn[j] = (mine && bn < r) ? trow[bn] : make_double2(0.0, 0.0);   // next batch
         }
-        __syncthreads();
-        const double2 cc = cb;
-        if (r > b && r < l) v = cmsub(v, cc, a.T[(long long)r * a.k + b]);
-        __syncthreads();
+#pragma unroll 1
+        for (int j = 0; j < kEimBatch && b0 + j < l; j++) {  // uniform over the block
+            const int b = b0 + j;
+            if (r == b) {
+                const double2 cv = cdiv(v, tdiag);
+                cb[b & 1] = cv;
+                a.c[b] = cv;
+            }
+            __syncthreads();
+            if (r > b && mine) v = cmsub(v, cb[b & 1], t[0]);
+#pragma unroll
+            for (int m = 0; m + 1 < kEimBatch; m++) t[m] = t[m + 1];  // t[0] = T[r][b + 1]
+        }
     }
 }
 
 // xi_l over all rows + maxloc of |xi_l|^2; the last block sets p_l and row l of T.
-__global__ void __launch_bounds__(256) k_eim_residual(EimArgs a, int l) {
-    __shared__ double s_m[8];
-    __shared__ long long s_j[8];
+constexpr int kEimThreads = 128;
+
+__global__ void __launch_bounds__(kEimThreads) k_eim_residual(EimArgs a, int l) {
+    __shared__ double s_m[kEimThreads / 32];
+    __shared__ long long s_j[kEimThreads / 32];
     __shared__ int s_last;
+    extern __shared__ double2 s_c[];  // c_0 .. c_{l-1}
+    for (int b = threadIdx.x; b < l; b += blockDim.x) s_c[b] = a.c[b];
+    __syncthreads();
     double bm = -1.0;
     long long bj = 0x7fffffffffffffffLL;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.N; i += (long long)gridDim.x * blockDim.x) {
         double2 x = load_q(a.Q, a.ldq_v, a.cplx, l, i);
-        for (int b = 0; b < l; b++) x = cmsub(x, a.c[b], a.Xi[(long long)b * a.N + i]);
+        // x -= c_b xi_b in increasing b; the xi loads of a batch are issued together
+        for (int b0 = 0; b0 < l; b0 += 16) {
+            double2 xi[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                xi[j] = (b0 + j < l) ? a.Xi[(long long)(b0 + j) * a.N + i] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                if (b0 + j < l) x = cmsub(x, s_c[b0 + j], xi[j]);
+        }
         a.Xi[(long long)l * a.N + i] = x;
         const double m = fma(x.x, x.x, x.y * x.y);
         if (m > bm) {  // rows visited in increasing order per thread
@@ -106,7 +144,7 @@ __global__ void __launch_bounds__(256) k_eim_residual(EimArgs a, int l) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; w++)
+        for (int w = 1; w < kEimThreads / 32; w++)
             if (rec_better(s_m[w], s_j[w], bm, bj)) {
                 bm = s_m[w];
                 bj = s_j[w];
@@ -155,7 +193,7 @@ __global__ void k_eim_nodes_matrix(EimArgs a, double2 *B) {
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
                     int *status_d, cudaStream_t s) {
     if (k < 1 || k > 1024) return cudaErrorInvalidValue;
-    const int blocks = (int)((N + 255) / 256 < 148 ? (N + 255) / 256 : 148);
+    const int blocks = (int)((N + kEimThreads - 1) / kEimThreads < 296 ? (N + kEimThreads - 1) / kEimThreads : 296);
     EimArgs a{};
     a.Q = Q;
     a.ldq_v = ldq_v;
@@ -175,11 +213,11 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     if (e == cudaSuccess) e = cudaMemsetAsync(a.c, 0, sizeof(double2) * k, s);
     for (int l = 0; l < k && e == cudaSuccess; l++) {
         if (l > 0) {
-            k_eim_solve<<<1, 1024, 0, s>>>(a, l);
+            k_eim_solve<<<1, (l + 31) / 32 * 32, 0, s>>>(a, l);
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) {
-            k_eim_residual<<<blocks, 256, 0, s>>>(a, l);
+            k_eim_residual<<<blocks, kEimThreads, sizeof(double2) * (size_t)(l > 0 ? l : 1), s>>>(a, l);
             e = cudaGetLastError();
         }
     }

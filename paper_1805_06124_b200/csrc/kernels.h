@@ -138,6 +138,7 @@ cudaError_t launch_sqrt_clamp(const double *in, double *out, long long M, cudaSt
 // Algorithm 4 (recon.cu)
 struct Rot;
 constexpr long long kGramChunk = 4096;  // columns per Gram chunk (R30)
+int gram_tile();  // pairs per k_gram tile side
 cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool cplx, double2 *P, long long chunk,
                         long long nchunks, int2 *tiles_d, int ntiles, cudaStream_t s);
 cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, double2 *G, cudaStream_t s);
@@ -148,6 +149,7 @@ cudaError_t launch_eig_sort(const double2 *G, int k, int kp, double tau2, int kr
 cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, int k, const double2 *V, int kp,
                            const int *order, int kr, double2 *X, long long ldx_v, bool cplx, cudaStream_t s);
 size_t rot_bytes(int kp);
+size_t jacobi_scratch_bytes(int kp);  // k_jacobi's per-pair 2 x 2 scratch
 
 // Greedy EIM nodes (eim.cu): nodes_d[k], B_d = Q(P, :) k x k column-major complex.
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,

@@ -23,24 +23,37 @@ namespace cg = cooperative_groups;
 
 namespace rbg {
 
-constexpr int kGramTile = 32;   // pairs per tile side
-constexpr int kGramSub = 32;    // columns staged per shared-memory step
+constexpr int kGramTile = 64;   // pairs per tile side
+constexpr int kGramSub = 16;    // columns staged per shared-memory step
+constexpr int kGramReg = 4;     // pairs per thread per side (4 x 4 register tile)
+
+int gram_tile() { return kGramTile; }
 
 // R: k rows of ldr elements (row-major).  P: nchunks x k x k partial sums (complex).
+// 256 threads own 4 x 4 pairs each, strided by 16 (thread (ta, tb) has pairs
+// (a0 + ta + 16u, b0 + tb + 16v)) so that a warp's shared-memory reads of one operand row
+// are consecutive 16-byte words; every pair is one sequential fma chain over the chunk's
+// columns in increasing index (the order k_gram_reduce and the oracle's orc_gram assume).
 template <bool CPLX>
 __global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, int k, long long M, long long chunk,
                                               const int2 *tiles, double2 *P) {
-    __shared__ double2 sa[kGramSub][kGramTile];
-    __shared__ double2 sb[kGramSub][kGramTile];
+    // +1 column of padding: the transposed staging stores (consecutive threads -> consecutive
+    // columns cc) would otherwise all hit the same banks
+    __shared__ double2 sa[kGramSub][kGramTile + 1];
+    __shared__ double2 sb[kGramSub][kGramTile + 1];
     const int2 t = tiles[blockIdx.x];
     const int a0 = t.x * kGramTile, b0 = t.y * kGramTile;
     const long long c = blockIdx.y;
     const long long j0 = c * chunk, j1 = (j0 + chunk < M) ? j0 + chunk : M;
     const int tid = threadIdx.x;
-    const int ta = (tid >> 4) * 2, tb = (tid & 15) * 2;   // this thread: pairs (a0+ta+{0,1}, b0+tb+{0,1})
-    double re[2][2] = {{0, 0}, {0, 0}}, im[2][2] = {{0, 0}, {0, 0}};
+    const int ta = tid >> 4, tb = tid & 15;
+    double re[kGramReg][kGramReg], im[kGramReg][kGramReg];
+#pragma unroll
+    for (int u = 0; u < kGramReg; u++)
+#pragma unroll
+        for (int v = 0; v < kGramReg; v++) re[u][v] = im[u][v] = 0.0;
     for (long long js = j0; js < j1; js += kGramSub) {
-        // stage rows a0..a0+31 and b0..b0+31, columns js..js+31 (transposed: [col][row])
+        // stage rows a0..a0+63 and b0..b0+63, columns js..js+15 (transposed: [col][row])
         for (int e = tid; e < kGramSub * kGramTile; e += 256) {
             const int r = e / kGramSub, cc = e % kGramSub;
             const long long j = js + cc;
@@ -57,15 +70,16 @@ __global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, in
         __syncthreads();
         const int n = (int)((j1 - js) < kGramSub ? (j1 - js) : kGramSub);
         for (int cc = 0; cc < n; cc++) {
-            double2 x[2], y[2];
-            x[0] = sa[cc][ta];
-            x[1] = sa[cc][ta + 1];
-            y[0] = sb[cc][tb];
-            y[1] = sb[cc][tb + 1];
+            double2 x[kGramReg], y[kGramReg];
 #pragma unroll
-            for (int u = 0; u < 2; u++)
+            for (int u = 0; u < kGramReg; u++) {
+                x[u] = sa[cc][ta + 16 * u];
+                y[u] = sb[cc][tb + 16 * u];
+            }
 #pragma unroll
-                for (int v = 0; v < 2; v++) {
+            for (int u = 0; u < kGramReg; u++)
+#pragma unroll
+                for (int v = 0; v < kGramReg; v++) {
                     // G_ab += R_a conj(R_b) = DOT(R_b, R_a) term: (p,q) = R_b, (x,y) = R_a
                     re[u][v] = fma(y[v].x, x[u].x, re[u][v]);
                     re[u][v] = fma(y[v].y, x[u].y, re[u][v]);
@@ -76,10 +90,10 @@ __global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, in
         __syncthreads();
     }
 #pragma unroll
-    for (int u = 0; u < 2; u++)
+    for (int u = 0; u < kGramReg; u++)
 #pragma unroll
-        for (int v = 0; v < 2; v++) {
-            const int a = a0 + ta + u, b = b0 + tb + v;
+        for (int v = 0; v < kGramReg; v++) {
+            const int a = a0 + ta + 16 * u, b = b0 + tb + 16 * v;
             if (a < k && b < k && b >= a) P[(c * k + a) * k + b] = make_double2(re[u][v], im[u][v]);
         }
 }
@@ -129,11 +143,69 @@ __device__ __forceinline__ void round_pair(int r, int i, int kp, int &p, int &q)
 
 __device__ __forceinline__ unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }
 
+// Grid-wide barrier for the co-resident blocks of a cooperative launch: arrival counter +
+// generation word (sense reversal), ~1-2 us instead of cooperative_groups' grid.sync.
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *vg = gen;
+        const unsigned g = *vg;
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *count = 0u;
+            __threadfence();
+            atomicExch(gen, g + 1u);
+        } else {
+            while (*vg == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ Rot make_rot(const double2 *G, int kp, int p, int q, unsigned long long *flag, bool note) {
+    const double a = G[p + (long long)p * kp].x, b = G[q + (long long)q * kp].x;
+    const double2 c = G[p + (long long)q * kp];  // g_pq
+    const double ac = sqrt(c.x * c.x + c.y * c.y);
+    Rot R;
+    R.p = p;
+    R.q = q;
+    if (ac == 0.0) {
+        R.cs = 1.0;
+        R.sn = 0.0;
+        R.er = 1.0;
+        R.ei = 0.0;
+    } else {
+        const double den = sqrt(fabs(a * b));
+        const double ratio = den > 0.0 ? ac / den : 1.0;
+        if (note) atomicMax(flag, dbits(ratio));
+        const double tau = (b - a) / (2.0 * ac);
+        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        R.cs = 1.0 / sqrt(1.0 + t * t);
+        R.sn = t * R.cs;
+        R.er = c.x / ac;
+        R.ei = c.y / ac;
+    }
+    return R;
+}
+
 // G: kp x kp Hermitian (column-major), V: kp x kp (column-major), identity on entry.
-// flags[2]: per-sweep max off-diagonal ratio (double bits, atomicMax; non-negative).
-__global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, Rot *rots,
+// flags[0..1]: per-sweep max off-diagonal ratio (double bits, atomicMax; non-negative);
+// flags[2]: barrier counter / generation (two 32-bit words, zero on entry).
+// Per round of the tournament: every block computes all kp/2 rotations of the round into
+// its shared memory (deterministic, identical bits in every block; block 0 records the
+// ratios), then G <- G J and V <- V J (columns p, q), barrier, G <- J^H G (rows p, q),
+// barrier: two grid-wide barriers per round.  Phase A reads only g_pp, g_qq, g_pq of the
+// round's pairs; so that no block's phase B can overwrite them while another block is still
+// in phase A, phase B leaves each pair's own 2 x 2 block (rows p, q of columns p, q) in G
+// untouched and writes it to the scratch B4 (4 entries per pair), which phase C reads.
+__global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, Rot *scratch,
                                                 unsigned long long *flags, int *sweeps_out) {
-    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char jsm[];
+    Rot *rots = reinterpret_cast<Rot *>(jsm);
+    double2 *B4 = reinterpret_cast<double2 *>(scratch);  // [pair][(row q?) + 2 (col q?)]
+    unsigned *bar = reinterpret_cast<unsigned *>(flags + 2);
+    const unsigned nblocks = gridDim.x;
     const int half = kp / 2;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
     const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -141,35 +213,13 @@ __global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, 
     for (; sweep < 40; sweep++) {
         unsigned long long *flag = &flags[sweep & 1];
         for (int r = 0; r < kp - 1; r++) {
-            // A: rotation parameters from the current 2x2 blocks
-            for (long long i = gtid; i < half; i += nthreads) {
+            // A: this round's rotations from the current 2x2 blocks (every block)
+            for (int i = threadIdx.x; i < half; i += blockDim.x) {
                 int p, q;
-                round_pair(r, (int)i, kp, p, q);
-                const double a = G[p + (long long)p * kp].x, b = G[q + (long long)q * kp].x;
-                const double2 c = G[p + (long long)q * kp];  // g_pq
-                const double ac = sqrt(c.x * c.x + c.y * c.y);
-                Rot R;
-                R.p = p;
-                R.q = q;
-                if (ac == 0.0) {
-                    R.cs = 1.0;
-                    R.sn = 0.0;
-                    R.er = 1.0;
-                    R.ei = 0.0;
-                } else {
-                    const double den = sqrt(fabs(a * b));
-                    const double ratio = den > 0.0 ? ac / den : 1.0;
-                    atomicMax(flag, dbits(ratio));
-                    const double tau = (b - a) / (2.0 * ac);
-                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    R.cs = 1.0 / sqrt(1.0 + t * t);
-                    R.sn = t * R.cs;
-                    R.er = c.x / ac;
-                    R.ei = c.y / ac;
-                }
-                rots[i] = R;
+                round_pair(r, i, kp, p, q);
+                rots[i] = make_rot(G, kp, p, q, flag, blockIdx.x == 0);
             }
-            grid.sync();
+            __syncthreads();
             // B: columns p, q of G and V: G <- G J, V <- V J
             for (long long e = gtid; e < (long long)half * kp * 2; e += nthreads) {
                 const long long pair = e / (2LL * kp), rem = e % (2LL * kp);
@@ -179,16 +229,32 @@ __global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, 
                 const double2 gp = M[row + (long long)R.p * kp], gq = M[row + (long long)R.q * kp];
                 // e^{-i phi} g_q
                 const double2 eq = make_double2(R.er * gq.x + R.ei * gq.y, R.er * gq.y - R.ei * gq.x);
-                M[row + (long long)R.p * kp] = make_double2(R.cs * gp.x - R.sn * eq.x, R.cs * gp.y - R.sn * eq.y);
-                M[row + (long long)R.q * kp] = make_double2(R.sn * gp.x + R.cs * eq.x, R.sn * gp.y + R.cs * eq.y);
+                const double2 np = make_double2(R.cs * gp.x - R.sn * eq.x, R.cs * gp.y - R.sn * eq.y);
+                const double2 nq = make_double2(R.sn * gp.x + R.cs * eq.x, R.sn * gp.y + R.cs * eq.y);
+                if (M == G && (row == R.p || row == R.q)) {
+                    const int rq = row == R.q ? 1 : 0;
+                    B4[pair * 4 + rq] = np;       // (row, p) after B
+                    B4[pair * 4 + rq + 2] = nq;   // (row, q) after B
+                } else {
+                    M[row + (long long)R.p * kp] = np;
+                    M[row + (long long)R.q * kp] = nq;
+                }
             }
-            grid.sync();
+            grid_barrier(bar, bar + 1, nblocks);
             // C: rows p, q of G: G <- J^H G, and the annihilated pair set to zero
             for (long long e = gtid; e < (long long)half * kp; e += nthreads) {
                 const long long pair = e / kp;
                 const int col = (int)(e % kp);
                 const Rot R = rots[pair];
-                const double2 rp = G[R.p + (long long)col * kp], rq = G[R.q + (long long)col * kp];
+                double2 rp, rq;
+                if (col == R.p || col == R.q) {
+                    const int cq = col == R.q ? 2 : 0;
+                    rp = B4[pair * 4 + cq];
+                    rq = B4[pair * 4 + 1 + cq];
+                } else {
+                    rp = G[R.p + (long long)col * kp];
+                    rq = G[R.q + (long long)col * kp];
+                }
                 // e^{i phi} r_q
                 const double2 eq = make_double2(R.er * rq.x - R.ei * rq.y, R.er * rq.y + R.ei * rq.x);
                 double2 np = make_double2(R.cs * rp.x - R.sn * eq.x, R.cs * rp.y - R.sn * eq.y);
@@ -200,12 +266,12 @@ __global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, 
                 G[R.p + (long long)col * kp] = np;
                 G[R.q + (long long)col * kp] = nq;
             }
-            grid.sync();
+            grid_barrier(bar, bar + 1, nblocks);
         }
         const double off = __longlong_as_double((long long)*(volatile unsigned long long *)flag);
-        grid.sync();  // everybody has read this sweep's flag
+        grid_barrier(bar, bar + 1, nblocks);  // everybody has read this sweep's flag
         if (gtid == 0) flags[(sweep + 1) & 1] = 0ull;
-        grid.sync();
+        grid_barrier(bar, bar + 1, nblocks);
         if (off < 1e-15) {
             sweep++;
             break;
@@ -245,31 +311,33 @@ __global__ void k_recon_x(const double2 *Q, long long ldq_v, long long nvec, int
 
 // Eigenvalues (diag of the converged G) in descending order, ties by index; sigma =
 // sqrt(max(lambda, 0)); kr = #{sigma > tau2} capped at kr_max (Algorithm 4 step 6).
-__global__ void k_eig_sort(const double2 *G, int k, int kp, double tau2, int kr_max, int *order, double *sigma,
-                           int *kr) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    for (int i = 0; i < k; i++) order[i] = i;
-    for (int i = 0; i < k; i++) {  // selection sort: k is small
-        int best = i;
-        for (int j = i + 1; j < k; j++) {
-            const double lj = G[order[j] + (long long)order[j] * kp].x, lb = G[order[best] + (long long)order[best] * kp].x;
-            if (lj > lb || (lj == lb && order[j] < order[best])) best = j;
+// Eigenvalues (the converged diagonal of G) in descending order, ties by index, as a rank
+// sort: element i goes to position #{j : l_j > l_i or (l_j == l_i and j < i)}; sigma = sqrt of
+// the clamped values; kr = length of the prefix with sigma > tau2, capped at kr_max.
+__global__ void __launch_bounds__(1024) k_eig_sort(const double2 *G, int k, int kp, double tau2, int kr_max,
+                                                   int *order, double *sigma, int *kr) {
+    __shared__ int s_first;  // first position with sigma <= tau2
+    if (threadIdx.x == 0) s_first = k;
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const double li = G[i + (long long)i * kp].x;
+        int r = 0;
+        for (int j = 0; j < k; j++) {
+            const double lj = G[j + (long long)j * kp].x;
+            r += (lj > li || (lj == li && j < i)) ? 1 : 0;
         }
-        const int t = order[i];
-        order[i] = order[best];
-        order[best] = t;
+        order[r] = i;
+        const double sg = sqrt(fmax(li, 0.0));
+        sigma[r] = sg;
+        if (!(sg > tau2)) atomicMin(&s_first, r);
     }
-    int n = 0;
-    for (int i = 0; i < k; i++) {
-        sigma[i] = sqrt(fmax(G[order[i] + (long long)order[i] * kp].x, 0.0));
-        if (sigma[i] > tau2 && n == i) n = i + 1;
-    }
-    *kr = n < kr_max ? n : kr_max;
+    __syncthreads();
+    if (threadIdx.x == 0) *kr = s_first < kr_max ? s_first : kr_max;
 }
 
 cudaError_t launch_eig_sort(const double2 *G, int k, int kp, double tau2, int kr_max, int *order, double *sigma,
                             int *kr, cudaStream_t s) {
-    k_eig_sort<<<1, 32, 0, s>>>(G, k, kp, tau2, kr_max, order, sigma, kr);
+    k_eig_sort<<<1, 1024, 0, s>>>(G, k, kp, tau2, kr_max, order, sigma, kr);
     return cudaGetLastError();
 }
 
@@ -290,15 +358,23 @@ cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int k
 
 cudaError_t launch_jacobi(double2 *G, double2 *V, int kp, Rot *rots, unsigned long long *flags, int *sweeps,
                           int num_sms, cudaStream_t s) {
+    const size_t smem = rot_bytes(kp);
+    cudaError_t e = cudaSuccess;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, 256, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, 256, smem);
     if (e != cudaSuccess) return e;
+    // one block per SM at most: the per-round work is small and the barrier cost grows with
+    // the number of arriving blocks
     const int want = (kp * kp + 255) / 256;
-    int grid = per_sm * num_sms;
+    int grid = (per_sm > 0 ? 1 : 0) * num_sms;
     if (grid > want) grid = want;
     if (grid < 1) grid = 1;
     void *args[] = {&G, &V, &kp, &rots, &flags, &sweeps};
-    return cudaLaunchCooperativeKernel((void *)k_jacobi, grid, 256, args, 0, s);
+    return cudaLaunchCooperativeKernel((void *)k_jacobi, grid, 256, args, smem, s);
 }
 
 cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, int k, const double2 *V, int kp,
@@ -311,5 +387,6 @@ cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, in
 }
 
 size_t rot_bytes(int kp) { return sizeof(Rot) * (size_t)(kp / 2); }
+size_t jacobi_scratch_bytes(int kp) { return 4 * sizeof(double2) * (size_t)(kp / 2); }
 
 }  // namespace rbg

@@ -10,6 +10,9 @@ After the k-iteration greedy on the device-generated config-2 matrix:
   * Algorithm 4 reconstruction: Gram (FP64 FLOP/s against the derived FP64 peak), Jacobi,
     X = Q V; total;
   * greedy EIM nodes of the k-vector basis.
+Beside each GPU number, the CPU oracle (oracle/, as it stands, all host cores) on the same
+data (a column sample for validation, scaled), so every NEXT row is measured against its
+roofline with the oracle timed beside it.
 Prints one JSON line.  Timed with CUDA events / wall clock around blocking ABI calls.
 """
 import argparse
@@ -23,6 +26,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+from oracle import oracle as O  # noqa: E402  (the CPU baseline legs only)
 from paper_1805_06124_b200 import inputs, rbg  # noqa: E402
 
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
@@ -79,6 +83,34 @@ def main():
         nodes, B = ctx.eim()
         out["eim"] = {"s": time.perf_counter() - t0, "k": int(len(nodes)),
                       "cond_B": float(np.linalg.cond(B))}
+        # ---- CPU oracle beside each row (same data; validation on a column sample, scaled)
+        Qh = ctx.basis()
+        Rh = ctx.R()
+        res = ctx.result(full=False)
+        res.Q, res.R = Qh, Rh
+        ncores = len(os.sched_getaffinity(0))
+        ns = 2048
+        Vh = V[:ns].cpu().numpy()
+        t0 = time.perf_counter()
+        O.validate(Qh, Vh, w)
+        tvo = (time.perf_counter() - t0) * a.val_cols / ns
+        out["validate"]["oracle_s"] = tvo
+        out["validate"]["oracle_sample"] = f"{ns} of {a.val_cols} columns, scaled"
+        t0 = time.perf_counter()
+        O.gram(Rh)
+        tgo = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.reconstruct(res, 1e-3)
+        tro = time.perf_counter() - t0
+        out["reconstruct"].update({"oracle_gram_s": tgo, "oracle_total_s": tro,
+                                   "jacobi_and_x_s": tr - tg,
+                                   "note": "oracle eigen-step = LAPACK eigh (a library step of the oracle)"})
+        t0 = time.perf_counter()
+        O.eim(Qh)
+        out["eim"].update({"oracle_s": time.perf_counter() - t0,
+                           "us_per_step": out["eim"]["s"] / max(len(nodes), 1) * 1e6,
+                           "bound": "latency (k dependent argmax-over-N steps, one forward substitution each)"})
+        out["oracle_cores"] = ncores
         # ---- f-1 enrichment step
         t0 = time.perf_counter()
         ctx.add_columns(V[:4096])
