@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1109,7 +1110,11 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     const int k = (int)h.k;
     if (kr_out) *kr_out = 0;
     if (k == 0) return RBG_OK;
-    const int kp = k + (k & 1);
+    // block Jacobi (default) pads to a multiple of 32; RBG_JACOBI=elem selects the element
+    // cyclic Jacobi (pads to even)
+    const char *jenv = getenv("RBG_JACOBI");
+    const bool block = !(jenv && std::strcmp(jenv, "elem") == 0);
+    const int kp = block ? jacobi_pad(k) : k + (k & 1);
     double2 *G = nullptr, *V = nullptr, *Xd = nullptr;
     Rot *rots = nullptr;
     unsigned long long *flags = nullptr;
@@ -1117,7 +1122,7 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     double *sig = nullptr;
     cudaError_t e = dmalloc(&G, sizeof(double2) * (size_t)kp * kp);
     if (e == cudaSuccess) e = dmalloc(&V, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = dmalloc(&rots, jacobi_scratch_bytes(kp));  // k_jacobi scratch
+    if (e == cudaSuccess) e = dmalloc(&rots, block ? bjacobi_scratch_bytes(kp) : jacobi_scratch_bytes(kp));
     if (e == cudaSuccess) e = dmalloc(&flags, 3 * sizeof(unsigned long long));  // ratios + barrier
     if (e == cudaSuccess) e = dmalloc(&sweeps, sizeof(int));
     if (e == cudaSuccess) e = dmalloc(&order, sizeof(int) * kp);
@@ -1130,11 +1135,19 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
         for (int i = 0; i < kp; i++) I[(size_t)i * kp + i] = make_double2(1.0, 0.0);
         e = cudaMemcpyAsync(V, I.data(), sizeof(double2) * I.size(), cudaMemcpyHostToDevice, c->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned long long), c->stream);
-        if (e == cudaSuccess) e = launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
+        if (e == cudaSuccess)
+            e = block ? launch_bjacobi(G, V, kp, reinterpret_cast<double2 *>(rots), flags, sweeps, c->num_sms, c->stream)
+                      : launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
         if (e == cudaSuccess)
             e = launch_eig_sort(G, k, kp, tau2, (int)std::min<int64_t>(kr_max ? kr_max : k, k), order, sig, krd,
                                 c->stream);
         int kr = 0;
+        if (e == cudaSuccess && getenv("RBG_DEBUG_JACOBI")) {
+            int sw = 0;
+            cudaMemcpyAsync(&sw, sweeps, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
+            fprintf(stderr, "rbg: jacobi (%s) k=%d kp=%d sweeps=%d\n", block ? "block" : "elem", k, kp, sw);
+        }
         if (e == cudaSuccess) e = cudaMemcpyAsync(&kr, krd, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && sigma) e = cudaMemcpy(sigma, sig, sizeof(double) * k, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);

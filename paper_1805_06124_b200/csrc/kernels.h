@@ -150,6 +150,11 @@ cudaError_t launch_recon_x(const double2 *Q, long long ldq_v, long long nvec, in
                            const int *order, int kr, double2 *X, long long ldx_v, bool cplx, cudaStream_t s);
 size_t rot_bytes(int kp);
 size_t jacobi_scratch_bytes(int kp);  // k_jacobi's per-pair 2 x 2 scratch
+// Block Jacobi (k_bjacobi): kp = jacobi_pad(k) (a multiple of 32), scratch U per block pair.
+int jacobi_pad(int k);
+size_t bjacobi_scratch_bytes(int kp);
+cudaError_t launch_bjacobi(double2 *G, double2 *V, int kp, double2 *Us, unsigned long long *flags, int *sweeps,
+                           int num_sms, cudaStream_t s);
 
 // Greedy EIM nodes (eim.cu): nodes_d[k], B_d = Q(P, :) k x k column-major complex.
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,

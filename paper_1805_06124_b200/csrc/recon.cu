@@ -280,6 +280,191 @@ __global__ void __launch_bounds__(256) k_jacobi(double2 *G, double2 *V, int kp, 
     if (gtid == 0) *sweeps_out = sweep;
 }
 
+// ------------------------------------------------------------------ block Jacobi
+// Two-sided block Jacobi on the Hermitian G (kp x kp, kp a multiple of 2 kJB): the index set
+// is cut into nb = kp / kJB blocks paired by the round-robin tournament (nb - 1 rounds per
+// sweep, nb / 2 block pairs per round).  Per round, in one cooperative grid:
+//   P1  one CTA per block pair (I, J): A = G[I u J, I u J] (32 x 32) into shared memory, one
+//       cyclic 2 x 2 Jacobi sweep on A (the same rotation formulas as k_jacobi) accumulating
+//       U = J_1 J_2 ...; U to a scratch; the max off-diagonal ratio of A before the sweep
+//       feeds the convergence flag;
+//   P2  G[:, I u J] <- G[:, I u J] U and V[:, I u J] <- V[:, I u J] U (one warp per row);
+//   P3  G[I u J, :] <- U^H G[I u J, :] (one warp per column), diagonal made real;
+// with a grid barrier after each phase: 3 (nb - 1) barriers per sweep instead of 2 (kp - 1).
+constexpr int kJB = 16;        // block size
+constexpr int kJL = 2 * kJB;   // local problem size (one warp wide)
+
+__device__ __forceinline__ int blk_idx(int I, int J, int a) { return a < kJB ? I * kJB + a : J * kJB + (a - kJB); }
+
+__global__ void __launch_bounds__(256) k_bjacobi(double2 *G, double2 *V, int kp, double2 *Us,
+                                                 unsigned long long *flags, int *sweeps_out) {
+    __shared__ double2 A[kJL][kJL + 1];   // A[row][col]
+    __shared__ double2 U[kJL][kJL + 1];
+    __shared__ Rot srot[kJL / 2];
+    unsigned *bar = reinterpret_cast<unsigned *>(flags + 2);
+    const unsigned nblocks = gridDim.x;
+    const int nb = kp / kJB, npairs = nb / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long gwarp = blockIdx.x * (long long)(blockDim.x >> 5) + warp;
+    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+    int sweep = 0;
+    for (; sweep < 40; sweep++) {
+        unsigned long long *flag = &flags[sweep & 1];
+        for (int r = 0; r < nb - 1; r++) {
+            // ---- P1: local problems
+            for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+                int I, J;
+                round_pair(r, pr, nb, I, J);
+                for (int e = tid; e < kJL * kJL; e += blockDim.x) {
+                    const int a = e % kJL, b = e / kJL;
+                    A[a][b] = G[blk_idx(I, J, a) + (long long)blk_idx(I, J, b) * kp];
+                    U[a][b] = make_double2(a == b ? 1.0 : 0.0, 0.0);
+                }
+                __syncthreads();
+                for (int e = tid; e < kJL * kJL; e += blockDim.x) {  // convergence measure
+                    const int a = e % kJL, b = e / kJL;
+                    if (a < b) {
+                        const double2 c = A[a][b];
+                        const double ac = sqrt(c.x * c.x + c.y * c.y);
+                        if (ac > 0.0) {
+                            const double den = sqrt(fabs(A[a][a].x * A[b][b].x));
+                            atomicMax(flag, dbits(den > 0.0 ? ac / den : 1.0));
+                        }
+                    }
+                }
+                for (int lr = 0; lr < kJL - 1; lr++) {
+                    if (tid < kJL / 2) {
+                        int p, q;
+                        round_pair(lr, tid, kJL, p, q);
+                        const double a = A[p][p].x, b = A[q][q].x;
+                        const double2 c = A[p][q];
+                        const double ac = sqrt(c.x * c.x + c.y * c.y);
+                        Rot R;
+                        R.p = p;
+                        R.q = q;
+                        if (ac == 0.0) {
+                            R.cs = 1.0;
+                            R.sn = 0.0;
+                            R.er = 1.0;
+                            R.ei = 0.0;
+                        } else {
+                            const double tau = (b - a) / (2.0 * ac);
+                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                            R.cs = 1.0 / sqrt(1.0 + t * t);
+                            R.sn = t * R.cs;
+                            R.er = c.x / ac;
+                            R.ei = c.y / ac;
+                        }
+                        srot[tid] = R;
+                    }
+                    __syncthreads();
+                    // columns p, q of A and U: X <- X J
+                    for (int e = tid; e < (kJL / 2) * kJL * 2; e += blockDim.x) {
+                        const int pi = e / (2 * kJL), rem = e % (2 * kJL), row = rem % kJL;
+                        double2(*M)[kJL + 1] = rem < kJL ? A : U;
+                        const Rot R = srot[pi];
+                        const double2 gp = M[row][R.p], gq = M[row][R.q];
+                        const double2 eq = make_double2(R.er * gq.x + R.ei * gq.y, R.er * gq.y - R.ei * gq.x);
+                        M[row][R.p] = make_double2(R.cs * gp.x - R.sn * eq.x, R.cs * gp.y - R.sn * eq.y);
+                        M[row][R.q] = make_double2(R.sn * gp.x + R.cs * eq.x, R.sn * gp.y + R.cs * eq.y);
+                    }
+                    __syncthreads();
+                    // rows p, q of A: A <- J^H A
+                    for (int e = tid; e < (kJL / 2) * kJL; e += blockDim.x) {
+                        const int pi = e / kJL, col = e % kJL;
+                        const Rot R = srot[pi];
+                        const double2 rp = A[R.p][col], rq = A[R.q][col];
+                        const double2 eq = make_double2(R.er * rq.x - R.ei * rq.y, R.er * rq.y + R.ei * rq.x);
+                        double2 np = make_double2(R.cs * rp.x - R.sn * eq.x, R.cs * rp.y - R.sn * eq.y);
+                        double2 nq = make_double2(R.sn * rp.x + R.cs * eq.x, R.sn * rp.y + R.cs * eq.y);
+                        if (col == R.q) np = make_double2(0.0, 0.0);
+                        if (col == R.p) nq = make_double2(0.0, 0.0);
+                        if (col == R.p) np.y = 0.0;
+                        if (col == R.q) nq.y = 0.0;
+                        A[R.p][col] = np;
+                        A[R.q][col] = nq;
+                    }
+                    __syncthreads();
+                }
+                double2 *Up = Us + (size_t)pr * kJL * kJL;   // column-major 32 x 32
+                for (int e = tid; e < kJL * kJL; e += blockDim.x) Up[e] = U[e % kJL][e / kJL];
+                __syncthreads();
+            }
+            grid_barrier(bar, bar + 1, nblocks);
+            // ---- P2: columns: M[row, I u J] <- M[row, I u J] U, one warp per (pair, matrix, row)
+            for (long long it = gwarp; it < (long long)npairs * 2 * kp; it += nwarps) {
+                const int pr = (int)(it / (2LL * kp)), rem = (int)(it % (2LL * kp)), row = rem % kp;
+                double2 *M = rem < kp ? G : V;
+                int I, J;
+                round_pair(r, pr, nb, I, J);
+                const double2 *Up = Us + (size_t)pr * kJL * kJL;
+                const long long col = blk_idx(I, J, lane);
+                const double2 x = M[row + col * kp];
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+                for (int m = 0; m < kJL; m++) {
+                    const double xr = __shfl_sync(0xffffffffu, x.x, m), xi = __shfl_sync(0xffffffffu, x.y, m);
+                    const double2 u = __ldg(&Up[m + lane * kJL]);   // U[m][lane]
+                    acc.x = fma(xr, u.x, acc.x);
+                    acc.x = fma(-xi, u.y, acc.x);
+                    acc.y = fma(xr, u.y, acc.y);
+                    acc.y = fma(xi, u.x, acc.y);
+                }
+                M[row + col * kp] = acc;
+            }
+            grid_barrier(bar, bar + 1, nblocks);
+            // ---- P3: rows: G[I u J, col] <- U^H G[I u J, col], one warp per (pair, column)
+            for (long long it = gwarp; it < (long long)npairs * kp; it += nwarps) {
+                const int pr = (int)(it / kp), col = (int)(it % kp);
+                int I, J;
+                round_pair(r, pr, nb, I, J);
+                const double2 *Up = Us + (size_t)pr * kJL * kJL;
+                const long long row = blk_idx(I, J, lane);
+                const double2 y = G[row + (long long)col * kp];
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+                for (int m = 0; m < kJL; m++) {
+                    const double yr = __shfl_sync(0xffffffffu, y.x, m), yi = __shfl_sync(0xffffffffu, y.y, m);
+                    const double2 u = __ldg(&Up[m + lane * kJL]);   // conj(U[m][lane]) y_m
+                    acc.x = fma(u.x, yr, acc.x);
+                    acc.x = fma(u.y, yi, acc.x);
+                    acc.y = fma(u.x, yi, acc.y);
+                    acc.y = fma(-u.y, yr, acc.y);
+                }
+                if (row == col) acc.y = 0.0;  // Hermitian: real diagonal
+                G[row + (long long)col * kp] = acc;
+            }
+            grid_barrier(bar, bar + 1, nblocks);
+        }
+        const double off = __longlong_as_double((long long)*(volatile unsigned long long *)flag);
+        grid_barrier(bar, bar + 1, nblocks);
+        if (blockIdx.x == 0 && tid == 0) flags[(sweep + 1) & 1] = 0ull;
+        grid_barrier(bar, bar + 1, nblocks);
+        if (off < 1e-15) {
+            sweep++;
+            break;
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) *sweeps_out = sweep;
+}
+
+int jacobi_pad(int k) {  // kp for the block Jacobi: a multiple of 2 kJB
+    return (k + kJL - 1) / kJL * kJL;
+}
+
+size_t bjacobi_scratch_bytes(int kp) { return sizeof(double2) * (size_t)(kp / kJL) * kJL * kJL; }
+
+cudaError_t launch_bjacobi(double2 *G, double2 *V, int kp, double2 *Us, unsigned long long *flags, int *sweeps,
+                           int num_sms, cudaStream_t s) {
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, 256, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    int grid = num_sms;
+    void *args[] = {&G, &V, &kp, &Us, &flags, &sweeps};
+    return cudaLaunchCooperativeKernel((void *)k_bjacobi, grid, 256, args, 0, s);
+}
+
 // X(:, r) = Q V(:, order[r]) for r < kr: X is N_v x kr vectors (column stride ldx_v), Q is
 // k columns of nvec vectors (stride ldq_v); each element a sequential sum over i.
 template <bool CPLX>
