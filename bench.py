@@ -117,15 +117,30 @@ def ncu_traffic():
         return None
 
 
-def cpu_sample(cols: int, iters: int, cfg: int = 2):
-    """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
+def cpu_sample(cols: int, iters: int, cfg: int = 2, S=None):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: the first `cols`
+    columns of the device matrix when given (the same bytes the GPU streamed), else the same
+    recipe generated on the host."""
     from oracle import oracle as O
     from paper_1805_06124_b200 import inputs
-    S, w, _, _ = inputs.config2(M=cols, N=N_ROWS, cfg=cfg)
+    if S is None:
+        S, w, _, _ = inputs.config2(M=cols, N=N_ROWS, cfg=cfg)
+    else:
+        w = inputs.simpson_weights(N_ROWS)
     t0 = time.perf_counter()
     r = O.greedy(S, w, 0.0, max(K_MAX, iters), lanes=O.CANONICAL, max_iters=iters)
     wall = time.perf_counter() - t0
     return r, wall
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def oracle_cores() -> int:
@@ -304,6 +319,9 @@ def run_ours(a):
         "gpu_launches": (3 if comm == rbg.COMM_PEER else 2) * K,
     }
 
+    # the oracle's sample: the first CPU_SAMPLE_COLS columns of the very bytes the GPU streamed
+    host_sample = S[:CPU_SAMPLE_COLS].cpu().numpy() if (rank == 0 and world == 1 and not a.no_cpu) else None
+
     # ---- end to end through the C ABI with host buffers (pinned), all iterations
     if not a.no_e2e:
         # the host copy needs |S| of pinned RAM per rank on this node: all ranks agree first
@@ -330,13 +348,17 @@ def run_ours(a):
     # ---- CPU oracle baseline (rank 0, one GPU only): the same k window as the timed
     # region (iterations W..W+K-1), on a bounded column sample (~10-30 s of CPU work)
     if rank == 0 and world == 1 and not a.no_cpu:
-        r, wall = cpu_sample(CPU_SAMPLE_COLS, W + K)
+        r, wall = cpu_sample(CPU_SAMPLE_COLS, W + K, S=host_sample)
+        del host_sample
         t_full = full_iter_seconds(r, W, W + K, CPU_SAMPLE_COLS, M_glob)
+        sweep_s = float(np.mean(np.asarray(r.t_iter[W:W + K]) - np.asarray(r.t_imgs[W:W + K])))
         line["cpu_baseline"] = {
             "value": 1.0 / t_full, "unit": "it/s", "cores": oracle_cores(), "kind": "oracle",
-            "sample": f"CPU oracle (canonical lanes, OpenMP) on {CPU_SAMPLE_COLS} of {M_glob} columns "
-                      f"x {N} rows of the same recipe, iterations {W}..{W + K - 1} ({wall:.1f} s wall); "
-                      f"sweep+pivot time scaled by {M_glob}/{CPU_SAMPLE_COLS}, IMGS as measured"}
+            "cpu_model": cpu_model(),
+            "sweep_gbs": CPU_SAMPLE_COLS * N * 16 / sweep_s / 1e9,
+            "sample": f"CPU oracle (canonical lanes, OpenMP) on the first {CPU_SAMPLE_COLS} of the {M_glob} "
+                      f"device columns (same bytes) x {N} rows, iterations {W}..{W + K - 1} ({wall:.1f} s "
+                      f"wall); sweep+pivot time scaled by {M_glob}/{CPU_SAMPLE_COLS}, IMGS as measured"}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
