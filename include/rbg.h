@@ -221,6 +221,18 @@ rbg_status rbg_gram(rbg_ctx *ctx, void *G, int64_t ldg, int on_device);
 rbg_status rbg_reconstruct(rbg_ctx *ctx, double tau2, int64_t kr_max, int64_t *kr, double *sigma, void *X,
                            int64_t ldx, int on_device);
 
+/* Sharded Algorithm 4 (column-sharded contexts; any world size).  rbg_gram_fold: G (k x k
+ * complex column-major, leading dimension ldg >= k, host or device) holds the Gram sum of the
+ * previous ranks (zeros on rank 0) and is replaced by G + R_loc R_loc^H, this rank's columns
+ * summed in chunks of 4096 local columns, each chunk added onto G in order (real and imaginary
+ * parts independently, diagonal made real).  Folding the ranks in rank order gives exactly
+ * rbg_gram of one context holding all columns when every rank's col_offset is a multiple of
+ * 4096 (reading R33).  rbg_reconstruct_gram: Algorithm 4 from a given Hermitian G
+ * (e.g. the folded one, identical on every rank) -- outputs as rbg_reconstruct.           */
+rbg_status rbg_gram_fold(rbg_ctx *ctx, void *G, int64_t ldg, int on_device);
+rbg_status rbg_reconstruct_gram(rbg_ctx *ctx, const void *G, int64_t ldg, int G_on_device, double tau2,
+                                int64_t kr_max, int64_t *kr, double *sigma, void *X, int64_t ldx, int on_device);
+
 /* Empirical interpolation nodes (standard greedy EIM in residual form,
  * DESIGN.md reading R31) for the current basis: nodes[k] row indices (distinct; ties -> lowest
  * row) and B = Q(nodes, :), the k x k node matrix (column-major, leading dimension ldb >= k,

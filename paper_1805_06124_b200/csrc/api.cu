@@ -1052,8 +1052,9 @@ rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, 
 }
 
 namespace {
-// G = R(0:k, :) R(0:k, :)^H into a zero-padded kp x kp column-major device buffer.
-rbg_status gram_device(rbg_ctx *c, int k, int kp, double2 *G) {
+// G = G0 + R(0:k, :) R(0:k, :)^H into a zero-padded kp x kp column-major device buffer
+// (G0: same layout, or NULL for zero; the running sum of the previous ranks when folding).
+rbg_status gram_device(rbg_ctx *c, int k, int kp, const double2 *G0, double2 *G) {
     const long long nchunks = std::max<long long>(1, (c->M + kGramChunk - 1) / kGramChunk);
     const int nt = (k + gram_tile() - 1) / gram_tile();
     std::vector<int2> tiles;
@@ -1067,7 +1068,7 @@ rbg_status gram_device(rbg_ctx *c, int k, int kp, double2 *G) {
         e = cudaMemcpyAsync(tiles_d, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess)
         e = launch_gram(c->R, c->M, k, c->M, c->cplx, P, kGramChunk, nchunks, tiles_d, (int)tiles.size(), c->stream);
-    if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G, c->stream);
+    if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G0, G, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     dfree(tiles_d);
     dfree(P);
@@ -1088,7 +1089,7 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     const int kp = k + (k & 1);
     double2 *Gd = nullptr;
     CU(dmalloc(&Gd, sizeof(double2) * (size_t)kp * kp));
-    rbg_status st = gram_device(c, k, kp, Gd);
+    rbg_status st = gram_device(c, k, kp, nullptr, Gd);
     if (st == RBG_OK) {
         cudaError_t e = cudaMemcpy2D(G, (size_t)ldg * 16, Gd, (size_t)kp * 16, (size_t)k * 16, k,
                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
@@ -1098,11 +1099,41 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     return st;
 }
 
-rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_out, double *sigma, void *X,
-                           int64_t ldx, int on_device) {
+rbg_status rbg_gram_fold(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     TRY(check_ctx(c));
     if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
-    if (c->world != 1) return fail(RBG_ESTATE, "reconstruct needs a single-GPU context");
+    if (c->local_pending) return fail(RBG_ESTATE, "gram_fold inside an EXTERNAL/PEER iteration");
+    DevState h;
+    TRY(read_state(c, &h));
+    const int k = (int)h.k;
+    if (!G || ldg < k) return fail(RBG_EINVAL, "null G or ldg < k");
+    if (k == 0) return RBG_OK;
+    const int kp = k + (k & 1);
+    const cudaMemcpyKind in = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaMemcpyKind out = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    double2 *G0 = nullptr, *G1 = nullptr;
+    cudaError_t e = dmalloc(&G0, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = dmalloc(&G1, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = cudaMemsetAsync(G0, 0, sizeof(double2) * (size_t)kp * kp, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(G0, (size_t)kp * 16, G, (size_t)ldg * 16, (size_t)k * 16, k, in, c->stream);
+    rbg_status st = e == cudaSuccess ? gram_device(c, k, kp, G0, G1) : fail(RBG_ECUDA, "gram_fold: %s", cudaGetErrorString(e));
+    if (st == RBG_OK) {
+        e = cudaMemcpy2D(G, (size_t)ldg * 16, G1, (size_t)kp * 16, (size_t)k * 16, k, out);
+        if (e != cudaSuccess) st = fail(RBG_ECUDA, "gram_fold copy: %s", cudaGetErrorString(e));
+    }
+    dfree(G0);
+    dfree(G1);
+    return st;
+}
+
+namespace {
+// Algorithm 4 after the Gram matrix: Gin = NULL -> this context's R R^H; else the given k x k
+// Hermitian matrix (leading dimension ldg, host or device), e.g. a sharded fold.
+rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_device, double tau2, int64_t kr_max,
+                            int64_t *kr_out, double *sigma, void *X, int64_t ldx, int on_device) {
+    TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
+    if (!Gin && c->world != 1) return fail(RBG_ESTATE, "reconstruct needs a single-GPU context (sharded: rbg_gram_fold + rbg_reconstruct_gram)");
     if (!(tau2 >= 0.0) || kr_max < 0) return fail(RBG_EINVAL, "tau2 < 0 or kr_max < 0");
     if (X && ldx < c->N) return fail(RBG_EINVAL, "ldx < N");
     DevState h;
@@ -1129,7 +1160,15 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     if (e == cudaSuccess) e = dmalloc(&krd, sizeof(int));
     if (e == cudaSuccess) e = dmalloc(&sig, sizeof(double) * kp);
     rbg_status st = e == cudaSuccess ? RBG_OK : fail(RBG_ENOMEM, "reconstruct buffers: %s", cudaGetErrorString(e));
-    if (st == RBG_OK) st = gram_device(c, k, kp, G);
+    if (st == RBG_OK && !Gin) st = gram_device(c, k, kp, nullptr, G);
+    if (st == RBG_OK && Gin) {
+        if (ldg < k) st = fail(RBG_EINVAL, "ldg < k");
+        if (st == RBG_OK) e = cudaMemsetAsync(G, 0, sizeof(double2) * (size_t)kp * kp, c->stream);
+        if (st == RBG_OK && e == cudaSuccess)
+            e = cudaMemcpy2DAsync(G, (size_t)kp * 16, Gin, (size_t)ldg * 16, (size_t)k * 16, k,
+                                  g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream);
+        if (st == RBG_OK && e != cudaSuccess) st = fail(RBG_ECUDA, "reconstruct upload: %s", cudaGetErrorString(e));
+    }
     if (st == RBG_OK) {
         std::vector<double2> I((size_t)kp * kp, make_double2(0.0, 0.0));
         for (int i = 0; i < kp; i++) I[(size_t)i * kp + i] = make_double2(1.0, 0.0);
@@ -1173,6 +1212,19 @@ rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_
     dfree(krd);
     dfree(sig);
     return st;
+}
+
+}  // namespace
+
+rbg_status rbg_reconstruct(rbg_ctx *c, double tau2, int64_t kr_max, int64_t *kr_out, double *sigma, void *X,
+                           int64_t ldx, int on_device) {
+    return reconstruct_impl(c, nullptr, 0, 0, tau2, kr_max, kr_out, sigma, X, ldx, on_device);
+}
+
+rbg_status rbg_reconstruct_gram(rbg_ctx *c, const void *G, int64_t ldg, int g_on_device, double tau2, int64_t kr_max,
+                                int64_t *kr_out, double *sigma, void *X, int64_t ldx, int on_device) {
+    if (!G) return fail(RBG_EINVAL, "null G");
+    return reconstruct_impl(c, G, ldg, g_on_device, tau2, kr_max, kr_out, sigma, X, ldx, on_device);
 }
 
 rbg_status rbg_eim(rbg_ctx *c, int64_t *nodes, void *B, int64_t ldb, int on_device) {

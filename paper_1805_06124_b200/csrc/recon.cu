@@ -98,15 +98,19 @@ __global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, in
         }
 }
 
-// G (kp x kp column-major, ld kp, zero padded) from chunk partials, summed in chunk order;
-// the lower triangle is the conjugate of the upper.
-__global__ void k_gram_reduce(const double2 *P, long long nchunks, int k, int kp, double2 *G) {
+// G (kp x kp column-major, ld kp, zero padded) from chunk partials, summed in chunk order,
+// starting from G0 (the running sum of the previous ranks of a sharded context, same layout)
+// or from zero; the lower triangle is the conjugate of the upper.  Real and imaginary parts
+// are independent sums, so zeroing the diagonal's imaginary part between ranks does not
+// change any other bit.
+__global__ void k_gram_reduce(const double2 *P, long long nchunks, int k, int kp, const double2 *G0, double2 *G) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)kp * kp;
          e += (long long)gridDim.x * blockDim.x) {
         const int a = (int)(e % kp), b = (int)(e / kp);   // G(a, b) at a + b*kp
         double2 g = make_double2(0.0, 0.0);
         if (a < k && b < k) {
             const int lo = a < b ? a : b, hi = a < b ? b : a;
+            if (G0) g = G0[lo + (long long)hi * kp];        // upper triangle of the running sum
             for (long long c = 0; c < nchunks; c++) {
                 const double2 p = P[(c * k + lo) * k + hi];
                 g.x = g.x + p.x;
@@ -535,9 +539,10 @@ cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool
     return cudaGetLastError();
 }
 
-cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, double2 *G, cudaStream_t s) {
+cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, const double2 *G0, double2 *G,
+                               cudaStream_t s) {
     const long long n = (long long)kp * kp;
-    k_gram_reduce<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(P, nchunks, k, kp, G);
+    k_gram_reduce<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(P, nchunks, k, kp, G0, G);
     return cudaGetLastError();
 }
 

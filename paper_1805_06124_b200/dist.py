@@ -89,3 +89,36 @@ def sharded_context(S_local, w, tol: float, k_max: int, M_global: int, group=Non
     uid = nccl_unique_id(group)
     return rbg.Context(S_local, w, tol, k_max, comm=rbg.COMM_NCCL, rank=rank, world=world,
                        col_offset=off, M_global=M_global, nccl_id=uid, **kw)
+
+
+def fold_over_ranks(fold, k: int, group=None):
+    """Rank-order fold of a k x k complex matrix: rank p receives the running value from rank
+    p - 1 (zeros on rank 0), applies `fold` (G -> G'), passes it to rank p + 1; the last rank's
+    result is broadcast.  Returns it (numpy, G[i, j]) on every rank."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf = torch.zeros((k, k), dtype=torch.complex128, device=dev)
+    ranks = dist.get_process_group_ranks(group) if group is not None else list(range(world))
+    if rank > 0:
+        dist.recv(buf, src=ranks[rank - 1], group=group)
+    G = fold(buf.cpu().numpy())                      # buf[i, j] = G(i, j)
+    buf.copy_(torch.from_numpy(np.ascontiguousarray(G)))
+    if rank < world - 1:
+        dist.send(buf, dst=ranks[rank + 1], group=group)
+    dist.broadcast(buf, src=ranks[world - 1], group=group)
+    return buf.cpu().numpy()
+
+
+def sharded_reconstruct(ctx, tau2: float = 0.0, kr_max: int = 0, group=None):
+    """Algorithm 4 on a column-sharded context: the Gram matrix R R^H is
+    folded rank by rank in rank order (rbg_gram_fold: rank p adds its chunk partials onto the
+    sum of ranks < p), the last rank's sum is broadcast, and every rank runs the eigen-step
+    and X = Q V on the same G (rbg_reconstruct_gram), so sigma and X are replicated.  Equal to
+    the single-GPU rbg_reconstruct bit for bit when every col_offset is a multiple of 4096
+    (R33).  Returns (sigma, kr, X)."""
+    G = fold_over_ranks(ctx.gram_fold, ctx.info()[0], group)
+    return ctx.reconstruct_gram(G, tau2, kr_max)

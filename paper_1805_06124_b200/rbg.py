@@ -98,6 +98,9 @@ SYMBOLS = {
     "rbg_gram": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_reconstruct": ([_P, ctypes.c_double, _I64, ctypes.POINTER(_I64), _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_eim": ([_P, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_gram_fold": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_reconstruct_gram": ([_P, _P, _I64, ctypes.c_int, ctypes.c_double, _I64, ctypes.POINTER(_I64), _P, _P, _I64,
+                              ctypes.c_int], ctypes.c_int),
     "rbg_gen_chirp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
 }
 
@@ -395,6 +398,29 @@ class Context:
         kr = ctypes.c_int64()
         _check(lib().rbg_reconstruct(self.h, float(tau2), int(kr_max), ctypes.byref(kr), sigma.ctypes.data,
                                      X.ctypes.data, self.N, 0))
+        return sigma[:k], kr.value, X[:kr.value]
+
+    def gram_fold(self, G: np.ndarray | None = None) -> np.ndarray:
+        """G + R_loc R_loc^H (rbg_gram_fold): fold this rank's coefficient block onto the
+        running Gram sum of the previous ranks (None = zeros, rank 0)."""
+        k = self.info()[0]
+        buf = (np.zeros((k, k), np.complex128, order="F") if G is None
+               else np.array(G, dtype=np.complex128, order="F", copy=True))   # column-major k x k
+        if buf.shape != (k, k):
+            raise ValueError(f"G must be {k} x {k}")
+        if k:
+            _check(lib().rbg_gram_fold(self.h, buf.ctypes.data, k, 0))
+        return buf
+
+    def reconstruct_gram(self, G: np.ndarray, tau2: float = 0.0, kr_max: int = 0):
+        """Algorithm 4 from a given Gram matrix (rbg_reconstruct_gram): (sigma, kr, X)."""
+        k = self.info()[0]
+        Gf = np.asfortranarray(G, dtype=np.complex128)
+        sigma = np.zeros(max(k, 1))
+        X = np.zeros((max(k, 1), self.N), np.complex128 if self.cplx else np.float64)
+        kr = ctypes.c_int64()
+        _check(lib().rbg_reconstruct_gram(self.h, Gf.ctypes.data, k, 0, float(tau2), int(kr_max), ctypes.byref(kr),
+                                          sigma.ctypes.data, X.ctypes.data, self.N, 0))
         return sigma[:k], kr.value, X[:kr.value]
 
     def eim(self):

@@ -174,3 +174,42 @@ def test_sharded_protocol_equals_single_process():
         np.testing.assert_array_equal(errs, ref.errors)     # same DAG: bit for bit
         np.testing.assert_array_equal(Q, ref.Q)
     assert ref.pivots[0] == 17 and 150 not in ref.pivots
+
+
+# ------------------------------------------------------------------------------ sharded Gram
+
+GRAM_M_SPLIT = (0, 8192, 12388)   # rank blocks start at multiples of the 4,096-column chunk
+
+
+def _gram_problem():
+    rng = np.random.default_rng(5)
+    k, M = 7, GRAM_M_SPLIT[-1]
+    return rng.standard_normal((k, M)) + 1j * rng.standard_normal((k, M))
+
+
+def _gram_fold_protocol(rank):
+    from oracle import oracle as O
+    from paper_1805_06124_b200 import dist as D
+    R = _gram_problem()
+    Rl = R[:, GRAM_M_SPLIT[rank]:GRAM_M_SPLIT[rank + 1]]
+
+    def fold(G):
+        # this rank's chunk partials added onto the running sum in chunk order; a one-chunk
+        # oracle gram is exactly that chunk's partial (0 + x = x)
+        G = G.copy()
+        for j0 in range(0, Rl.shape[1], O.GRAM_CHUNK):
+            G = G + O.gram(Rl[:, j0:j0 + O.GRAM_CHUNK])
+        return G
+
+    return D.fold_over_ranks(fold, R.shape[0])
+
+
+def test_sharded_gram_fold_equals_single_process():
+    """The rank-order Gram fold of dist.sharded_reconstruct over gloo reproduces the oracle's
+    single-process chunked Gram bit for bit when the rank blocks are chunk aligned (R33)."""
+    from oracle import oracle as O
+    ref = O.gram(_gram_problem())
+    for G in run_world(_gram_fold_protocol):
+        G = G.copy()
+        np.fill_diagonal(G, G.diagonal().real)          # the library zeroes it at every fold
+        np.testing.assert_array_equal(G, ref)

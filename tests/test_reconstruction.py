@@ -113,3 +113,56 @@ def test_gpu_reconstruct_parity(orc, case):
     # the GPU basis is W-orthonormal
     Gx = (X_g.conj() * w) @ X_g.T
     np.testing.assert_allclose(Gx, np.eye(kr_g), atol=1e-10)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", [(0, 8192, 12388), (0, 4096, 8192, 12388), (0, 5000, 12388)])
+def test_gpu_sharded_gram_fold_and_reconstruct(orc, split):
+    """Sharded Algorithm 4 (rbg_gram_fold + rbg_reconstruct_gram, R33): column-sharded
+    contexts (EXTERNAL exchange, one GPU) fold the Gram matrix in rank order.  Chunk-aligned
+    rank blocks reproduce the one-context Gram, singular values and basis bit for bit; an
+    unaligned split gives the oracle's per-rank chunked fold bit for bit and the one-context
+    Gram to rounding."""
+    from paper_1805_06124_b200 import inputs, rbg
+    S, w, tol, _ = inputs.config1(M=split[-1], N=600)
+    k_max = 40
+    M = S.shape[0]
+    with rbg.Context(S, w, tol, k_max) as ctx1:
+        ctx1.run()
+        G1 = ctx1.gram()
+        s1, kr1, X1 = ctx1.reconstruct(1e-3)
+        R1 = ctx1.R()
+    world = len(split) - 1
+    ctxs = [rbg.Context(S[split[p]:split[p + 1]], w, tol, k_max, comm=rbg.COMM_EXTERNAL, rank=p, world=world,
+                        col_offset=split[p], M_global=M) for p in range(world)]
+    for _ in range(k_max + 1):
+        for c in ctxs:
+            c.iter_local()
+        rbg.emulate_allgather(ctxs)
+        for c in ctxs:
+            c.iter_finish()
+    G = None
+    for c in ctxs:
+        G = c.gram_fold(G)
+    # the oracle's fold: each rank's 4,096-column chunks of its own block, added in order
+    ref = np.zeros_like(G1)
+    for p in range(world):
+        Rp = R1[:, split[p]:split[p + 1]]
+        for j0 in range(0, Rp.shape[1], orc.GRAM_CHUNK):
+            ref = ref + orc.gram(Rp[:, j0:j0 + orc.GRAM_CHUNK])
+    np.fill_diagonal(ref, ref.diagonal().real)
+    np.testing.assert_array_equal(G, ref)
+    aligned = all(o % orc.GRAM_CHUNK == 0 for o in split[:-1])
+    if aligned:
+        np.testing.assert_array_equal(G, G1)
+    else:
+        np.testing.assert_allclose(G, G1, rtol=0, atol=1e-13 * np.abs(G1).max())
+    for c in ctxs:
+        s, kr, X = c.reconstruct_gram(G, 1e-3)
+        assert kr == kr1
+        if aligned:
+            np.testing.assert_array_equal(s, s1)
+            np.testing.assert_array_equal(X, X1)
+        else:
+            np.testing.assert_allclose(s, s1, rtol=0, atol=1e-12 * s1[0])
+        c.close()
