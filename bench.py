@@ -194,7 +194,7 @@ def config_dict(a, world):
             "k_window": [a.warmup, a.warmup + a.steps], "parallelism": f"column-sharded x{world}",
             "l2": "inputs (65.5 GB/GPU) >> 126 MB L2; no flush",
             "ortho": getattr(a, "ortho", "mgs"), "residual": getattr(a, "residual", "recurrence"),
-            "exchange": (getattr(a, "comm", "peer") if world > 1 else "none"),
+            "exchange": (getattr(a, "comm", "peer") if world > 1 else "none"),  # as requested
             "value_unit": "greedy iterations/s x (cols_global / 409,600) -- plain it/s at 1 GPU"}
 
 
@@ -235,25 +235,48 @@ def run_ours(a):
     S = torch.empty((M_loc, N), dtype=torch.complex128, device=dev)
     rbg.gen_chirp(S, t_grid, w, q[sl], chi[sl], psi[sl], spin=True)
 
-    nccl_id = None
+    stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
+    torch.cuda.set_stream(stream)
+
+    def make_ctx(comm):
+        nccl_id = D.nccl_unique_id() if comm == rbg.COMM_NCCL else None
+        ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
+                          world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id, ortho=a.ortho,
+                          residual=a.residual, peer_timeout_ms=20000)
+        if comm == rbg.COMM_PEER:
+            D.connect_peers(ctx)
+        ctx.set_timing(True)
+        if a.graph_batch:
+            ctx.set_graph_batch(a.graph_batch)
+        ctx.step(W)                                  # warm-up: sweep 0 + W iterations
+        torch.cuda.synchronize()
+        return ctx
+
     comm = rbg.COMM_NONE
     if world > 1:
         comm = rbg.COMM_PEER if a.comm == "peer" else rbg.COMM_NCCL
-        if comm == rbg.COMM_NCCL:
-            nccl_id = D.nccl_unique_id()
-    stream = torch.cuda.Stream(dev)                 # the library enqueues on this stream
-    torch.cuda.set_stream(stream)
-    ctx = rbg.Context(S, w, 0.0, k_max, stream=stream.cuda_stream, comm=comm, rank=rank,
-                      world=world, col_offset=off, M_global=M_glob, nccl_id=nccl_id, ortho=a.ortho,
-                      residual=a.residual)
+    fallback = None
     if comm == rbg.COMM_PEER:
-        D.connect_peers(ctx)
-    ctx.set_timing(True)
-    if a.graph_batch:
-        ctx.set_graph_batch(a.graph_batch)
+        # the PEER exchange needs CUDA IPC between the ranks' processes: if any rank cannot map
+        # its peers or the warm-up timed out, every rank falls back to the NCCL exchange
+        ok, ctx = True, None
+        try:
+            ctx = make_ctx(comm)
+            ok = ctx.info()[2] != "PEER_TIMEOUT"
+        except rbg.RbgError as e:
+            ok, fallback = False, str(e)
+        t = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if not bool(t.item()):
+            if ctx is not None:
+                ctx.close()
+            fallback = fallback or "PEER warm-up failed on some rank"
+            comm = rbg.COMM_NCCL
+            ctx = make_ctx(comm)
+    else:
+        ctx = make_ctx(comm)
 
-    # ---- warm-up (sweep 0 + W iterations), then exactly K timed iterations
-    ctx.step(W)
+    # ---- exactly K timed iterations
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -315,6 +338,8 @@ def run_ours(a):
                             "rel_gap": float((ms - (np.sum(sw) + np.sum(xc) + np.sum(im))) / ms)},
         "final_err": float(errs[-1]) if len(errs) else None,
         "roofline": roof, "clocks": clocks,
+        "exchange_used": {rbg.COMM_NONE: "none", rbg.COMM_PEER: "peer", rbg.COMM_NCCL: "nccl"}[comm],
+        **({"exchange_fallback": fallback} if fallback else {}),
         # ours per iteration: sweep + IMGS (+ the PEER wait kernel); NCCL's own kernel not counted
         "gpu_launches": (3 if comm == rbg.COMM_PEER else 2) * K,
     }
@@ -336,7 +361,7 @@ def run_ours(a):
             host.copy_(S)
             del S
             torch.cuda.empty_cache()
-            line["e2e"] = e2e(a, host, w, k_max, W + K, stream, rank, world, M_loc, M_glob, dev)
+            line["e2e"] = e2e(a, host, w, k_max, W + K, stream, rank, world, M_loc, M_glob, dev, comm)
             del host
         else:
             line["e2e"] = {"value": None, "unit": "it/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
@@ -377,7 +402,7 @@ def host_mem_available() -> float:
     return 0.0
 
 
-def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev):
+def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev, comm):
     """Same metric through the public API with HOST buffers: H2D of S (pinned host copy)
     inside the timed region (create), all iterations, and the D2H read of pivots, errors
     and basis."""
@@ -389,10 +414,8 @@ def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev):
     Sh = host.numpy()
     nccl_id = None
     from paper_1805_06124_b200 import dist as D
-    comm = rbg.COMM_NONE
     if world > 1:
         dist.barrier()
-        comm = rbg.COMM_PEER if a.comm == "peer" else rbg.COMM_NCCL
         if comm == rbg.COMM_NCCL:
             nccl_id = D.nccl_unique_id()
     torch.cuda.synchronize()

@@ -61,8 +61,18 @@ def all_gather_bytes(payload: bytes, group=None) -> list[bytes]:
 
 
 def connect_peers(ctx, group=None):
-    """PEER exchange setup: all-gather every rank's IPC handles and map them."""
-    ctx.peer_connect(all_gather_bytes(ctx.peer_export(), group))
+    """PEER exchange setup: all-gather every rank's IPC handles and map them.  Every rank
+    takes part in the all-gather even if its export failed (then every rank raises), so a
+    failure never leaves the ranks in different collectives."""
+    from . import rbg
+    try:
+        mine = ctx.peer_export()
+    except rbg.RbgError:
+        mine = None
+    handles = all_gather_bytes(mine, group)
+    if any(h is None for h in handles):
+        raise rbg.RbgError(rbg.ESTATE, "a rank could not export its PEER handles")
+    ctx.peer_connect(handles)
     return ctx
 
 

@@ -95,3 +95,28 @@ def test_connect_peers_over_gloo():
     res = run_world(_connect)
     for got in res:
         assert got == [bytes([p]) * 128 for p in range(WORLD)]
+
+
+class _FailingCtx(_FakeCtx):
+    def peer_export(self):
+        from paper_1805_06124_b200 import rbg
+        if self.rank == 1:
+            raise rbg.RbgError(rbg.ECUDA, "no IPC here")
+        return super().peer_export()
+
+
+def _connect_failing(rank):
+    from paper_1805_06124_b200 import dist as D
+    from paper_1805_06124_b200 import rbg
+    try:
+        D.connect_peers(_FailingCtx(rank))
+    except rbg.RbgError as e:
+        return e.status
+    return None
+
+
+def test_connect_peers_failure_reaches_every_rank():
+    """A rank that cannot export its handles still takes part in the all-gather, and every
+    rank raises (bench.py then falls back to the NCCL exchange on all ranks)."""
+    from paper_1805_06124_b200 import rbg
+    assert run_world(_connect_failing) == [rbg.ESTATE, rbg.ESTATE]
