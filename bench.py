@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--rows", type=int, default=N_ROWS)
     p.add_argument("--cols-per-gpu", type=int, default=M_PER_GPU)
+    p.add_argument("--strong-cols", type=int, default=0,
+                   help="strong scaling: this many columns in total, split over the GPUs "
+                        "(BASELINE config 3: 1,638,400 at 2/4/8 GPUs); default weak scaling")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--graph-batch", type=int, default=0)
@@ -169,12 +172,12 @@ def run_reference(a):
     W, K = a.warmup, a.steps
     r, wall = cpu_sample(CPU_SAMPLE_COLS, W + K)
     t = full_iter_seconds(r, W, W + K, CPU_SAMPLE_COLS, m_full)
-    val = 1.0 / t * world
+    val = 1.0 / t * (m_full / M_PER_GPU)     # the same whole-job unit as our arm
     cores = oracle_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "it/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if a.strong_cols else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(a, world),
         "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "oracle",
                          "sample": f"CPU oracle (canonical lanes) on {CPU_SAMPLE_COLS} of "
@@ -187,9 +190,13 @@ def run_reference(a):
 
 
 def config_dict(a, world):
-    return {"workload": ("config2: complex fp64 chirp snapshots 10,000 x 409,600 (65.5 GB), k_max 300"
-                         if world == 1 else
-                         f"config3 weak: 10,000 x 409,600 per GPU x {world} GPUs, k_max 300"),
+    if getattr(a, "strong_cols", 0):
+        wl = f"config3 strong: 10,000 x {a.strong_cols} over {world} GPUs ({a.cols_per_gpu} per GPU), k_max 300"
+    elif world == 1:
+        wl = "config2: complex fp64 chirp snapshots 10,000 x 409,600 (65.5 GB), k_max 300"
+    else:
+        wl = f"config3 weak: 10,000 x 409,600 per GPU x {world} GPUs, k_max 300"
+    return {"workload": wl,
             "rows": a.rows, "cols_per_gpu": a.cols_per_gpu, "cols_global": a.cols_per_gpu * world,
             "k_window": [a.warmup, a.warmup + a.steps], "parallelism": f"column-sharded x{world}",
             "l2": "inputs (65.5 GB/GPU) >> 126 MB L2; no flush",
@@ -327,7 +334,8 @@ def run_ours(a):
 
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": "strong" if a.strong_cols else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (device-generated chirps, BASELINE.json config 2/3 recipe)",
         "config": config_dict(a, world), "iters_per_s": it_s,
         "hbm_gbs_per_gpu": achieved, "hbm_gbs_total": achieved * world,
@@ -443,6 +451,11 @@ def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev, comm)
 
 def main():
     a = parse()
+    if a.strong_cols:
+        world = a.gpus
+        if a.strong_cols % world:
+            raise SystemExit("--strong-cols must be divisible by --gpus")
+        a.cols_per_gpu = a.strong_cols // world
     if a.impl == "reference":
         return run_reference(a)
     return run_ours(a)
