@@ -204,8 +204,19 @@ rbg_status rbg_validate(rbg_ctx *ctx, const void *V, int64_t M_v, int64_t ldv, r
  * single-GPU context.  Their R rows and residuals are computed with the greedy's own
  * arithmetic, the pivot search restarts over all columns and a stopped greedy may continue
  * (rbg_run / rbg_step).  The snapshot matrix becomes library-owned (a borrowed S is copied).
- * ESTATE on sharded contexts.  Blocking.                                                   */
+ * ESTATE on sharded contexts (see rbg_add_columns_ex).  Blocking.                          */
 rbg_status rbg_add_columns(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem);
+/* Enrichment of a column-sharded context (also valid on one GPU): every rank calls it, in the
+ * same round, with its own failing columns (M_f >= 0; F may be NULL when M_f = 0).  They get
+ * the global indices first_gid .. first_gid + M_f - 1, which must lie in [M_global,
+ * M_global_new); M_global_new is the new total over all ranks (the same on every rank).  With
+ * the ranks' appended blocks numbered in rank order (first_gid = old M_global + the counts of
+ * the ranks before), the result equals one context enriched with the concatenated columns bit
+ * for bit.  The pivot search restarts on every rank (its candidate published to the exchange
+ * with a new record epoch) and a stopped greedy may continue.  first_gid < 0 and
+ * M_global_new <= 0 select the single-GPU defaults (M_global, M_global + M_f).  Blocking.   */
+rbg_status rbg_add_columns_ex(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem, int64_t first_gid,
+                              int64_t M_global_new);
 
 /* Gram matrix G = R R^H of the k x M coefficient block (k = basis size): k x k Hermitian,
  * column-major with leading dimension ldg >= k, complex (16-byte) entries even for a real

@@ -109,6 +109,10 @@ struct rbg_ctx {
     bool peer_ipc[kMaxPeers] = {};
     bool peer_connected = false;
     long long peer_timeout_ns = 0;
+    // sharded enrichment: global index of each local column (sorted) once columns were
+    // appended, and the record-tag epoch (bumped by every sharded append)
+    long long *gid = nullptr;
+    unsigned long long epoch = 0;
 };
 
 namespace {
@@ -126,6 +130,7 @@ void free_ctx(rbg_ctx *c) {
             cudaIpcCloseMemHandle(c->peer_send[q]);
         }
     dfree(c->peer_in);
+    dfree(c->gid);
     if (c->own_S) dfree(c->S);
     dfree(c->w);
     dfree(c->Q);
@@ -176,6 +181,8 @@ SweepArgs sweep_args(const rbg_ctx *c) {
         a.peer_world = c->world;
         for (int q = 0; q < c->world; q++) a.peer_in[q] = c->peer_rec[q];
     }
+    a.peer_epoch = c->epoch;
+    a.gid = c->gid;
     return a;
 }
 
@@ -206,6 +213,7 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.peer_mine = c->comm == RBG_COMM_PEER ? c->peer_in : nullptr;
     a.peer_slot = c->slot;
     for (int q = 0; q < kMaxPeers; q++) a.peer_send[q] = q < c->world ? c->peer_send[q] : nullptr;
+    a.gid = c->gid;
     return a;
 }
 
@@ -222,7 +230,7 @@ rbg_status enqueue_local(rbg_ctx *c) {
 
 rbg_status enqueue_xchg(rbg_ctx *c) {
     if (c->comm == RBG_COMM_PEER) {
-        CU(launch_peer_wait(c->peer_in, c->world, c->st, c->peer_timeout_ns, c->stream));
+        CU(launch_peer_wait(c->peer_in, c->world, c->st, c->epoch, c->peer_timeout_ns, c->stream));
         return RBG_OK;
     }
     if (c->comm == RBG_COMM_NCCL) {
@@ -366,6 +374,8 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     a.ticket = ticket;
     a.col_offset = 0;
     a.send = nullptr;
+    a.peer_world = 0;   // a block outside the training set: no exchange, its own indices
+    a.gid = nullptr;
     a.qi = -1;
     if (e == cudaSuccess) e = launch_sweep(a, c->cplx, true, c->cfg_init, c->stream);
     for (long long i = 0; i < k && e == cudaSuccess; i++) {
@@ -982,57 +992,93 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
     return st;
 }
 
-rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem) {
+rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem, int64_t first_gid,
+                              int64_t M_global_new) {
     TRY(check_ctx(c));
     if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
-    if (c->world != 1 || c->comm != RBG_COMM_NONE) return fail(RBG_ESTATE, "add_columns needs a single-GPU context");
+    if (c->local_pending) return fail(RBG_ESTATE, "add_columns inside an EXTERNAL/PEER iteration");
+    const bool sharded = c->comm != RBG_COMM_NONE;
+    if (first_gid < 0) first_gid = c->M_global;
+    if (M_global_new <= 0) M_global_new = c->M_global + M_f;
+    if (M_f < 0 || (!sharded && M_f < 1)) return fail(RBG_EINVAL, "M_f < 1");
+    if (first_gid < c->M_global || first_gid + M_f > M_global_new)
+        return fail(RBG_EINVAL, "appended ids [%lld, %lld) must lie in [M_global=%lld, M_global_new=%lld)",
+                    (long long)first_gid, (long long)(first_gid + M_f), c->M_global, (long long)M_global_new);
+    if (!sharded && (first_gid != c->M_global || M_global_new != c->M_global + M_f))
+        return fail(RBG_EINVAL, "a single-GPU context appends at the end (ids M_global..M_global+M_f)");
     DevState h;
     TRY(read_state(c, &h));
-    double2 *Fd = nullptr;
-    TRY(upload_block(c, F, M_f, ldf, F_mem, &Fd));
     const long long M0 = c->M, M1 = c->M + M_f;
+    double2 *Fd = nullptr;
+    if (M_f > 0) TRY(upload_block(c, F, M_f, ldf, F_mem, &Fd));
     const size_t pitch = (size_t)c->nvec * 16;
-    double2 *S1 = nullptr;
-    double *R1 = nullptr, *r21 = nullptr;
-    cudaError_t e = dmalloc(&S1, pitch * M1);
-    if (e == cudaSuccess) e = dmalloc(&R1, (size_t)c->k_max * M1 * c->se);
-    if (e == cudaSuccess) e = dmalloc(&r21, sizeof(double) * M1);
-    if (e == cudaSuccess) e = cudaMemcpy2DAsync(S1, pitch, c->S, (size_t)c->ldv * 16, pitch, M0, cudaMemcpyDeviceToDevice, c->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(S1 + M0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(R1, 0, (size_t)c->k_max * M1 * c->se, c->stream);
-    if (e == cudaSuccess && h.k)
-        e = cudaMemcpy2DAsync(R1, (size_t)M1 * c->se, c->R, (size_t)M0 * c->se, (size_t)M0 * c->se, h.k,
-                              cudaMemcpyDeviceToDevice, c->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(r21, c->r2, sizeof(double) * M0, cudaMemcpyDeviceToDevice, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    double2 *S1 = c->S;
+    double *R1 = c->R, *r21 = c->r2;
+    long long *gid1 = c->gid;
+    cudaError_t e = cudaSuccess;
+    if (M_f > 0) {
+        S1 = nullptr;
+        R1 = nullptr;
+        r21 = nullptr;
+        e = dmalloc(&S1, pitch * M1);
+        if (e == cudaSuccess) e = dmalloc(&R1, (size_t)c->k_max * M1 * c->se);
+        if (e == cudaSuccess) e = dmalloc(&r21, sizeof(double) * M1);
+        if (e == cudaSuccess) e = cudaMemcpy2DAsync(S1, pitch, c->S, (size_t)c->ldv * 16, pitch, M0, cudaMemcpyDeviceToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(S1 + M0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(R1, 0, (size_t)c->k_max * M1 * c->se, c->stream);
+        if (e == cudaSuccess && h.k)
+            e = cudaMemcpy2DAsync(R1, (size_t)M1 * c->se, c->R, (size_t)M0 * c->se, (size_t)M0 * c->se, h.k,
+                                  cudaMemcpyDeviceToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(r21, c->r2, sizeof(double) * M0, cudaMemcpyDeviceToDevice, c->stream);
+        if (e == cudaSuccess && sharded) {
+            // global indices: the rank's original block, earlier appends, then these columns
+            std::vector<long long> g((size_t)M1);
+            if (c->gid) e = cudaMemcpy(g.data(), c->gid, sizeof(long long) * M0, cudaMemcpyDeviceToHost);
+            else
+                for (long long j = 0; j < M0; j++) g[(size_t)j] = c->col_offset + j;
+            for (long long j = 0; j < M_f; j++) g[(size_t)(M0 + j)] = first_gid + j;
+            gid1 = nullptr;
+            if (e == cudaSuccess) e = dmalloc(&gid1, sizeof(long long) * M1);
+            if (e == cudaSuccess) e = cudaMemcpy(gid1, g.data(), sizeof(long long) * M1, cudaMemcpyHostToDevice);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    }
     dfree(Fd);
+    auto drop_new = [&]() {
+        if (M_f > 0) {
+            dfree(S1);
+            dfree(R1);
+            dfree(r21);
+            if (gid1 != c->gid) dfree(gid1);
+        }
+    };
     if (e != cudaSuccess) {
-        dfree(S1);
-        dfree(R1);
-        dfree(r21);
+        drop_new();
         return fail(e == cudaErrorMemoryAllocation ? RBG_ENOMEM : RBG_ECUDA, "add_columns: %s", cudaGetErrorString(e));
     }
-    if (c->started) {
+    if (c->started && M_f > 0) {
         // the new columns get R rows 0..k-1 and the recurrence residual, then the pivot
         // search restarts over all columns and the next iteration begins at the decision
         rbg_status st = coeff_passes(c, S1 + M0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), M1, r21 + M0, h.k);
         if (st != RBG_OK) {
-            dfree(S1);
-            dfree(R1);
-            dfree(r21);
+            drop_new();
             return st;
         }
     }
-    if (c->own_S) dfree(c->S);
-    dfree(c->R);
-    dfree(c->r2);
-    c->S = S1;
-    c->own_S = true;
-    c->ldv = c->nvec;
-    c->R = R1;
-    c->r2 = r21;
-    c->M = M1;
-    c->M_global = M1;
+    if (M_f > 0) {
+        if (c->own_S) dfree(c->S);
+        dfree(c->R);
+        dfree(c->r2);
+        if (gid1 != c->gid) dfree(c->gid);
+        c->S = S1;
+        c->own_S = true;
+        c->ldv = c->nvec;
+        c->R = R1;
+        c->r2 = r21;
+        c->gid = gid1;
+        c->M = M1;
+    }
+    c->M_global = M_global_new;
     for (auto &p : c->ev)
         for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
     c->ev.clear();
@@ -1042,13 +1088,27 @@ rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, 
         c->graph = nullptr;
     }
     if (c->started) {
-        CU(launch_maxloc(c->r2, M1, 0, c->st, c->stream));
         CU(cudaMemsetAsync(&c->st->stop, 0, sizeof(int), c->stream));
+        if (sharded) {
+            // new record tags (the stopped decision's records have the old epoch), the local
+            // candidate packed and, on PEER, published; the next iteration exchanges and decides
+            c->epoch++;
+            CU(launch_restart(sweep_args(c), c->cplx, c->stream));
+        } else {
+            CU(launch_maxloc(c->r2, M1, 0, c->st, c->stream));
+        }
         c->resume_pending = true;
         c->iters = h.k;
     }
     CU(cudaStreamSynchronize(c->stream));
     return RBG_OK;
+}
+
+rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem) {
+    TRY(check_ctx(c));
+    if (c->world != 1 || c->comm != RBG_COMM_NONE)
+        return fail(RBG_ESTATE, "sharded contexts use rbg_add_columns_ex (global ids of the appended columns)");
+    return rbg_add_columns_ex(c, F, M_f, ldf, F_mem, -1, 0);
 }
 
 namespace {

@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
         a.piv[k] = J;
         a.nu[k] = nu;
         a.rdiag[k] = nn;
-        const long long jl = J - a.col_offset;
-        if (jl >= 0 && jl < a.M_loc) a.r2[jl] = -INFINITY;
+        const long long jl = local_col(a, J);
+        if (jl >= 0) a.r2[jl] = -INFINITY;
         a.st->k = k + 1;
     }
 }

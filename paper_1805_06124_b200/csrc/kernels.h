@@ -35,7 +35,21 @@ struct SweepArgs {
     PeerRec *peer_in[kMaxPeers];
     int peer_world, peer_rank;
     size_t peer_slot;
+    unsigned long long peer_epoch;  // bumped by every sharded rbg_add_columns_ex (record tags)
+    const long long *gid;   // global index of each local column once columns were appended to a
+                            // sharded context (sorted ascending), else NULL: col_offset + local
 };
+
+// Global index of local column j (sweep records).
+__device__ __forceinline__ long long global_col(const SweepArgs &a, long long j) {
+    if (j == 0x7fffffffffffffffLL) return j;
+    return a.gid ? a.gid[j] : j + a.col_offset;
+}
+
+// PEER record tag of the sweep / decision with basis size k.
+__host__ __device__ inline unsigned long long peer_tag(unsigned long long epoch, long long k) {
+    return (epoch << 32) | (unsigned long long)(k + 1);
+}
 
 // Pivot decision + iterated MGS (a3 finalize, a5, a6).
 struct ImgsArgs {
@@ -63,7 +77,23 @@ struct ImgsArgs {
     const PeerRec *peer_mine;
     const unsigned char *peer_send[kMaxPeers];
     size_t peer_slot;
+    const long long *gid;  // as SweepArgs::gid (the owner masks its selected local column)
 };
+
+// Local index of global column J on this rank, -1 if another rank owns it.
+__device__ __forceinline__ long long local_col(const ImgsArgs &a, long long J) {
+    if (!a.gid) {
+        const long long jl = J - a.col_offset;
+        return (jl >= 0 && jl < a.M_loc) ? jl : -1;
+    }
+    long long lo = 0, hi = a.M_loc;  // gid is sorted ascending: binary search
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (a.gid[mid] < J) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < a.M_loc && a.gid[lo] == J) ? lo : -1;
+}
 
 // Pivot decision (a3) from this rank's maxloc, the all-gathered slots (NCCL / EXTERNAL) or the
 // PEER records; `src` = the pivot column (local S, a received slot, or the owner's send slot
@@ -108,7 +138,12 @@ __device__ __forceinline__ void pivot_decision(const ImgsArgs &a, long long k, d
 
 // PEER exchange wait (a4): until every rank's record of this iteration has arrived (tag), or
 // timeout_ns passed (then stop = PEER_TIMEOUT).  One warp; no-op once stopped.
-cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, long long timeout_ns, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, unsigned long long epoch, long long timeout_ns,
+                             cudaStream_t s);
+// Pivot search restart after columns were added to a sharded context: the local maxloc of r2
+// (one CTA, the sweep's total order and global indices) into the state, the candidate column
+// packed into the send slot and, on a PEER context, the record published to every rank.
+cudaError_t launch_restart(const SweepArgs &a, bool cplx, cudaStream_t s);
 
 struct SweepConfig {
     int grid, threads;

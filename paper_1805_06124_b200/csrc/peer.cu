@@ -12,13 +12,14 @@
 
 namespace rbg {
 
-__global__ void k_peer_wait(const PeerRec *mine, int world, DevState *st, long long timeout_ns) {
+__global__ void k_peer_wait(const PeerRec *mine, int world, DevState *st, unsigned long long epoch,
+                            long long timeout_ns) {
     if (st->stop) return;
-    const unsigned long long tag = (unsigned long long)st->k + 1;
+    const unsigned long long tag = peer_tag(epoch, st->k);
     const int p = threadIdx.x;
     bool late = false;
     if (p < world) {
-        const PeerRec *r = mine + (tag & 1) * world + p;
+        const PeerRec *r = mine + ((st->k + 1) & 1) * world + p;
         const unsigned long long t0 = globaltimer_ns();
         while (ld_acquire_sys(&r->tag) != tag) {
             if ((long long)(globaltimer_ns() - t0) > timeout_ns) {
@@ -31,8 +32,9 @@ __global__ void k_peer_wait(const PeerRec *mine, int world, DevState *st, long l
     if (__any_sync(0xffffffffu, late) && p == 0) st->stop = kStopPeer;
 }
 
-cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, long long timeout_ns, cudaStream_t s) {
-    k_peer_wait<<<1, 32, 0, s>>>(mine, world, st, timeout_ns);
+cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, unsigned long long epoch, long long timeout_ns,
+                             cudaStream_t s) {
+    k_peer_wait<<<1, 32, 0, s>>>(mine, world, st, epoch, timeout_ns);
     return cudaGetLastError();
 }
 

@@ -133,7 +133,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
             }
         }
         if (lane == 0) {
-            const long long jg = (bj == 0x7fffffffffffffffLL) ? bj : bj + a.col_offset;
+            const long long jg = global_col(a, bj);
             a.st->m_loc = bm;
             a.st->j_loc = jg;
             *a.ticket = 0u;
@@ -162,8 +162,8 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
             // every GPU, then publish the record in every rank's array and release the tag
             __syncthreads();
             if (tid == 0) {
-                const unsigned long long tag = (unsigned long long)a.st->k + 1;
-                const int par = (int)(tag & 1);
+                const unsigned long long tag = peer_tag(a.peer_epoch, a.st->k);
+                const int par = (int)((a.st->k + 1) & 1);
                 __threadfence_system();
                 for (int q = 0; q < a.peer_world; q++) {
                     PeerRec *r = a.peer_in[q] + par * a.peer_world + a.peer_rank;
@@ -443,6 +443,37 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_ring(const SweepArgs
         }
     }
     sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
+}
+
+// Pivot search restart (sharded rbg_add_columns_ex): one CTA; thread t scans r2[t], r2[t + T],
+// ... (increasing index: first max wins), warp maxloc, then sweep_finish (grid of one CTA: it
+// is the last CTA) writes the state, packs the candidate and publishes the PEER record.
+template <bool CPLX>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_restart(const SweepArgs a) {
+    double bm = -INFINITY;
+    long long bj = 0x7fffffffffffffffLL;
+    for (long long j = threadIdx.x; j < a.M; j += blockDim.x) {
+        const double m = a.r2[j];
+        if (m > bm) {
+            bm = m;
+            bj = j;
+        }
+    }
+    for (int h = 16; h >= 1; h >>= 1) {  // exact: total order
+        const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+        const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+        if (rec_better(om, oj, bm, bj)) {
+            bm = om;
+            bj = oj;
+        }
+    }
+    sweep_finish<CPLX>(a, bm, bj, !CPLX && (a.N & 1));
+}
+
+cudaError_t launch_restart(const SweepArgs &a, bool cplx, cudaStream_t s) {
+    if (cplx) k_restart<true><<<1, kSweepThreads, 0, s>>>(a);
+    else k_restart<false><<<1, kSweepThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int device) {

@@ -132,3 +132,45 @@ def sharded_reconstruct(ctx, tau2: float = 0.0, kr_max: int = 0, group=None):
     (R33).  Returns (sigma, kr, X)."""
     G = fold_over_ranks(ctx.gram_fold, ctx.info()[0], group)
     return ctx.reconstruct_gram(G, tau2, kr_max)
+
+
+def enrich_plan(counts: list[int], rank: int, M_global: int) -> tuple[int, int]:
+    """(first_gid, M_global_new) of `rank` for one sharded enrichment round: the ranks'
+    appended blocks are numbered in rank order after the current M_global columns, so the
+    global column order is that of one context enriched with the concatenated blocks."""
+    return M_global + sum(counts[:rank]), M_global + sum(counts)
+
+
+def sharded_enrich(ctx, V_local, tol: float, rounds: int = 3, group=None, M_global: int | None = None):
+    """Iterative refinement (reading R32) on a column-sharded context: each
+    rank validates its own block of the validation set, appends its failing columns (not
+    appended before) with global ids from enrich_plan, and the greedy continues on every rank.
+    V_local is this rank's block of a validation set partitioned in rank order; M_global is the
+    current total (default: the M_global the context was created with, tracked here).
+    Returns (per-round max validation error over all ranks, passed)."""
+    import numpy as np
+    import torch.distributed as dist
+    Vh = V_local.cpu().numpy() if hasattr(V_local, "cpu") else np.asarray(V_local)
+    added = np.zeros(Vh.shape[0], bool)
+    history = []
+    total = M_global if M_global is not None else ctx.M_global
+
+    def max_err(err):
+        return max(all_gather_bytes(float(err.max()) if err.size else 0.0, group))
+
+    for _ in range(rounds):
+        err = ctx.validate(Vh)
+        history.append(max_err(err))
+        fail = (err >= tol) & ~added
+        counts = all_gather_bytes(int(fail.sum()), group)
+        if sum(counts) == 0:
+            passed = all(all_gather_bytes(bool(np.all(err < tol)), group))
+            return history, passed
+        first, total_new = enrich_plan(counts, dist.get_rank(group), total)
+        ctx.add_columns(Vh[fail], first_gid=first, M_global=total_new)
+        total = total_new
+        added |= fail
+        ctx.run()
+    err = ctx.validate(Vh)
+    history.append(max_err(err))
+    return history, all(all_gather_bytes(bool(np.all(err < tol)), group))

@@ -95,6 +95,7 @@ SYMBOLS = {
     "rbg_destroy": ([_P], None),
     "rbg_validate": ([_P, _P, _I64, _I64, ctypes.c_int, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_add_columns": ([_P, _P, _I64, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_add_columns_ex": ([_P, _P, _I64, _I64, ctypes.c_int, _I64, _I64], ctypes.c_int),
     "rbg_gram": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_reconstruct": ([_P, ctypes.c_double, _I64, ctypes.POINTER(_I64), _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_eim": ([_P, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
@@ -245,6 +246,7 @@ class Context:
         if nccl_id is not None:
             ctypes.memmove(d.nccl_id, nccl_id, 128)
         self.N, self.M = int(d.N), int(d.M)
+        self.M_global = int(d.M_global) if d.M_global else int(d.M)
         self.cplx = d.dtype == COMPLEX_F64
         self.k_max = int(k_max)
         h = ctypes.c_void_p()
@@ -375,11 +377,21 @@ class Context:
         del keep
         return (err, C[:k]) if coeffs else err
 
-    def add_columns(self, F):
-        """Append the columns of F (M_f, N) to the training set (rbg_add_columns)."""
-        ptr, mf, ld, mem, keep = self._block(F)
-        _check(lib().rbg_add_columns(self.h, ptr, mf, ld, mem))
+    def add_columns(self, F, first_gid: int | None = None, M_global: int | None = None):
+        """Append the columns of F (M_f, N) to the training set: rbg_add_columns on one GPU,
+        rbg_add_columns_ex with their global ids (first_gid..) and the new total M_global on
+        a sharded context (F may have 0 rows there)."""
+        if F is None or (hasattr(F, "shape") and F.shape[0] == 0):
+            ptr, mf, ld, mem, keep = None, 0, self.N, MEM_HOST, None
+        else:
+            ptr, mf, ld, mem, keep = self._block(F)
+        if first_gid is None and M_global is None:
+            _check(lib().rbg_add_columns(self.h, ptr, mf, ld, mem))
+        else:
+            _check(lib().rbg_add_columns_ex(self.h, ptr, mf, ld, mem, -1 if first_gid is None else int(first_gid),
+                                            0 if M_global is None else int(M_global)))
         self.M += mf
+        self.M_global = int(M_global) if M_global is not None else self.M_global + mf
         del keep
 
     def gram(self) -> np.ndarray:

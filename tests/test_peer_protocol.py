@@ -120,3 +120,13 @@ def test_connect_peers_failure_reaches_every_rank():
     rank raises (bench.py then falls back to the NCCL exchange on all ranks)."""
     from paper_1805_06124_b200 import rbg
     assert run_world(_connect_failing) == [rbg.ESTATE, rbg.ESTATE]
+
+
+def test_enrich_plan_numbers_appended_blocks_in_rank_order():
+    from paper_1805_06124_b200 import dist as D
+    counts = [3, 0, 5, 1]
+    plans = [D.enrich_plan(counts, r, 1000) for r in range(4)]
+    assert plans == [(1000, 1009), (1003, 1009), (1003, 1009), (1008, 1009)]
+    # concatenating the blocks in rank order gives ids 1000..1008 without gaps
+    ids = [i for r in range(4) for i in range(plans[r][0], plans[r][0] + counts[r])]
+    assert ids == list(range(1000, 1009))

@@ -112,3 +112,80 @@ def test_gpu_enrichment_bit_exact(orc, cplx):
     np.testing.assert_array_equal(g.errors, res.errors)
     np.testing.assert_array_equal(g.Q, res.Q)
     np.testing.assert_array_equal(g.R, res.R)
+
+
+def _drive(rbg, ctxs, mode, n):
+    for _ in range(n):
+        for c in ctxs:
+            c.iter_local()
+        if mode == "external":
+            rbg.emulate_allgather(ctxs)
+        for c in ctxs:
+            c.iter_finish()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,cplx", [("peer", True), ("external", True), ("peer", False)])
+def test_gpu_sharded_enrichment_bit_exact(orc, mode, cplx):
+    """Enrichment of a 2-rank column-sharded greedy (rbg_add_columns_ex, R34): each
+    rank validates its own block of V and appends its failing columns with global ids numbered
+    in rank order (dist.enrich_plan); the pivot search restarts on every rank with a new record
+    epoch.  Pivots, errors, Q, the history and R / r2 (gathered by global column id) equal the
+    single-process oracle enrichment of the concatenated V bit for bit."""
+    import torch
+
+    from paper_1805_06124_b200 import dist as D
+    from paper_1805_06124_b200 import rbg
+    S, V, w = _sets(M_train=60)
+    if not cplx:
+        S, V = S.real.copy(), V.real.copy()
+    tol, k_max, rounds = 1e-5, 150, 4
+    res, S2, hist_o, ok_o = orc.enrich(S, V, w, tol, k_max, rounds=rounds)
+    M, Mv = S.shape[0], V.shape[0]
+    sb, vb = [0, 23, M], [0, Mv // 3, Mv]            # ranks' training / validation blocks
+    comm = rbg.COMM_PEER if mode == "peer" else rbg.COMM_EXTERNAL
+    stream = torch.cuda.Stream()
+    ctxs = [rbg.Context(S[sb[p]:sb[p + 1]], w, tol, k_max, stream=stream.cuda_stream, comm=comm, rank=p, world=2,
+                        col_offset=sb[p], M_global=M) for p in range(2)]
+    if mode == "peer":
+        rbg.peer_connect_local(ctxs)
+    gids = [list(range(sb[p], sb[p + 1])) for p in range(2)]
+    _drive(rbg, ctxs, mode, k_max + 1)
+    Vb = [V[vb[p]:vb[p + 1]] for p in range(2)]
+    added = [np.zeros(vb[p + 1] - vb[p], bool) for p in range(2)]
+    total, hist, ok = M, [], None
+    for _ in range(rounds):
+        errs = [ctxs[p].validate(Vb[p]) for p in range(2)]
+        hist.append(max(float(e.max()) for e in errs))
+        fails = [(errs[p] >= tol) & ~added[p] for p in range(2)]
+        counts = [int(f.sum()) for f in fails]
+        if sum(counts) == 0:
+            ok = all(bool(np.all(e < tol)) for e in errs)
+            break
+        for p in range(2):
+            first, total_new = D.enrich_plan(counts, p, total)
+            ctxs[p].add_columns(Vb[p][fails[p]], first_gid=first, M_global=total_new)
+            gids[p] += list(range(first, first + counts[p]))
+            added[p] |= fails[p]
+        total = total_new
+        _drive(rbg, ctxs, mode, k_max + 1)
+    if ok is None:
+        errs = [ctxs[p].validate(Vb[p]) for p in range(2)]
+        hist.append(max(float(e.max()) for e in errs))
+        ok = all(bool(np.all(e < tol)) for e in errs)
+    assert ok == ok_o and hist == hist_o
+    out = [c.result() for c in ctxs]
+    for g in out:
+        assert (g.k, g.stop) == (res.k, res.stop)
+        np.testing.assert_array_equal(g.pivots, res.pivots)
+        np.testing.assert_array_equal(g.errors, res.errors)
+        np.testing.assert_array_equal(g.Q, res.Q)
+    R = np.zeros_like(res.R)
+    r2 = np.zeros_like(res.r2)
+    for p in range(2):
+        R[:, gids[p]] = out[p].R
+        r2[gids[p]] = out[p].r2
+    np.testing.assert_array_equal(R, res.R)
+    np.testing.assert_array_equal(r2, res.r2)
+    for c in ctxs:
+        c.close()
