@@ -1234,9 +1234,25 @@ rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_d
         for (int i = 0; i < kp; i++) I[(size_t)i * kp + i] = make_double2(1.0, 0.0);
         e = cudaMemcpyAsync(V, I.data(), sizeof(double2) * I.size(), cudaMemcpyHostToDevice, c->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned long long), c->stream);
-        if (e == cudaSuccess)
-            e = block ? launch_bjacobi(G, V, kp, reinterpret_cast<double2 *>(rots), flags, sweeps, c->num_sms, c->stream)
-                      : launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
+        if (e == cudaSuccess) {
+            unsigned long long *trace = nullptr;  // RBG_DEBUG_JACOBI: phase timestamps of 8 rounds
+            if (block && getenv("RBG_DEBUG_JACOBI") && dmalloc(&trace, 32 * sizeof(unsigned long long)) != cudaSuccess)
+                trace = nullptr;
+            if (e == cudaSuccess)
+                e = block ? launch_bjacobi(G, V, kp, reinterpret_cast<double2 *>(rots), flags, sweeps, c->num_sms,
+                                           c->stream, trace)
+                          : launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
+            if (trace) {
+                unsigned long long tt[32];
+                cudaMemcpyAsync(tt, trace, sizeof tt, cudaMemcpyDeviceToHost, c->stream);
+                cudaStreamSynchronize(c->stream);
+                for (int r = 1; r < 8; r++)
+                    fprintf(stderr, "rbg: bjacobi round %d: P1+bar %.1f us, P2+bar %.1f us, P3+bar %.1f us\n", r,
+                            (tt[r * 4 + 1] - tt[r * 4]) * 1e-3, (tt[r * 4 + 2] - tt[r * 4 + 1]) * 1e-3,
+                            (tt[r * 4 + 3] - tt[r * 4 + 2]) * 1e-3);
+                dfree(trace);
+            }
+        }
         if (e == cudaSuccess)
             e = launch_eig_sort(G, k, kp, tau2, (int)std::min<int64_t>(kr_max ? kr_max : k, k), order, sig, krd,
                                 c->stream);

@@ -190,7 +190,7 @@ size_t jacobi_scratch_bytes(int kp);  // k_jacobi's per-pair 2 x 2 scratch
 int jacobi_pad(int k);
 size_t bjacobi_scratch_bytes(int kp);
 cudaError_t launch_bjacobi(double2 *G, double2 *V, int kp, double2 *Us, unsigned long long *flags, int *sweeps,
-                           int num_sms, cudaStream_t s);
+                           int num_sms, cudaStream_t s, unsigned long long *trace = nullptr);
 
 // Greedy EIM nodes (eim.cu): nodes_d[k], B_d = Q(P, :) k x k column-major complex.
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,

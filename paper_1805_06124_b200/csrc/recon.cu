@@ -300,8 +300,11 @@ constexpr int kJL = 2 * kJB;   // local problem size (one warp wide)
 
 __device__ __forceinline__ int blk_idx(int I, int J, int a) { return a < kJB ? I * kJB + a : J * kJB + (a - kJB); }
 
-__global__ void __launch_bounds__(256) k_bjacobi(double2 *G, double2 *V, int kp, double2 *Us,
-                                                 unsigned long long *flags, int *sweeps_out) {
+constexpr int kBjThreads = 1024;  // 32 warps per SM: P2/P3 are latency-bound row/column passes
+
+__global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, int kp, double2 *Us,
+                                                 unsigned long long *flags, int *sweeps_out,
+                                                 unsigned long long *trace) {
     __shared__ double2 A[kJL][kJL + 1];   // A[row][col]
     __shared__ double2 U[kJL][kJL + 1];
     __shared__ Rot srot[kJL / 2];
@@ -315,6 +318,8 @@ __global__ void __launch_bounds__(256) k_bjacobi(double2 *G, double2 *V, int kp,
     for (; sweep < 40; sweep++) {
         unsigned long long *flag = &flags[sweep & 1];
         for (int r = 0; r < nb - 1; r++) {
+            const bool tr = trace && sweep == 0 && r < 8 && blockIdx.x == 0 && tid == 0;
+            if (tr) trace[r * 4 + 0] = globaltimer_ns();
             // ---- P1: local problems
             for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
                 int I, J;
@@ -362,31 +367,40 @@ __global__ void __launch_bounds__(256) k_bjacobi(double2 *G, double2 *V, int kp,
                         srot[tid] = R;
                     }
                     __syncthreads();
-                    // columns p, q of A and U: X <- X J
-                    for (int e = tid; e < (kJL / 2) * kJL * 2; e += blockDim.x) {
-                        const int pi = e / (2 * kJL), rem = e % (2 * kJL), row = rem % kJL;
-                        double2(*M)[kJL + 1] = rem < kJL ? A : U;
-                        const Rot R = srot[pi];
-                        const double2 gp = M[row][R.p], gq = M[row][R.q];
-                        const double2 eq = make_double2(R.er * gq.x + R.ei * gq.y, R.er * gq.y - R.ei * gq.x);
-                        M[row][R.p] = make_double2(R.cs * gp.x - R.sn * eq.x, R.cs * gp.y - R.sn * eq.y);
-                        M[row][R.q] = make_double2(R.sn * gp.x + R.cs * eq.x, R.sn * gp.y + R.cs * eq.y);
-                    }
-                    __syncthreads();
-                    // rows p, q of A: A <- J^H A
-                    for (int e = tid; e < (kJL / 2) * kJL; e += blockDim.x) {
-                        const int pi = e / kJL, col = e % kJL;
-                        const Rot R = srot[pi];
-                        const double2 rp = A[R.p][col], rq = A[R.q][col];
-                        const double2 eq = make_double2(R.er * rq.x - R.ei * rq.y, R.er * rq.y + R.ei * rq.x);
-                        double2 np = make_double2(R.cs * rp.x - R.sn * eq.x, R.cs * rp.y - R.sn * eq.y);
-                        double2 nq = make_double2(R.sn * rp.x + R.cs * eq.x, R.sn * rp.y + R.cs * eq.y);
-                        if (col == R.q) np = make_double2(0.0, 0.0);
-                        if (col == R.p) nq = make_double2(0.0, 0.0);
-                        if (col == R.p) np.y = 0.0;
-                        if (col == R.q) nq.y = 0.0;
-                        A[R.p][col] = np;
-                        A[R.q][col] = nq;
+                    // A <- J^H A J and U <- U J, fused: the rotation pairs partition the indices,
+                    // so thread (i, j) owns the 2 x 2 blocks (rows of pair i, columns of pair j)
+                    // of A and U -- it reads all four entries before writing them and no other
+                    // thread touches them (same per-element operations as column-then-row
+                    // passes; one barrier per local round instead of two)
+                    for (int e = tid; e < (kJL / 2) * (kJL / 2); e += blockDim.x) {
+                        const Rot Ri = srot[e / (kJL / 2)], Rj = srot[e % (kJL / 2)];
+                        const int rows[2] = {Ri.p, Ri.q}, cols[2] = {Rj.p, Rj.q};
+                        double2 a[2][2];
+#pragma unroll
+                        for (int x = 0; x < 2; x++) {  // columns: [a_p, a_q] <- [a_p, a_q] J_j
+                            const double2 gp = A[rows[x]][Rj.p], gq = A[rows[x]][Rj.q];
+                            const double2 eq = make_double2(Rj.er * gq.x + Rj.ei * gq.y, Rj.er * gq.y - Rj.ei * gq.x);
+                            a[x][0] = make_double2(Rj.cs * gp.x - Rj.sn * eq.x, Rj.cs * gp.y - Rj.sn * eq.y);
+                            a[x][1] = make_double2(Rj.sn * gp.x + Rj.cs * eq.x, Rj.sn * gp.y + Rj.cs * eq.y);
+                            const double2 up = U[rows[x]][Rj.p], uq = U[rows[x]][Rj.q];
+                            const double2 fq = make_double2(Rj.er * uq.x + Rj.ei * uq.y, Rj.er * uq.y - Rj.ei * uq.x);
+                            U[rows[x]][Rj.p] = make_double2(Rj.cs * up.x - Rj.sn * fq.x, Rj.cs * up.y - Rj.sn * fq.y);
+                            U[rows[x]][Rj.q] = make_double2(Rj.sn * up.x + Rj.cs * fq.x, Rj.sn * up.y + Rj.cs * fq.y);
+                        }
+#pragma unroll
+                        for (int y = 0; y < 2; y++) {  // rows: [a_p; a_q] <- J_i^H [a_p; a_q]
+                            const int col = cols[y];
+                            const double2 rp = a[0][y], rq = a[1][y];
+                            const double2 eq = make_double2(Ri.er * rq.x - Ri.ei * rq.y, Ri.er * rq.y + Ri.ei * rq.x);
+                            double2 np = make_double2(Ri.cs * rp.x - Ri.sn * eq.x, Ri.cs * rp.y - Ri.sn * eq.y);
+                            double2 nq = make_double2(Ri.sn * rp.x + Ri.cs * eq.x, Ri.sn * rp.y + Ri.cs * eq.y);
+                            if (col == Ri.q) np = make_double2(0.0, 0.0);
+                            if (col == Ri.p) nq = make_double2(0.0, 0.0);
+                            if (col == Ri.p) np.y = 0.0;
+                            if (col == Ri.q) nq.y = 0.0;
+                            A[Ri.p][col] = np;
+                            A[Ri.q][col] = nq;
+                        }
                     }
                     __syncthreads();
                 }
@@ -395,50 +409,74 @@ __global__ void __launch_bounds__(256) k_bjacobi(double2 *G, double2 *V, int kp,
                 __syncthreads();
             }
             grid_barrier(bar, bar + 1, nblocks);
-            // ---- P2: columns: M[row, I u J] <- M[row, I u J] U, one warp per (pair, matrix, row)
-            for (long long it = gwarp; it < (long long)npairs * 2 * kp; it += nwarps) {
-                const int pr = (int)(it / (2LL * kp)), rem = (int)(it % (2LL * kp)), row = rem % kp;
-                double2 *M = rem < kp ? G : V;
-                int I, J;
-                round_pair(r, pr, nb, I, J);
-                const double2 *Up = Us + (size_t)pr * kJL * kJL;
-                const long long col = blk_idx(I, J, lane);
-                const double2 x = M[row + col * kp];
-                double2 acc = make_double2(0.0, 0.0);
+            if (tr) trace[r * 4 + 1] = globaltimer_ns();
+            // ---- P2: columns: M[row, I u J] <- M[row, I u J] U.  The grid is cut into npairs
+            // groups of CTAs, each group owns one block pair; a CTA stages that pair's U in
+            // shared memory (conflict-free U[m][lane] reads) and its warps take rows.
+            {
+                const int S = (int)gridDim.x / npairs > 0 ? (int)gridDim.x / npairs : 1;
+                const int wpc = blockDim.x >> 5;
+                for (int u = blockIdx.x; u < npairs * S; u += gridDim.x) {
+                    const int pr = u / S, slice = u % S;
+                    int I, J;
+                    round_pair(r, pr, nb, I, J);
+                    const double2 *Up = Us + (size_t)pr * kJL * kJL;
+                    for (int e = tid; e < kJL * kJL; e += blockDim.x) U[e % kJL][e / kJL] = Up[e];
+                    __syncthreads();
+                    const long long col = blk_idx(I, J, lane);
+                    for (int rit = slice * wpc + warp; rit < 2 * kp; rit += S * wpc) {
+                        double2 *M = rit < kp ? G : V;
+                        const int row = rit % kp;
+                        const double2 x = M[row + col * kp];
+                        double2 acc = make_double2(0.0, 0.0);
 #pragma unroll 8
-                for (int m = 0; m < kJL; m++) {
-                    const double xr = __shfl_sync(0xffffffffu, x.x, m), xi = __shfl_sync(0xffffffffu, x.y, m);
-                    const double2 u = __ldg(&Up[m + lane * kJL]);   // U[m][lane]
-                    acc.x = fma(xr, u.x, acc.x);
-                    acc.x = fma(-xi, u.y, acc.x);
-                    acc.y = fma(xr, u.y, acc.y);
-                    acc.y = fma(xi, u.x, acc.y);
+                        for (int m = 0; m < kJL; m++) {
+                            const double xr = __shfl_sync(0xffffffffu, x.x, m), xi = __shfl_sync(0xffffffffu, x.y, m);
+                            const double2 uu = U[m][lane];
+                            acc.x = fma(xr, uu.x, acc.x);
+                            acc.x = fma(-xi, uu.y, acc.x);
+                            acc.y = fma(xr, uu.y, acc.y);
+                            acc.y = fma(xi, uu.x, acc.y);
+                        }
+                        M[row + col * kp] = acc;
+                    }
+                    __syncthreads();
                 }
-                M[row + col * kp] = acc;
             }
             grid_barrier(bar, bar + 1, nblocks);
-            // ---- P3: rows: G[I u J, col] <- U^H G[I u J, col], one warp per (pair, column)
-            for (long long it = gwarp; it < (long long)npairs * kp; it += nwarps) {
-                const int pr = (int)(it / kp), col = (int)(it % kp);
-                int I, J;
-                round_pair(r, pr, nb, I, J);
-                const double2 *Up = Us + (size_t)pr * kJL * kJL;
-                const long long row = blk_idx(I, J, lane);
-                const double2 y = G[row + (long long)col * kp];
-                double2 acc = make_double2(0.0, 0.0);
+            if (tr) trace[r * 4 + 2] = globaltimer_ns();
+            // ---- P3: rows: G[I u J, col] <- U^H G[I u J, col], same grouping, warps take columns
+            {
+                const int S = (int)gridDim.x / npairs > 0 ? (int)gridDim.x / npairs : 1;
+                const int wpc = blockDim.x >> 5;
+                for (int u = blockIdx.x; u < npairs * S; u += gridDim.x) {
+                    const int pr = u / S, slice = u % S;
+                    int I, J;
+                    round_pair(r, pr, nb, I, J);
+                    const double2 *Up = Us + (size_t)pr * kJL * kJL;
+                    for (int e = tid; e < kJL * kJL; e += blockDim.x) U[e % kJL][e / kJL] = Up[e];
+                    __syncthreads();
+                    const long long row = blk_idx(I, J, lane);
+                    for (int col = slice * wpc + warp; col < kp; col += S * wpc) {
+                        const double2 y = G[row + (long long)col * kp];
+                        double2 acc = make_double2(0.0, 0.0);
 #pragma unroll 8
-                for (int m = 0; m < kJL; m++) {
-                    const double yr = __shfl_sync(0xffffffffu, y.x, m), yi = __shfl_sync(0xffffffffu, y.y, m);
-                    const double2 u = __ldg(&Up[m + lane * kJL]);   // conj(U[m][lane]) y_m
-                    acc.x = fma(u.x, yr, acc.x);
-                    acc.x = fma(u.y, yi, acc.x);
-                    acc.y = fma(u.x, yi, acc.y);
-                    acc.y = fma(-u.y, yr, acc.y);
+                        for (int m = 0; m < kJL; m++) {
+                            const double yr = __shfl_sync(0xffffffffu, y.x, m), yi = __shfl_sync(0xffffffffu, y.y, m);
+                            const double2 uu = U[m][lane];   // conj(U[m][lane]) y_m
+                            acc.x = fma(uu.x, yr, acc.x);
+                            acc.x = fma(uu.y, yi, acc.x);
+                            acc.y = fma(uu.x, yi, acc.y);
+                            acc.y = fma(-uu.y, yr, acc.y);
+                        }
+                        if (row == col) acc.y = 0.0;  // Hermitian: real diagonal
+                        G[row + (long long)col * kp] = acc;
+                    }
+                    __syncthreads();
                 }
-                if (row == col) acc.y = 0.0;  // Hermitian: real diagonal
-                G[row + (long long)col * kp] = acc;
             }
             grid_barrier(bar, bar + 1, nblocks);
+            if (tr) trace[r * 4 + 3] = globaltimer_ns();
         }
         const double off = __longlong_as_double((long long)*(volatile unsigned long long *)flag);
         grid_barrier(bar, bar + 1, nblocks);
@@ -459,14 +497,14 @@ int jacobi_pad(int k) {  // kp for the block Jacobi: a multiple of 2 kJB
 size_t bjacobi_scratch_bytes(int kp) { return sizeof(double2) * (size_t)(kp / kJL) * kJL * kJL; }
 
 cudaError_t launch_bjacobi(double2 *G, double2 *V, int kp, double2 *Us, unsigned long long *flags, int *sweeps,
-                           int num_sms, cudaStream_t s) {
+                           int num_sms, cudaStream_t s, unsigned long long *trace) {
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, 256, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, kBjThreads, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     int grid = num_sms;
-    void *args[] = {&G, &V, &kp, &Us, &flags, &sweeps};
-    return cudaLaunchCooperativeKernel((void *)k_bjacobi, grid, 256, args, 0, s);
+    void *args[] = {&G, &V, &kp, &Us, &flags, &sweeps, &trace};
+    return cudaLaunchCooperativeKernel((void *)k_bjacobi, grid, kBjThreads, args, 0, s);
 }
 
 // X(:, r) = Q V(:, order[r]) for r < kr: X is N_v x kr vectors (column stride ldx_v), Q is
