@@ -312,8 +312,6 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
     const unsigned nblocks = gridDim.x;
     const int nb = kp / kJB, npairs = nb / 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long gwarp = blockIdx.x * (long long)(blockDim.x >> 5) + warp;
-    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
     int sweep = 0;
     for (; sweep < 40; sweep++) {
         unsigned long long *flag = &flags[sweep & 1];
