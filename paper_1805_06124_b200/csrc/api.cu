@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx, no-ops otherwise
+
 #include "comm.h"
 #include "kernels.h"
 #include "rbg.h"
@@ -55,6 +57,12 @@ rbg_status fail(rbg_status s, const char *fmt, ...) {
 
 struct PhaseEvents {
     cudaEvent_t e[4];
+};
+
+// NVTX range for the host-side enqueue of one phase (SURVEY §5 tracing)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 }  // namespace
@@ -218,6 +226,7 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
 }
 
 rbg_status enqueue_local(rbg_ctx *c) {
+    NvtxRange range("rbg.sweep");
     if (c->resume_pending) {  // r2 / R of the added columns are already up to date
         c->resume_pending = false;
         return RBG_OK;
@@ -229,6 +238,7 @@ rbg_status enqueue_local(rbg_ctx *c) {
 }
 
 rbg_status enqueue_xchg(rbg_ctx *c) {
+    NvtxRange range("rbg.exchange");
     if (c->comm == RBG_COMM_PEER) {
         CU(launch_peer_wait(c->peer_in, c->world, c->st, c->epoch, c->peer_timeout_ns, c->stream));
         return RBG_OK;
@@ -242,6 +252,7 @@ rbg_status enqueue_xchg(rbg_ctx *c) {
 }
 
 rbg_status enqueue_finish(rbg_ctx *c) {
+    NvtxRange range("rbg.imgs");
     if (c->ortho == RBG_ORTHO_CGS)
         CU(launch_imgs_cgs(imgs_args(c), c->cplx, c->cgs_v, c->cgs_c, c->cgs_grid, c->stream));
     else
@@ -250,6 +261,7 @@ rbg_status enqueue_finish(rbg_ctx *c) {
 }
 
 rbg_status enqueue_iteration(rbg_ctx *c) {
+    NvtxRange range("rbg.iteration");
     PhaseEvents *pe = nullptr;
     if (c->timing) {
         PhaseEvents p;
