@@ -309,6 +309,15 @@ def run_ours(a):
     im = imgs_ms[W:W + K]
     xc = xchg_ms[W:W + K]
     errs = ctx.errors()
+    replicas = None
+    if world > 1:
+        # the replicated IMGS must leave bit-identical pivots / errors / basis on every rank
+        # (SURVEY §5 integrity check): compare a hash of their bits across the ranks
+        import hashlib
+        hsh = hashlib.sha256()
+        for arr in (ctx.pivots(), errs, ctx.basis()):
+            hsh.update(np.ascontiguousarray(arr).tobytes())
+        replicas = len(set(D.all_gather_bytes(hsh.hexdigest()))) == 1
     ctx.close()
 
     it_s = K / (ms / 1e3)
@@ -348,6 +357,7 @@ def run_ours(a):
         "roofline": roof, "clocks": clocks,
         "exchange_used": {rbg.COMM_NONE: "none", rbg.COMM_PEER: "peer", rbg.COMM_NCCL: "nccl"}[comm],
         **({"exchange_fallback": fallback} if fallback else {}),
+        **({"replicas_bit_identical": replicas} if replicas is not None else {}),
         # ours per iteration: sweep + IMGS (+ the PEER wait kernel); NCCL's own kernel not counted
         "gpu_launches": (3 if comm == rbg.COMM_PEER else 2) * K,
     }
