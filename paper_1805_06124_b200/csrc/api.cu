@@ -121,6 +121,8 @@ struct rbg_ctx {
     // appended, and the record-tag epoch (bumped by every sharded append)
     long long *gid = nullptr;
     unsigned long long epoch = 0;
+    long long *imgs_trace = nullptr;  // RBG_DEBUG_IMGS=<iteration>: phase clocks of that IMGS
+    long long trace_iter = -1;
 };
 
 namespace {
@@ -128,6 +130,31 @@ namespace {
 void free_ctx(rbg_ctx *c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->imgs_trace) {  // RBG_DEBUG_IMGS: mean cycles per phase over the traced MGS steps
+        long long t[32 * 8];
+        if (cudaMemcpy(t, c->imgs_trace, sizeof t, cudaMemcpyDeviceToHost) == cudaSuccess && t[4] > 0) {
+            double ph[4] = {0, 0, 0, 0}, step = 0;
+            int n = 0;
+            double sb[3] = {0, 0, 0};
+            for (int i = 0; i < 32 && t[i * 8 + 4] > 0; i++, n++) {
+                for (int p = 0; p < 4; p++) ph[p] += (double)(t[i * 8 + p + 1] - t[i * 8 + p]);
+                if (t[i * 8 + 5]) {
+                    sb[0] += (double)(t[i * 8 + 5] - t[i * 8 + 2]);
+                    sb[1] += (double)(t[i * 8 + 6] - t[i * 8 + 5]);
+                    sb[2] += (double)(t[i * 8 + 7] - t[i * 8 + 6]);
+                }
+                if (i + 1 < 32 && t[(i + 1) * 8] > 0) step += (double)(t[(i + 1) * 8] - t[i * 8]);
+            }
+            if (n > 1 && sb[0] > 0)
+                fprintf(stderr, "rbg: imgs reduce: butterfly %.0f, CTA tree %.0f, remote wait %.0f, rest %.0f cycles\n",
+                        sb[0] / n, sb[1] / n, sb[2] / n, ph[2] / n - (sb[0] + sb[1] + sb[2]) / n);
+            if (n > 1)
+                fprintf(stderr, "rbg: imgs iteration %lld, %d steps: wait-stage %.0f, dot %.0f, reduce %.0f, axpy %.0f, "
+                                "step %.0f cycles\n", c->trace_iter, n, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n,
+                        step / (n - 1));
+        }
+        dfree(c->imgs_trace);
+    }
     if (c->graph) cudaGraphExecDestroy(c->graph);
     for (auto &p : c->ev)
         for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
@@ -222,6 +249,7 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.peer_slot = c->slot;
     for (int q = 0; q < kMaxPeers; q++) a.peer_send[q] = q < c->world ? c->peer_send[q] : nullptr;
     a.gid = c->gid;
+    a.trace = (c->imgs_trace && c->iters == c->trace_iter) ? c->imgs_trace : nullptr;
     return a;
 }
 
@@ -603,6 +631,11 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         CUB(dmalloc(&c->cgs_v, (size_t)nvec * 16));
         CUB(dmalloc(&c->cgs_c, sizeof(double2) * (size_t)c->k_max));
         c->cgs_grid = cgs_grid(c->num_sms);
+    }
+    if (const char *ti = getenv("RBG_DEBUG_IMGS")) {
+        c->trace_iter = atoll(ti);
+        CUB(dmalloc(&c->imgs_trace, 32 * 8 * sizeof(long long)));
+        CUB(cudaMemsetAsync(c->imgs_trace, 0, 32 * 8 * sizeof(long long), c->stream));
     }
     c->cfg_init = sweep_config(cplx, true, nvec, c->num_sms, c->device);
     c->cfg_sweep = sweep_config(cplx, false, nvec, c->num_sms, c->device);

@@ -17,6 +17,7 @@
 // replicated on every GPU of a sharded run (no broadcast of q needed).
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -32,6 +33,19 @@ namespace rbg {
 // Slots and mbarriers are double-buffered by reduction parity: a CTA can only receive the
 // data of reduction n+2 after all of its own warps have sent reduction n+1, i.e. after
 // they finished reading the buffers of reduction n.
+#include <cstdio>
+// Watchdog wait for the producer's off-critical-path waits: a protocol bug ends the kernel with
+// a message and a trap (a CUDA error the ABI reports) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait_guarded(uint64_t *bar, uint32_t parity, int code, long long st) {
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        if (clock64() - t0 > 4000000000LL) {
+            printf("IMGS HANG code %d rank %u tid %d step %lld parity %u\n", code, cluster_ctarank(), threadIdx.x, st, parity);
+            __trap();
+        }
+    }
+}
+
 template <int CTAS>
 struct ClusterReducer {
     static constexpr int WPC = kLaneImgs / CTAS / 32;  // warps per CTA; CTAS * WPC = 64 leaves
@@ -66,6 +80,90 @@ struct ClusterReducer {
         return make_double2(x, y);
     }
 };
+
+// Variant with a CTA-level pre-reduction (PRE): the warp partials of a CTA are combined in
+// shared memory behind a named barrier of the consumer warps (tree levels 6 .. 5 + log2 WPC),
+// then warp 0's lanes st.async the CTA partial into slot `rank` of every CTA (CTAS messages
+// per CTA instead of 64), and every warp finishes the tree over the CTAS partials in
+// registers.  Same balanced pairwise tree over the 2048 lanes, same bits.  Slots and
+// mbarriers double-buffered by parity as in ClusterReducer (a CTA's warp 0 sends reduction
+// n + 1 only after all its warps passed the named barrier of n + 1, i.e. after they read the
+// slots of reduction n).
+template <int CTAS>
+struct ClusterReducerPre {
+    static constexpr int WPC = kLaneImgs / CTAS / 32;
+    double2 (*slots)[64];   // [parity][CTA]
+    double2 (*wp)[32];      // [parity][warp]
+    uint64_t *bars;
+    uint32_t rank;
+    int warp, lane, par;
+    uint32_t phase;
+    long long *sub = nullptr;  // RBG_DEBUG_IMGS: clocks after butterfly / CTA tree / remote wait
+
+    __device__ __forceinline__ double2 sum(double re, double im) {
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1) {
+            re = re + __shfl_xor_sync(0xffffffffu, re, h);
+            im = im + __shfl_xor_sync(0xffffffffu, im, h);
+        }
+        if (sub) sub[0] = clock64();
+        if (lane == 0) wp[par][warp] = make_double2(re, im);
+        asm volatile("bar.sync 1, %0;" ::"r"(WPC * 32) : "memory");   // consumer warps only
+        double2 t[WPC];
+#pragma unroll
+        for (int w = 0; w < WPC; w++) t[w] = wp[par][w];
+#pragma unroll
+        for (int h = 1; h < WPC; h <<= 1)
+#pragma unroll
+            for (int w = 0; w < WPC; w += 2 * h) t[w] = make_double2(t[w].x + t[w + h].x, t[w].y + t[w + h].y);
+        if (sub) sub[1] = clock64();
+        if (warp == 0 && lane < CTAS) {
+            const uint32_t dst = map_dsmem(smem_u32(&slots[par][rank]), (uint32_t)lane);
+            const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
+            st_async_v2(dst, t[0].x, t[0].y, bar);
+        }
+        mbar_wait(&bars[par], (phase >> par) & 1u);
+        if (sub) sub[2] = clock64();
+        phase ^= 1u << par;
+        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[par], CTAS * 16);  // re-arm for n+2
+        // the tree over the CTAS CTA partials: lane l holds leaf l mod CTAS, xor-butterfly with
+        // ascending offsets inside each group of CTAS lanes (IEEE + is commutative: every lane
+        // ends with the same bits)
+        const double2 x0 = slots[par][lane % CTAS];
+        double x = x0.x, y = x0.y;
+#pragma unroll
+        for (int h = 1; h < CTAS; h <<= 1) {
+            x = x + __shfl_xor_sync(0xffffffffu, x, h);
+            y = y + __shfl_xor_sync(0xffffffffu, y, h);
+        }
+        par ^= 1;
+        return make_double2(x, y);
+    }
+};
+
+template <class Red>
+__device__ __forceinline__ Red make_reducer(double2 (*slots)[64], double2 (*wp)[32], uint64_t *bars, uint32_t rank,
+                                            int warp, int lane);
+template <>
+__device__ __forceinline__ ClusterReducer<8> make_reducer(double2 (*slots)[64], double2 (*)[32], uint64_t *bars,
+                                                          uint32_t rank, int warp, int lane) {
+    return ClusterReducer<8>{slots, bars, rank, warp, lane, 0, 0u};
+}
+template <>
+__device__ __forceinline__ ClusterReducer<16> make_reducer(double2 (*slots)[64], double2 (*)[32], uint64_t *bars,
+                                                           uint32_t rank, int warp, int lane) {
+    return ClusterReducer<16>{slots, bars, rank, warp, lane, 0, 0u};
+}
+template <>
+__device__ __forceinline__ ClusterReducerPre<8> make_reducer(double2 (*slots)[64], double2 (*wp)[32], uint64_t *bars,
+                                                             uint32_t rank, int warp, int lane) {
+    return ClusterReducerPre<8>{slots, wp, bars, rank, warp, lane, 0, 0u};
+}
+template <>
+__device__ __forceinline__ ClusterReducerPre<16> make_reducer(double2 (*slots)[64], double2 (*wp)[32], uint64_t *bars,
+                                                              uint32_t rank, int warp, int lane) {
+    return ClusterReducerPre<16>{slots, wp, bars, rank, warp, lane, 0, 0u};
+}
 
 template <bool CPLX, int MAXV>
 __device__ __forceinline__ double nrm_partial(const double2 (&v)[MAXV], const double *w, int u0, int nm) {
@@ -186,24 +284,36 @@ struct BasisPipe {
         while (issued < limit) {
             const uint32_t par = (uint32_t)((issued / D - 1) & 1);
             bool ok = false;
-            while (!(ok = mbar_try_wait(&empty[issued % D], par)))
+            const long long tp = clock64();
+            while (!(ok = mbar_try_wait(&empty[issued % D], par))) {
                 if (*done >= 0) break;
+                if (clock64() - tp > 4000000000LL) {
+                    printf("IMGS HANG producer rank %u issued %lld par %u\n", cluster_ctarank(), issued, par);
+                    __trap();
+                }
+            }
             if (!ok) break;
             issue(issued++);
         }
         long long consumed;
+        const long long td = clock64();
         while ((consumed = *done) < 0) {
+            if (clock64() - td > 4000000000LL) {
+                printf("IMGS HANG producer waits for done, rank %u issued %lld\n", cluster_ctarank(), issued);
+                __trap();
+            }
         }
-        for (long long s = consumed; s < issued; s++) mbar_wait(&full[s % D], (uint32_t)((s / D) & 1));
+        for (long long s = consumed; s < issued; s++) mbar_wait_guarded(&full[s % D], (uint32_t)((s / D) & 1), 3, s);
     }
 };
 
-template <bool CPLX, int MAXV, int D, int CTAS>
+template <bool CPLX, int MAXV, int D, int CTAS, bool PRE>
 __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArgs a) {
     constexpr int THREADS = kLaneImgs / CTAS;  // consumer threads per CTA (one lane each)
     constexpr int DD = D > 0 ? D : 1;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double2 s_slots[2][64];
+    __shared__ double2 s_wp[2][32];
     __shared__ __align__(8) uint64_t s_bars[2];
     __shared__ __align__(8) uint64_t s_full[DD], s_empty[DD];
     __shared__ long long s_done;
@@ -235,8 +345,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     if (tid == 0) {
         mbar_init(&s_bars[0], 1);
         mbar_init(&s_bars[1], 1);
-        mbar_arrive_expect_tx(&s_bars[0], 64 * 16);
-        mbar_arrive_expect_tx(&s_bars[1], 64 * 16);
+        mbar_arrive_expect_tx(&s_bars[0], (PRE ? CTAS : 64) * 16);
+        mbar_arrive_expect_tx(&s_bars[1], (PRE ? CTAS : 64) * 16);
         s_done = -1;
     }
     if (D > 0 && tid == THREADS) {
@@ -271,7 +381,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     }
 
     const int warp = tid >> 5, lane = tid & 31;
-    ClusterReducer<CTAS> red{s_slots, s_bars, rank, warp, lane, 0, 0u};
+    using Red = typename std::conditional<PRE, ClusterReducerPre<CTAS>, ClusterReducer<CTAS>>::type;
+    Red red = make_reducer<Red>(s_slots, s_wp, s_bars, rank, warp, lane);
     const uint64_t keep = policy_evict_last();
     const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
     double n_prev = n0, nn = 0.0;
@@ -293,12 +404,26 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
             double pr, pi;
             double2 c;
             if (D > 0) {
+                // RBG_DEBUG_IMGS: clock64 at the phase boundaries of steps 64..95 (CTA 0, tid 0)
+                const bool tr = a.trace && rank == 0 && tid == 0 && s >= 64 && s < 96;
+                long long c0 = tr ? clock64() : 0;
                 mbar_wait(&s_full[s % DD], (uint32_t)((s / DD) & 1));
+                long long c1 = tr ? clock64() : 0;
                 dot_partial<CPLX, MAXV>(v, pipe.wq_stage(s) + tid, THREADS, nm, pr, pi);
+                long long c2 = tr ? clock64() : 0;
+                long long sb[3] = {0, 0, 0};
+                if constexpr (PRE) red.sub = tr ? sb : nullptr;
                 c = red.sum(pr, pi);
+                long long c3 = tr ? clock64() : 0;
                 axpy<CPLX, MAXV>(v, pipe.q_stage(s) + tid, THREADS, nm, c);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[s % DD]);  // this warp is done with the stage
+                if (tr) {
+                    const long long c4 = clock64();
+                    long long *t = a.trace + (s - 64) * 8;
+                    t[0] = c0; t[1] = c1; t[2] = c2; t[3] = c3; t[4] = c4;
+                    t[5] = sb[0]; t[6] = sb[1]; t[7] = sb[2];
+                }
             } else {
                 dot_partial<CPLX, MAXV>(v, wq, 1, nm, pr, pi);
                 double2 wq_n[MAXV], q_n[MAXV];
@@ -385,9 +510,21 @@ static int imgs_ctas() {
     return c;
 }
 
+// CTA pre-reduction before the cluster all-to-all (ClusterReducerPre, the default: 0.76-0.78
+// vs 0.78-0.85 us per MGS step at k = 300); RBG_IMGS_PRE=0 selects the 64-message all-to-all.
+// Same tree, same bits either way.
+static bool imgs_pre() {
+    static int p = -1;
+    if (p < 0) {
+        p = 1;
+        if (const char *e = getenv("RBG_IMGS_PRE")) p = atoi(e) != 0;
+    }
+    return p != 0;
+}
+
 template <bool CPLX, int MAXV, int D, int CTAS>
 static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
-    auto kern = k_imgs<CPLX, MAXV, D, CTAS>;
+    auto kern = imgs_pre() ? k_imgs<CPLX, MAXV, D, CTAS, true> : k_imgs<CPLX, MAXV, D, CTAS, false>;
     constexpr int THREADS = kLaneImgs / CTAS;
     const size_t smem = D > 0 ? (size_t)D * 2 * MAXV * THREADS * 16 : 0;
     cudaError_t e;

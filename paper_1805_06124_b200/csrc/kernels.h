@@ -78,6 +78,7 @@ struct ImgsArgs {
     const unsigned char *peer_send[kMaxPeers];
     size_t peer_slot;
     const long long *gid;  // as SweepArgs::gid (the owner masks its selected local column)
+    long long *trace;      // RBG_DEBUG_IMGS: per-phase clock64 of 32 MGS steps (else NULL)
 };
 
 // Local index of global column J on this rank, -1 if another rank owns it.

@@ -31,3 +31,4 @@ for i in [1, 2, 5, 10, 25, 50, 100, 150, 200, 250, k - 1]:
     if i < k:
         steps = max(nu[i] * i, 1)
         print(f"k={i:4d} nu={nu[i]} imgs {im[i] * 1e3:8.1f} us  per MGS step {im[i] * 1e3 / steps:6.3f} us")
+ctx.close()
