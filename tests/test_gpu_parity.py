@@ -380,3 +380,35 @@ def test_explicit_residual_parity(rbg, orc, case):
     compare(g, o)
     if case in ("cfg0", "cfg1"):
         assert g.stop == "TOL"
+
+
+@pytest.mark.parametrize("world,M,N,cplx", [(4, 5, 40, True), (3, 7, 33, False), (2, 2, 9, True)])
+def test_peer_tiny_shards_until_all_selected(rbg, orc, world, M, N, cplx):
+    """PEER ranks holding one or two columns each (most warps and CTAs have no column; a rank's
+    record is -inf once its columns are selected) run to ALL_SELECTED with the oracle's bits."""
+    import torch
+    from paper_1805_06124_b200 import dist as D
+    rng = np.random.default_rng(M * 31 + N)
+    S = rng.standard_normal((M, N)) + (1j * rng.standard_normal((M, N)) if cplx else 0)
+    w = rng.uniform(0.5, 1.5, N)
+    k_max = M
+    o = orc.greedy(S, w, 0.0, k_max, lanes=orc.CANONICAL)
+    stream = torch.cuda.Stream()
+    ctxs = []
+    for p in range(world):
+        off, m = D.partition(M, world, p)
+        ctxs.append(rbg.Context(S[off:off + m], w, 0.0, k_max, stream=stream.cuda_stream, comm=rbg.COMM_PEER,
+                                rank=p, world=world, col_offset=off, M_global=M, peer_timeout_ms=20000))
+    rbg.peer_connect_local(ctxs)
+    for _ in range(k_max + 2):
+        for c in ctxs:
+            c.iter_local()
+        for c in ctxs:
+            c.iter_finish()
+    for c in ctxs:
+        r = c.result()
+        assert (r.k, r.stop) == (o.k, o.stop)
+        np.testing.assert_array_equal(r.pivots, o.pivots)
+        np.testing.assert_array_equal(r.errors, o.errors)
+        np.testing.assert_array_equal(r.Q, o.Q)
+        c.close()
