@@ -10,6 +10,9 @@ Functions follow arXiv 1805.06124 (PAPER.md line numbers):
   * ``imgs``    -- the IMGS step alone;
   * ``dot`` / ``nrm`` -- the weighted inner product and norm in the canonical order.
 
+Parity unpinned: the exact pivot sequence below the recurrence floor (R8) and the
+exact k of a RANK stop are fixed only by the canonical summation order, not by the paper.
+
 Lane counts: ``L_S`` (sweep) and ``L_I`` (IMGS).  ``L_S = L_I = 1`` is the plain
 sequential-sum mode; ``CANONICAL = (32, 2048)`` is the order of DESIGN.md's
 canonical arithmetic contract.  These numbers are written here from DESIGN.md, not

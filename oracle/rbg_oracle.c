@@ -25,6 +25,10 @@
  *
  * Pins: tests/test_oracle_pins.py (closed forms, Prop. 5.5 equivalence with Algorithm 2,
  * LAPACK xGEQP3, Cor. 5.6 brute force, Cor. 5.7 volume identity, error bound of the dot).
+ * Parity unpinned: the exact pivot sequence once the residuals reach the recurrence's accuracy
+ * floor (R8) and the exact k of a RANK stop (configs 0, 1, 4) are fixed only by the
+ * summation order above -- the paper does not determine them; the plain-mode test reports
+ * where two valid orders part.
  */
 #include <math.h>
 #include <stdint.h>
