@@ -532,3 +532,157 @@ def gen_chirp(S, t, w, q, chi, psi, spin: bool, stream=None):
         raise RbgError(ECUDA, f"rbg_gen_chirp failed ({rc})")
     torch.cuda.current_stream(dev).synchronize()
     del A, base, wt, qt, ct, pt
+
+
+# ----------------------------------------------------------------------------- C-ABI names
+# One Python function per entry point of include/rbg.h, named as the C function without its
+# `rbg_` prefix (argument marshalling only; tests/test_abi.py checks the correspondence).
+
+def create(S, N: int | None = None, M: int | None = None, w=None, tol: float = 0.0, k_max: int = 1,
+           dtype=None) -> Context:
+    """rbg_create: host S (M, N) array (N, M, dtype are implied by the array)."""
+    return Context(np.asarray(S), w, tol, k_max)
+
+
+def create_ex(S, w=None, tol: float = 0.0, k_max: int = 1, **kw) -> Context:
+    """rbg_create_ex: host array or CUDA tensor, plus the rbg_desc fields as keywords."""
+    return Context(S, w, tol, k_max, **kw)
+
+
+def desc_init() -> Desc:
+    """rbg_desc_init: a descriptor with the library defaults."""
+    d = Desc()
+    lib().rbg_desc_init(ctypes.byref(d))
+    return d
+
+
+def get_unique_id() -> bytes:
+    return unique_id()
+
+
+def run(ctx: Context):
+    return ctx.run()
+
+
+def step(ctx: Context, n: int):
+    ctx.step(n)
+
+
+def set_timing(ctx: Context, on: bool):
+    ctx.set_timing(on)
+
+
+def set_graph_batch(ctx: Context, batch: int):
+    ctx.set_graph_batch(batch)
+
+
+def sync(ctx: Context):
+    ctx.sync()
+
+
+def result_info(ctx: Context) -> tuple[int, int, str]:
+    return ctx.info()
+
+
+def get_pivots(ctx: Context) -> np.ndarray:
+    return ctx.pivots()
+
+
+def get_errors(ctx: Context) -> np.ndarray:
+    return ctx.errors()
+
+
+def get_nu(ctx: Context) -> np.ndarray:
+    return ctx.nu()
+
+
+def get_rdiag(ctx: Context) -> np.ndarray:
+    return ctx.rdiag()
+
+
+def get_basis(ctx: Context) -> np.ndarray:
+    return ctx.basis()
+
+
+def get_R(ctx: Context) -> np.ndarray:  # noqa: N802 (C name)
+    return ctx.R()
+
+
+def get_r2(ctx: Context) -> np.ndarray:
+    return ctx.r2()
+
+
+def get_stats(ctx: Context) -> Stats:
+    return ctx.stats()
+
+
+def get_timings(ctx: Context, n: int):
+    return ctx.timings(n)
+
+
+def validate(ctx: Context, V, coeffs: bool = False):
+    return ctx.validate(V, coeffs)
+
+
+def add_columns(ctx: Context, F):
+    ctx.add_columns(F)
+
+
+def add_columns_ex(ctx: Context, F, first_gid: int, M_global: int):
+    ctx.add_columns(F, first_gid=first_gid, M_global=M_global)
+
+
+def gram(ctx: Context) -> np.ndarray:
+    return ctx.gram()
+
+
+def gram_fold(ctx: Context, G=None) -> np.ndarray:
+    return ctx.gram_fold(G)
+
+
+def reconstruct(ctx: Context, tau2: float = 0.0, kr_max: int = 0):
+    return ctx.reconstruct(tau2, kr_max)
+
+
+def reconstruct_gram(ctx: Context, G, tau2: float = 0.0, kr_max: int = 0):
+    return ctx.reconstruct_gram(G, tau2, kr_max)
+
+
+def eim(ctx: Context):
+    return ctx.eim()
+
+
+def iter_local(ctx: Context):
+    ctx.iter_local()
+
+
+def iter_finish(ctx: Context):
+    ctx.iter_finish()
+
+
+def xchg_buffers(ctx: Context):
+    return ctx.xchg_buffers()
+
+
+def peer_export(ctx: Context) -> bytes:
+    return ctx.peer_export()
+
+
+def peer_connect(ctx: Context, handles: list[bytes]):
+    ctx.peer_connect(handles)
+
+
+def debug_set_canary(on: bool):
+    set_canary(on)
+
+
+def debug_canary_violations() -> tuple[int, str]:
+    return canary_violations()
+
+
+def last_error() -> str:
+    return lib().rbg_last_error().decode()
+
+
+def destroy(ctx: Context):
+    ctx.close()

@@ -84,3 +84,9 @@ def test_invalid_arguments_rejected(rbg, case):
 
 def test_destroy_null_is_safe(rbg):
     rbg.lib().rbg_destroy(None)
+
+
+def test_python_binding_has_every_c_name(rbg):
+    """The thin binding offers every entry point under the C name without its `rbg_` prefix."""
+    missing = [n for n in declared_functions() if not callable(getattr(rbg, n[len("rbg_"):], None))]
+    assert not missing, missing
