@@ -270,6 +270,13 @@ def test_peer_exchange_on_one_gpu(rbg, orc, world, ortho):
         np.testing.assert_array_equal(r.Q, o.Q)
     np.testing.assert_array_equal(np.concatenate([r.R for r in res], axis=1), o.R)
     np.testing.assert_array_equal(np.concatenate([r.r2 for r in res]), o.r2)
+    if ortho == "mgs":
+        # EIM works on any rank of a sharded run (the basis is replicated): the oracle's nodes
+        nodes_o, B_o = orc.eim(o.Q)
+        for c in ctxs:
+            nodes, B = c.eim()
+            np.testing.assert_array_equal(nodes, nodes_o)
+            np.testing.assert_array_equal(B, B_o)
     for c in ctxs:
         c.close()
 
