@@ -90,6 +90,7 @@ void free_ctx(rbg_ctx *c) {
     dfree(c->nu);
     dfree(c->recs);
     dfree(c->ticket);
+    dfree(c->next_col);
     dfree(c->send);
     dfree(c->recv);
     dfree(c->cgs_v);
@@ -117,6 +118,7 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.st = c->st;
     a.recs = c->recs;
     a.ticket = c->ticket;
+    a.next_col = c->next_col;
     a.col_offset = c->col_offset;
     a.send = c->comm != RBG_COMM_NONE ? c->send : nullptr;
     a.peer_world = 0;
@@ -310,9 +312,12 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     const int grid = std::max(c->cfg_init.grid, c->cfg_sweep.grid);
     cudaError_t e = dmalloc(&vst, sizeof(DevState));
     if (e == cudaSuccess) e = dmalloc(&recs, sizeof(Rec) * grid);
+    unsigned long long *ncol = nullptr;
     if (e == cudaSuccess) e = dmalloc(&ticket, sizeof(unsigned));
+    if (e == cudaSuccess) e = dmalloc(&ncol, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(vst, 0, sizeof(DevState), c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(ticket, 0, sizeof(unsigned), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ncol, 0, sizeof(unsigned long long), c->stream);
     SweepArgs a = sweep_args(c);
     a.S = V;
     a.ldv = c->nvec;
@@ -323,6 +328,7 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     a.st = vst;
     a.recs = recs;
     a.ticket = ticket;
+    a.next_col = ncol;
     a.col_offset = 0;
     a.send = nullptr;
     a.peer_world = 0;   // a block outside the training set: no exchange, its own indices
@@ -337,6 +343,7 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     dfree(vst);
     dfree(recs);
     dfree(ticket);
+    dfree(ncol);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "coefficient passes: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
@@ -555,6 +562,8 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(dmalloc(&c->recs, sizeof(Rec) * max_grid));
     CUB(dmalloc(&c->ticket, sizeof(unsigned)));
     CUB(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
+    CUB(dmalloc(&c->next_col, sizeof(unsigned long long)));
+    CUB(cudaMemsetAsync(c->next_col, 0, sizeof(unsigned long long), c->stream));
 
     if (d->comm == RBG_COMM_PEER) {  // two send slots (by tag parity) + 2 x world records
         c->slot = (xchg_slot_bytes(nvec) + 15) / 16 * 16;

@@ -66,6 +66,7 @@ struct rbg_ctx {
     int *nu = nullptr;
     Rec *recs = nullptr;
     unsigned *ticket = nullptr;
+    unsigned long long *next_col = nullptr;  // dynamic column counter of the sweep
     double tol = 0.0;
     long long k_max = 0;
     rbg_comm comm = RBG_COMM_NONE;

@@ -28,6 +28,7 @@ struct SweepArgs {
     DevState *st;
     Rec *recs;             // one record per CTA
     unsigned *ticket;      // last-CTA-done counter (returns to 0)
+    unsigned long long *next_col;  // dynamic column counter of k_sweep_dyn (returns to 0)
     long long col_offset;  // global index of local column 0
     unsigned char *send;   // exchange slot of this rank (NULL on one GPU)
     // PEER exchange (peer_world > 0): every rank's record array, this rank's index, and the

@@ -24,6 +24,7 @@
 // Sweep 0 (INIT) is the same kernel with e~ = w and the weighted norm of CAC rule 4.
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels.h"
 
@@ -137,6 +138,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
             a.st->m_loc = bm;
             a.st->j_loc = jg;
             *a.ticket = 0u;
+            if (a.next_col) *a.next_col = 0ull;  // every warp has taken its last column
             if (a.send) {
                 Rec *h = reinterpret_cast<Rec *>(send_slot(a));
                 h->m = bm;
@@ -476,6 +478,133 @@ cudaError_t launch_restart(const SweepArgs &a, bool cplx, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Dynamically scheduled ring sweep (default for the recurrence): the ring of k_sweep_ring, but a
+// warp's columns come from a grid-wide counter instead of a static block, so SMs that stream
+// faster take more columns (ncu on the static kernel: SMs active 91.8-100 % of the launch,
+// 95.6 % on average).  The first column of a warp is its global warp index; each later one is
+// one atomicAdd (lane 0) taken a column ahead of use, so its latency never stalls the ring.  A
+// warp's columns increase, so "first max wins" keeps the lowest index among a warp's ties and
+// the CTA / grid maxloc uses the total order: results are bit-identical to k_sweep_ring.  The
+// counter (a.next_col) returns to 0 in the last CTA.
+template <bool CPLX, bool INIT, bool ESMEM, int U>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t mbar;
+
+    if (a.st->stop) return;
+    const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long nvec = a.nvec;
+    const bool odd_tail = !CPLX && (a.N & 1);
+
+    const double2 *Eg = INIT ? reinterpret_cast<const double2 *>(a.w) : a.WQ + (k - 1) * a.ldq_v;
+    const double2 *E = Eg;
+    const double *Ew = a.w;
+    if (ESMEM) {
+        const size_t bytes = (INIT && CPLX) ? ((size_t)nvec * 8 + 15) / 16 * 16 : (size_t)nvec * 16;
+        if (tid == 0) {
+            mbar_init(&mbar, 1);
+            mbar_arrive_expect_tx(&mbar, (uint32_t)bytes);
+            const unsigned char *src = reinterpret_cast<const unsigned char *>(Eg);
+            for (size_t off = 0; off < bytes; off += kBulkChunk) {
+                uint32_t n = (uint32_t)((bytes - off) < kBulkChunk ? (bytes - off) : kBulkChunk);
+                bulk_g2s(smem + off, src + off, n, &mbar);
+            }
+        }
+        __syncthreads();
+        E = reinterpret_cast<const double2 *>(smem);
+        Ew = reinterpret_cast<const double *>(smem);
+    }
+
+    const uint64_t pol = policy_evict_first();
+    const int nv = (int)nvec;
+    const int gpc = (int)((nvec + 32 * U - 1) / (32 * U));  // groups of U trips per column
+    const long long M = a.M;
+    const long long nwg = (long long)gridDim.x * kSweepWarps;
+    // column window of this warp: A = being consumed, B = next, pend = the one after (raw
+    // counter value held by lane 0, shuffled out only at the next shift)
+    long long colA = (long long)blockIdx.x * kSweepWarps + warp;
+    unsigned long long raw = 0;
+    if (lane == 0) raw = atomicAdd(a.next_col, 1ull);
+    long long colB = (long long)__shfl_sync(0xffffffffu, raw, 0) + nwg;
+    unsigned long long praw = 0;
+    if (lane == 0) praw = atomicAdd(a.next_col, 1ull);
+
+    // the issue cursor is always exactly one group ahead of the consume cursor (group cg of
+    // colA): group cg + 1 of colA, or group 0 of colB when cg is colA's last group
+    double2 xr[U];
+    {
+        const double2 *lp = a.S + colA * a.ldv + lane;
+#pragma unroll
+        for (int t = 0; t < U; t++)
+            xr[t] = (colA < M && t * 32 + lane < nv) ? ld_stream(lp + t * 32, pol) : make_double2(0.0, 0.0);
+    }
+    if (ESMEM) mbar_wait(&mbar, 0);
+
+    double best_m = -INFINITY;
+    long long best_j = 0x7fffffffffffffffLL;
+    double re = 0.0, im = 0.0;
+    int cg = 0;
+    double old = (!INIT && colA < M) ? a.r2[colA] : 0.0;
+
+    while (colA < M) {
+        const bool last = cg + 1 == gpc;
+        const long long lc = last ? colB : colA;
+        const int lgrp = last ? 0 : cg + 1;
+        const int lu0 = lgrp * 32 * U + lane;
+        const int cu0 = cg * 32 * U + lane;
+        const double2 *lp = a.S + lc * a.ldv + lu0;
+        const bool lvalid = lc < M;
+#pragma unroll
+        for (int t = 0; t < U; t++) {
+            double2 x = xr[t];
+            xr[t] = (lvalid && lu0 + t * 32 < nv) ? ld_stream(lp + t * 32, pol) : make_double2(0.0, 0.0);
+            const int u = cu0 + t * 32;
+            if (u < nv) {
+                if (odd_tail && u == nv - 1) x.y = 0.0;  // row N is padding
+                accum<CPLX, INIT>(re, im, x, load_e<CPLX, INIT, ESMEM>(E, Ew, u));
+            }
+        }
+        if (!last) {
+            cg++;
+            continue;
+        }
+        // column colA complete (warp-uniform)
+        cg = 0;
+        const long long c = colA;
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1) {  // CAC rule 3
+            re = re + __shfl_xor_sync(0xffffffffu, re, h);
+            if (CPLX && !INIT) im = im + __shfl_xor_sync(0xffffffffu, im, h);
+        }
+        double r2n;
+        if (INIT) {
+            r2n = re;
+            if (lane == 0) a.r2[c] = r2n;
+        } else {
+            const double cc = CPLX ? fma(re, re, im * im) : re * re;  // CAC rule 5
+            r2n = old - cc;                                            // CAC rule 6
+            if (lane == 0) {
+                if (CPLX) reinterpret_cast<double2 *>(a.R)[(k - 1) * a.ldr + c] = make_double2(re, im);
+                else a.R[(k - 1) * a.ldr + c] = re;
+                a.r2[c] = r2n;
+            }
+            old = colB < M ? a.r2[colB] : 0.0;
+        }
+        if (r2n > best_m) {  // a warp's columns increase: first max wins
+            best_m = r2n;
+            best_j = c;
+        }
+        re = 0.0;
+        im = 0.0;
+        // shift the window: B becomes current, the pending column becomes B, take a new one
+        colA = colB;
+        colB = (long long)__shfl_sync(0xffffffffu, praw, 0) + nwg;
+        if (lane == 0) praw = atomicAdd(a.next_col, 1ull);
+    }
+    sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
+}
+
 SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int device) {
     SweepConfig c;
     c.threads = kSweepThreads;
@@ -500,19 +629,24 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
 using SweepKernel = void (*)(const SweepArgs);
 
 template <bool CPLX, bool INIT, bool ESMEM, int U>
-static SweepKernel pick_kernel(bool ring) {
-    // the explicit mode (a.V) re-reads and rewrites each column: per-column loop of k_sweep
+static SweepKernel pick_kernel(bool ring, bool dyn) {
+    // the explicit mode (a.V) re-reads and rewrites each column: per-column loop of k_sweep;
+    // the recurrence: the dynamically scheduled ring (default) or the static-block ring
+    if (dyn) return k_sweep_dyn<CPLX, INIT, ESMEM, U>;
     return ring ? k_sweep_ring<CPLX, INIT, ESMEM, U> : k_sweep<CPLX, INIT, ESMEM, U>;
 }
 
 template <bool CPLX, bool INIT, bool ESMEM>
 static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStream_t s) {
-    const bool ring = a.V == nullptr && getenv("RBG_SWEEP_PERCOL") == nullptr;
-    auto kern = pick_kernel<CPLX, INIT, ESMEM, 4>(ring);
+    // RBG_SWEEP_KIND = dyn (default) | ring (static blocks) | percol (per-column ring)
+    const char *kind = getenv("RBG_SWEEP_KIND");
+    const bool ring = a.V == nullptr && !(kind && std::strcmp(kind, "percol") == 0);
+    const bool dyn = ring && a.next_col != nullptr && !(kind && std::strcmp(kind, "ring") == 0);
+    auto kern = pick_kernel<CPLX, INIT, ESMEM, 4>(ring, dyn);
     switch (cfg.unroll) {
-        case 8: kern = pick_kernel<CPLX, INIT, ESMEM, 8>(ring); break;
-        case 12: kern = pick_kernel<CPLX, INIT, ESMEM, 12>(ring); break;
-        case 16: kern = pick_kernel<CPLX, INIT, ESMEM, 16>(ring); break;
+        case 8: kern = pick_kernel<CPLX, INIT, ESMEM, 8>(ring, dyn); break;
+        case 12: kern = pick_kernel<CPLX, INIT, ESMEM, 12>(ring, dyn); break;
+        case 16: kern = pick_kernel<CPLX, INIT, ESMEM, 16>(ring, dyn); break;
         default: break;
     }
     if (cfg.smem > 48 * 1024) {
