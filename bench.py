@@ -39,10 +39,10 @@ M_PER_GPU = 409_600
 K_MAX = 300
 CPU_SAMPLE_COLS = 16_384
 SPEC_HBM_GBS = 8000.0          # B200 datasheet HBM3e bandwidth (context)
-# measured read-only ceiling of the sweep's own access pattern on this pool's B200s
-# (one warp per 160 KB column, 16-byte loads, 12 in flight per lane): scripts/hbm_probe2.cu,
-# profiles/r01/hbm_probe2.txt
-READ_STREAM_GBS = 7228.5
+# measured read-only ceiling of the sweep's own access pattern on this pool's B200s (one warp
+# per 160 KB column, 16-byte loads, columns dealt dynamically from a grid-wide counter, best
+# of the T/U/occupancy variants): scripts/hbm_probe2.cu, profiles/r01/hbm_probe2.txt
+READ_STREAM_GBS = 7465.3
 
 
 def parse():
@@ -329,7 +329,7 @@ def run_ours(a):
     achieved = bytes_sweep / sweep_avg_s / 1e9
     pk = peaks()
     peak = pk.get("hbm_gbs") or 6650.0
-    roof = {"kernel": "k_sweep (fused coefficient sweep + r2 update + maxloc)", "bound": "hbm",
+    roof = {"kernel": "k_sweep_dyn (fused coefficient sweep + r2 update + maxloc, dynamically scheduled columns)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if pk.get("hbm_gbs") else "fallback 6.65 TB/s",
             "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": bytes_sweep,

@@ -616,9 +616,11 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
     if (c.smem * 2 + 4096 <= 227 * 1024) per_sm = 2;
     (void)device;
     c.grid = num_sms * per_sm;
-    // loads in flight per lane: ~12 keeps ~96 KB per SM outstanding (scripts/hbm_probe.cu)
+    // loads in flight per lane: 16 (128 KB per SM outstanding) for the dynamically scheduled
+    // ring (7.43-7.45 vs 7.42 TB/s for 12, profiles/r01/sweep_dyn_tuning.jsonl); the explicit
+    // mode's per-column kernel caps it at 12
     const long long trips = (nvec + 31) / 32;
-    c.unroll = trips >= 12 ? 12 : (trips >= 8 ? 8 : 4);
+    c.unroll = trips >= 16 ? 16 : (trips >= 12 ? 12 : (trips >= 8 ? 8 : 4));
     if (const char *env = getenv("RBG_SWEEP_UNROLL")) {
         const int u = atoi(env);
         if (u == 4 || u == 8 || u == 12 || u == 16) c.unroll = u;
@@ -643,7 +645,8 @@ static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStre
     const bool ring = a.V == nullptr && !(kind && std::strcmp(kind, "percol") == 0);
     const bool dyn = ring && a.next_col != nullptr && !(kind && std::strcmp(kind, "ring") == 0);
     auto kern = pick_kernel<CPLX, INIT, ESMEM, 4>(ring, dyn);
-    switch (cfg.unroll) {
+    const int unroll = (a.V && cfg.unroll > 12) ? 12 : cfg.unroll;
+    switch (unroll) {
         case 8: kern = pick_kernel<CPLX, INIT, ESMEM, 8>(ring, dyn); break;
         case 12: kern = pick_kernel<CPLX, INIT, ESMEM, 12>(ring, dyn); break;
         case 16: kern = pick_kernel<CPLX, INIT, ESMEM, 16>(ring, dyn); break;

@@ -49,6 +49,35 @@ __global__ void __launch_bounds__(T) col_stream(const double2 *S, long long nvec
     if (acc == 12345.678) out[0] = acc;
 }
 
+// the same column stream with dynamic column assignment (grid-wide atomic counter, a column
+// taken one ahead), as the sweep's k_sweep_dyn
+template <int T, int U>
+__global__ void __launch_bounds__(T) col_stream_dyn(const double2 *S, long long nvec, long long M, double *out,
+                                                    unsigned long long *ctr) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long nwg = (long long)gridDim.x * (T / 32);
+    double acc = 0.0;
+    long long c = (long long)blockIdx.x * (T / 32) + warp;
+    unsigned long long raw = 0;
+    if (lane == 0) raw = atomicAdd(ctr, 1ull);
+    while (c < M) {
+        const double2 *col = S + c * nvec;
+        double2 xa[U];
+#pragma unroll
+        for (int t = 0; t < U; t++) { long long u = t * 32 + lane; xa[t] = u < nvec ? ldnc(col + u) : make_double2(0, 0); }
+        for (long long b = 0; b < nvec; b += 32 * U) {
+            double2 xb[U];
+#pragma unroll
+            for (int t = 0; t < U; t++) { long long u = b + 32 * U + t * 32 + lane; xb[t] = u < nvec ? ldnc(col + u) : make_double2(0, 0); }
+#pragma unroll
+            for (int t = 0; t < U; t++) { acc = fma(xa[t].x, xa[t].y, acc); xa[t] = xb[t]; }
+        }
+        c = (long long)__shfl_sync(0xffffffffu, raw, 0) + nwg;
+        if (lane == 0) raw = atomicAdd(ctr, 1ull);
+    }
+    if (acc == 12345.678) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t *b, uint32_t n) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
@@ -130,6 +159,11 @@ int main() {
 #define COL(T, U, OCC, P) rep("col_stream T=" #T " U=" #U " ctas/SM=" #OCC " L2::256B=" #P, \
         timeit([&] { col_stream<T, U, P><<<sms * OCC, T>>>(S, nvec, M, out); }), bytes);
     COL(512, 12, 1, false) COL(512, 12, 1, true) COL(512, 8, 1, true) COL(256, 16, 4, false) COL(256, 16, 4, true)
+    unsigned long long *ctr;
+    CK(cudaMalloc(&ctr, 8));
+#define DYN(T, U, OCC) rep("col_stream_dyn T=" #T " U=" #U " ctas/SM=" #OCC, \
+        timeit([&] { cudaMemsetAsync(ctr, 0, 8); col_stream_dyn<T, U><<<sms * OCC, T>>>(S, nvec, M, out, ctr); }), bytes);
+    DYN(512, 12, 1) DYN(512, 16, 1) DYN(256, 16, 4) DYN(1024, 8, 1)
 #define TMA(CH, ST, OCC) { \
         auto k = tma_stream<CH, ST>; const int smem = CH * ST; \
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
