@@ -193,7 +193,10 @@ rbg_status rbg_get_timings(rbg_ctx *ctx, double *sweep_ms, double *xchg_ms, doub
  * (column stride ldv elements, 0 => N; host or device), the coefficients
  * C(i, j) = <q_i, v_j>_w against the current basis (i < k) and the projection error
  * err_j = sqrt(max(||v_j||_w^2 - sum_i |C(i,j)|^2, 0)) evaluated with the same per-column
- * arithmetic as the greedy's own residuals (sweep 0 + one sweep per basis vector).
+ * arithmetic as the greedy's own residuals (sweep 0 + the coefficient recurrence; all k
+ * coefficients of a column come from one blocked pass over V, bit-identical to one sweep per
+ * basis vector).  A device V with column pitch equal to the library's padded layout (complex,
+ * or real with N even, ldv = N) and 16-byte alignment is read in place, otherwise copied.
  * err: M_v doubles (may be NULL); C: k x M_v row-major with row stride ldc (may be NULL);
  * both on the device if out_on_device.  Blocking.  ENONFINITE if V holds NaN/Inf.         */
 rbg_status rbg_validate(rbg_ctx *ctx, const void *V, int64_t M_v, int64_t ldv, rbg_mem V_mem, double *err,

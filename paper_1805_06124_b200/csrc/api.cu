@@ -270,18 +270,28 @@ rbg_status read_state(rbg_ctx *c, DevState *h) {
 
 // Device copy of a caller block in the library's column layout (nvec 16-byte vectors per
 // column, zero padded), with the NaN/Inf scan.  *out is owned by the caller of this helper.
-rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld, rbg_mem mem, double2 **out) {
+rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld, rbg_mem mem, double2 **out,
+                        bool *owned) {
     *out = nullptr;
+    *owned = false;
     if (!src || Mb < 1) return fail(RBG_EINVAL, "null block or no columns");
     if (ld == 0) ld = c->N;
     if (ld < c->N) return fail(RBG_EINVAL, "ld=%lld < N=%lld", ld, c->N);
     const size_t pitch = (size_t)c->nvec * 16, col_bytes = (size_t)c->N * c->se;
+    // a device block already in the padded layout (16-byte aligned, column pitch nvec*16) is
+    // read in place for the duration of the call; anything else is copied
+    const bool borrow = mem == RBG_MEM_DEVICE && (size_t)ld * c->se == pitch && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
     double2 *d = nullptr;
-    CU(dmalloc(&d, pitch * Mb));
-    const cudaMemcpyKind kind = mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     cudaError_t e = cudaSuccess;
-    if (pitch != col_bytes) e = cudaMemsetAsync(d, 0, pitch * Mb, c->stream);
-    if (e == cudaSuccess) e = cudaMemcpy2DAsync(d, pitch, src, (size_t)ld * c->se, col_bytes, Mb, kind, c->stream);
+    if (borrow) {
+        d = const_cast<double2 *>(static_cast<const double2 *>(src));
+    } else {
+        CU(dmalloc(&d, pitch * Mb));
+        *owned = true;
+        const cudaMemcpyKind kind = mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        if (pitch != col_bytes) e = cudaMemsetAsync(d, 0, pitch * Mb, c->stream);
+        if (e == cudaSuccess) e = cudaMemcpy2DAsync(d, pitch, src, (size_t)ld * c->se, col_bytes, Mb, kind, c->stream);
+    }
     unsigned long long *bad = nullptr, hbad = ~0ull;
     if (e == cudaSuccess) e = dmalloc(&bad, sizeof *bad);
     if (e == cudaSuccess) e = cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream);
@@ -290,11 +300,13 @@ rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld,
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     dfree(bad);
     if (e != cudaSuccess) {
-        dfree(d);
+        if (*owned) dfree(d);
+        *owned = false;
         return fail(RBG_ECUDA, "uploading a column block: %s", cudaGetErrorString(e));
     }
     if (hbad != ~0ull) {
-        dfree(d);
+        if (*owned) dfree(d);
+        *owned = false;
         return fail(RBG_ENONFINITE, "non-finite entry at (row %lld, col %lld)", (long long)(hbad % c->N),
                     (long long)(hbad / c->N));
     }
@@ -335,9 +347,14 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     a.gid = nullptr;
     a.qi = -1;
     if (e == cudaSuccess) e = launch_sweep(a, c->cplx, true, c->cfg_init, c->stream);
-    for (long long i = 0; i < k && e == cudaSuccess; i++) {
-        a.qi = i;
-        e = launch_sweep(a, c->cplx, false, c->cfg_sweep, c->stream);
+    if (coeff_block_enabled()) {  // one blocked pass for all k basis vectors (coeff.cu)
+        if (e == cudaSuccess)
+            e = launch_coeff_block(V, c->nvec, Mv, c->WQ, c->ldq_v, k, c->nvec, c->N, c->cplx, R, ldr, r2, c->stream);
+    } else {
+        for (long long i = 0; i < k && e == cudaSuccess; i++) {
+            a.qi = i;
+            e = launch_sweep(a, c->cplx, false, c->cfg_sweep, c->stream);
+        }
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     dfree(vst);

@@ -23,7 +23,8 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
     DevState h;
     TRY(read_state(c, &h));
     double2 *Vd = nullptr;
-    TRY(upload_block(c, V, M_v, ldv, V_mem, &Vd));
+    bool v_owned = false;
+    TRY(upload_block(c, V, M_v, ldv, V_mem, &Vd, &v_owned));
     const long long k = h.k;
     double *Rv = nullptr, *e2 = nullptr, *ed = nullptr;
     cudaError_t e = dmalloc(&Rv, (size_t)std::max<long long>(k, 1) * M_v * c->se);
@@ -42,7 +43,7 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "validation coefficients: %s", cudaGetErrorString(e));
     }
     cudaStreamSynchronize(c->stream);
-    dfree(Vd);
+    if (v_owned) dfree(Vd);
     dfree(Rv);
     dfree(e2);
     dfree(ed);
@@ -67,7 +68,8 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     TRY(read_state(c, &h));
     const long long M0 = c->M, M1 = c->M + M_f;
     double2 *Fd = nullptr;
-    if (M_f > 0) TRY(upload_block(c, F, M_f, ldf, F_mem, &Fd));
+    bool f_owned = false;
+    if (M_f > 0) TRY(upload_block(c, F, M_f, ldf, F_mem, &Fd, &f_owned));
     const size_t pitch = (size_t)c->nvec * 16;
     double2 *S1 = c->S;
     double *R1 = c->R, *r21 = c->r2;
@@ -100,7 +102,7 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
         }
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     }
-    dfree(Fd);
+    if (f_owned) dfree(Fd);
     auto drop_new = [&]() {
         if (M_f > 0) {
             dfree(S1);

@@ -115,7 +115,8 @@ SweepArgs sweep_args(const rbg_ctx *c);
 ImgsArgs imgs_args(const rbg_ctx *c);
 rbg_status check_ctx(rbg_ctx *c);
 rbg_status read_state(rbg_ctx *c, DevState *h);
-rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld, rbg_mem mem, double2 **out);
+rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld, rbg_mem mem, double2 **out,
+                        bool *owned);  // *owned = false: a device block read in place
 rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, long long ldr, double *r2,
                         long long k);
 

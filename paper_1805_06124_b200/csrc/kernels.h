@@ -195,6 +195,12 @@ cudaError_t launch_bjacobi(double2 *G, double2 *V, int kp, double2 *Us, unsigned
                            int num_sms, cudaStream_t s, unsigned long long *trace = nullptr);
 
 // Greedy EIM nodes (eim.cu): nodes_d[k], B_d = Q(P, :) k x k column-major complex.
+// coeff.cu: C(i, j) = <q_i, v_j>_w for i < k, j < M in one blocked pass over V, then
+// r2_j -= |C(i, j)|^2 in order i (r2 may be null); bit-identical to k coefficient sweeps.
+bool coeff_block_enabled();
+cudaError_t launch_coeff_block(const double2 *V, long long ldv, long long M, const double2 *WQ, long long ldq_v,
+                               long long k, long long nvec, long long N, bool cplx, double *C, long long ldc,
+                               double *r2, cudaStream_t s);
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
                     int *status_d, cudaStream_t s);
 

@@ -189,3 +189,42 @@ def test_gpu_sharded_enrichment_bit_exact(orc, mode, cplx):
     np.testing.assert_array_equal(r2, res.r2)
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cplx,N,M_v,k", [
+    (True, 400, 37, 35),      # ragged column and basis tiles, 6.25 stages of 64 rows
+    (True, 400, 16, 16),      # exactly one tile
+    (True, 400, 5, 1),        # one basis vector
+    (False, 257, 50, 33),     # real, odd N (padding row in the last 16-byte vector)
+    (False, 128, 17, 20),     # real, N a multiple of the stage
+    (True, 2000, 1000, 100),  # config-1 rows, many CTAs per column tile
+])
+def test_gpu_coefficient_block_bit_exact(orc, monkeypatch, cplx, N, M_v, k):
+    """The blocked coefficient kernel (coeff.cu: all k basis vectors in one pass over V) gives
+    the oracle's errors and coefficients bit for bit, and the same bits as the k streaming
+    coefficient sweeps it replaces (RBG_COEFF=passes), across tile edges and ragged tails."""
+    from paper_1805_06124_b200 import rbg
+    if N % 2:   # odd N (Simpson needs even N): Gaussian columns, weights U[0.5, 1.5]
+        rng = np.random.default_rng(7)
+        S, V = rng.standard_normal((max(2 * k, 60), N)), rng.standard_normal((M_v, N))
+        w = rng.uniform(0.5, 1.5, N)
+    else:
+        S, w, _, _ = inputs.config1(M=max(2 * k, 60), N=N)
+        t = inputs.chirp_grid(N)
+        q, chi, psi = inputs.chirp_params(M_v, 13, spin=False)
+        V = inputs.chirp_columns(t, w, q, chi, psi, spin=False)
+    if not cplx:
+        S, V = S.real.copy(), V.real.copy()
+    r = orc.greedy(S, w, 0.0, k)
+    assert r.k == k or r.k > 16              # RANK may stop early; still several basis tiles
+    e_o, C_o, _ = orc.validate(r.Q, V, w)
+    with rbg.Context(S, w, 0.0, k) as ctx:
+        ctx.run()
+        err, C = ctx.validate(V, coeffs=True)
+        monkeypatch.setenv("RBG_COEFF", "passes")
+        err_p, C_p = ctx.validate(V, coeffs=True)
+    np.testing.assert_array_equal(err, e_o)
+    np.testing.assert_array_equal(C, C_o)
+    np.testing.assert_array_equal(err_p, err)
+    np.testing.assert_array_equal(C_p, C)
