@@ -11,7 +11,10 @@
 // column (a barrier per column, rows in parallel -- the same per-row DAG as the row-wise
 // sequential sum), then a grid over the N rows forms xi_l, |xi_l|^2 and a deterministic
 // maxloc (last-block-done), and gathers row l of T.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.h"
 
@@ -48,6 +51,7 @@ struct EimArgs {
     int k;
     double2 *Xi;     // k columns of N complex
     double2 *T;      // k x k row-major, T[a*k + b] = xi_b(p_a)
+    double2 *Tt;     // the same, column-major: Tt[b*k + a] = xi_b(p_a)
     double2 *c;      // k coefficients
     long long *nodes;
     double *bm;      // per-block maxloc values
@@ -178,7 +182,222 @@ __global__ void __launch_bounds__(kEimThreads) k_eim_residual(EimArgs a, int l) 
     }
     __syncthreads();
     const long long p = s_j[0];
-    for (int b = threadIdx.x; b <= l; b += blockDim.x) a.T[(long long)l * a.k + b] = __ldcg(&a.Xi[(long long)b * a.N + p]);
+    for (int b = threadIdx.x; b <= l; b += blockDim.x) {
+        const double2 t = __ldcg(&a.Xi[(long long)b * a.N + p]);
+        a.T[(long long)l * a.k + b] = t;
+        a.Tt[(long long)b * a.k + l] = t;
+    }
+}
+
+// ---- warp-level forward substitution (default) -----------------------------------------
+// One warp; row a of the system lives in lane a % 32, register slot a / 32.  Per column b:
+// the owner of row b forms c_b = v_b / T_bb (den of T_bb precomputed: the same two IEEE
+// divisions as cdiv), one shuffle broadcasts it, and every lane subtracts c_b T_ab from its
+// rows a > b -- right-looking, so each row still receives its updates in increasing b, the
+// oracle's sequential sum.  Column b of T (contiguous in the column-major copy Tt) arrives in
+// a shared-memory ring through cp.async.bulk, kRing columns ahead.
+template <int SLOTS>
+struct EimRing {
+    static constexpr int kRows = SLOTS * 32;
+    static constexpr int kDepth = (196608 / (kRows * 16)) < 8 ? 8 : ((196608 / (kRows * 16)) > 64 ? 64 : 196608 / (kRows * 16));
+    static constexpr size_t kSmem = (size_t)kDepth * kRows * 16 + 2 * kDepth * sizeof(uint64_t);
+};
+
+// Warp 0 solves; warp 1 is the producer: it refills ring slot b % kDepth with column
+// b + kDepth of Tt once warp 0 has released it (empty barrier), so the solver's per-column
+// work is a barrier wait, the division, one broadcast and its row updates.
+template <int SLOTS>
+__global__ void __launch_bounds__(64) k_eim_solve_w(EimArgs a, int l) {
+    using G = EimRing<SLOTS>;
+    extern __shared__ __align__(128) unsigned char sm[];
+    double2 *ring = reinterpret_cast<double2 *>(sm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)G::kDepth * G::kRows * 16), *empty = full + G::kDepth;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t col_bytes = (uint32_t)l * 16u;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < G::kDepth; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {  // producer
+        if (lane == 0) {
+            for (int b = 0; b < l; b++) {
+                const int slot = b % G::kDepth;
+                if (b >= G::kDepth) mbar_wait(&empty[slot], (uint32_t)((b / G::kDepth - 1) & 1));
+                mbar_arrive_expect_tx(&full[slot], col_bytes);
+                bulk_g2s(ring + (size_t)slot * G::kRows, a.Tt + (long long)b * a.k, col_bytes, &full[slot]);
+            }
+        }
+        return;
+    }
+    double2 v[SLOTS], td[SLOTS];
+    double dd[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; s++) {
+        const int r = s * 32 + lane;
+        v[s] = make_double2(0.0, 0.0);
+        td[s] = make_double2(1.0, 0.0);
+        if (r < l) {
+            v[s] = load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]);   // rhs q_l(p_r)
+            td[s] = a.Tt[(long long)r * a.k + r];
+        }
+        dd[s] = fma(td[s].x, td[s].x, td[s].y * td[s].y);
+    }
+    // b = sb * 32 + bl: the slot of row b is the compile-time sb, so no register selects.
+    // Only the owner lane divides: a lane dividing a zero (a padding row) would take the
+    // division's slow path (~1,000 clocks) and hold up the warp (scripts/chain_probe.cu).
+#pragma unroll
+    for (int sb = 0; sb < SLOTS; sb++) {
+        const int bl_end = l - sb * 32 < 32 ? l - sb * 32 : 32;
+#pragma unroll 1
+        for (int bl = 0; bl < bl_end; bl++) {
+            const int b = sb * 32 + bl, slot = b % G::kDepth;
+            double cx = 0.0, cy = 0.0;
+            if (lane == bl) {
+                cx = fma(v[sb].x, td[sb].x, v[sb].y * td[sb].y) / dd[sb];   // cdiv(v_b, T_bb)
+                cy = fma(v[sb].y, td[sb].x, -(v[sb].x * td[sb].y)) / dd[sb];
+                a.c[b] = make_double2(cx, cy);
+            }
+            const double2 cb = make_double2(__shfl_sync(0xffffffffu, cx, bl), __shfl_sync(0xffffffffu, cy, bl));
+            mbar_wait(&full[slot], (uint32_t)((b / G::kDepth) & 1));
+            const double2 *col = ring + (size_t)slot * G::kRows;
+#pragma unroll
+            for (int s = sb; s < SLOTS; s++) {
+                const int r = s * 32 + lane;
+                if (r > b && r < l) v[s] = cmsub(v[s], cb, col[r]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);   // every read of the slot has been used
+        }
+    }
+}
+
+// xi_l over all rows with a ring of kEimU loads in flight per thread (one row per thread, the
+// xi_b of row i consumed in increasing b: the oracle's sequential sum), maxloc as k_eim_residual.
+constexpr int kEimU = 32;
+constexpr int kEimThreadsW = 64;
+
+__global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int l) {
+    __shared__ double s_m[kEimThreadsW / 32];
+    __shared__ long long s_j[kEimThreadsW / 32];
+    __shared__ int s_last;
+    extern __shared__ double2 s_c[];  // c_0 .. c_{l-1}
+    for (int b = threadIdx.x; b < l; b += blockDim.x) s_c[b] = a.c[b];
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const bool mine = i < a.N;
+    double2 xr[kEimU];
+#pragma unroll
+    for (int t = 0; t < kEimU; t++) xr[t] = (mine && t < l) ? a.Xi[(long long)t * a.N + i] : make_double2(0.0, 0.0);
+    double2 x = mine ? load_q(a.Q, a.ldq_v, a.cplx, l, i) : make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int b0 = 0; b0 < l; b0 += kEimU) {
+#pragma unroll
+        for (int t = 0; t < kEimU; t++) {
+            const int b = b0 + t, bn = b + kEimU;
+            const double2 xi = xr[t];
+            xr[t] = (mine && bn < l) ? a.Xi[(long long)bn * a.N + i] : make_double2(0.0, 0.0);
+            if (b < l) x = cmsub(x, s_c[b], xi);
+        }
+    }
+    double bm = -1.0;
+    long long bj = 0x7fffffffffffffffLL;
+    if (mine) {
+        a.Xi[(long long)l * a.N + i] = x;
+        bm = fma(x.x, x.x, x.y * x.y);
+        bj = i;
+    }
+    for (int h = 16; h >= 1; h >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+        const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+        if (rec_better(om, oj, bm, bj)) {
+            bm = om;
+            bj = oj;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_m[threadIdx.x >> 5] = bm;
+        s_j[threadIdx.x >> 5] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kEimThreadsW / 32; w++)
+            if (rec_better(s_m[w], s_j[w], bm, bj)) {
+                bm = s_m[w];
+                bj = s_j[w];
+            }
+        a.bm[blockIdx.x] = bm;
+        a.bj[blockIdx.x] = bj;
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < 32) {  // one warp reduces the per-block records
+        bm = -1.0;
+        bj = 0x7fffffffffffffffLL;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+            const double m = __ldcg(&a.bm[b]);
+            const long long j = __ldcg(&a.bj[b]);
+            if (rec_better(m, j, bm, bj)) {
+                bm = m;
+                bj = j;
+            }
+        }
+        for (int h = 16; h >= 1; h >>= 1) {
+            const double om = __shfl_xor_sync(0xffffffffu, bm, h);
+            const long long oj = __shfl_xor_sync(0xffffffffu, bj, h);
+            if (rec_better(om, oj, bm, bj)) {
+                bm = om;
+                bj = oj;
+            }
+        }
+        if (threadIdx.x == 0) {
+            *a.ticket = 0u;
+            if (!(bm > 0.0)) {
+                *a.status = 1;
+                bj = 0;
+            }
+            a.nodes[l] = bj;
+            s_j[0] = bj;
+        }
+    }
+    __syncthreads();
+    const long long p = s_j[0];
+    for (int b = threadIdx.x; b <= l; b += blockDim.x) {
+        const double2 t = __ldcg(&a.Xi[(long long)b * a.N + p]);
+        a.T[(long long)l * a.k + b] = t;
+        a.Tt[(long long)b * a.k + l] = t;
+    }
+}
+
+template <int SLOTS>
+static cudaError_t launch_solve_w(const EimArgs &a, int l, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_eim_solve_w<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)EimRing<SLOTS>::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_eim_solve_w<SLOTS><<<1, 64, EimRing<SLOTS>::kSmem, s>>>(a, l);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_solve(const EimArgs &a, int l, cudaStream_t s) {
+    const int slots = (l + 31) / 32;
+    if (slots <= 1) return launch_solve_w<1>(a, l, s);
+    if (slots <= 2) return launch_solve_w<2>(a, l, s);
+    if (slots <= 4) return launch_solve_w<4>(a, l, s);
+    if (slots <= 6) return launch_solve_w<6>(a, l, s);
+    if (slots <= 8) return launch_solve_w<8>(a, l, s);
+    if (slots <= 10) return launch_solve_w<10>(a, l, s);
+    if (slots <= 12) return launch_solve_w<12>(a, l, s);
+    if (slots <= 16) return launch_solve_w<16>(a, l, s);
+    if (slots <= 24) return launch_solve_w<24>(a, l, s);
+    return launch_solve_w<32>(a, l, s);
 }
 
 // B_ab = q_b(p_a), column-major k x k (the EIM node matrix).
@@ -194,6 +413,7 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
                     int *status_d, cudaStream_t s) {
     if (k < 1 || k > 1024) return cudaErrorInvalidValue;
     const int blocks = (int)((N + kEimThreads - 1) / kEimThreads < 296 ? (N + kEimThreads - 1) / kEimThreads : 296);
+    const long long nrec = std::max<long long>(blocks, (N + 63) / 64);   // per-block maxloc records
     EimArgs a{};
     a.Q = Q;
     a.ldq_v = ldq_v;
@@ -204,20 +424,32 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     a.status = status_d;
     cudaError_t e = dmalloc(&a.Xi, sizeof(double2) * (size_t)k * N);
     if (e == cudaSuccess) e = dmalloc(&a.T, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = dmalloc(&a.Tt, sizeof(double2) * (size_t)k * k);
     if (e == cudaSuccess) e = dmalloc(&a.c, sizeof(double2) * k);
-    if (e == cudaSuccess) e = dmalloc(&a.bm, sizeof(double) * blocks);
-    if (e == cudaSuccess) e = dmalloc(&a.bj, sizeof(long long) * blocks);
+    if (e == cudaSuccess) e = dmalloc(&a.bm, sizeof(double) * nrec);
+    if (e == cudaSuccess) e = dmalloc(&a.bj, sizeof(long long) * nrec);
     if (e == cudaSuccess) e = dmalloc(&a.ticket, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(status_d, 0, sizeof(int), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.c, 0, sizeof(double2) * k, s);
+    // RBG_EIM=block: the first version (one CTA of up to 1024 threads with a barrier per
+    // column; 128-thread residual blocks with batches of 16 loads); same bits
+    const char *ev = getenv("RBG_EIM");
+    const bool v1 = ev && !strcmp(ev, "block");
+    const int blocks_w = (int)((N + kEimThreadsW - 1) / kEimThreadsW);
     for (int l = 0; l < k && e == cudaSuccess; l++) {
         if (l > 0) {
-            k_eim_solve<<<1, (l + 31) / 32 * 32, 0, s>>>(a, l);
-            e = cudaGetLastError();
+            if (v1) {
+                k_eim_solve<<<1, (l + 31) / 32 * 32, 0, s>>>(a, l);
+                e = cudaGetLastError();
+            } else {
+                e = launch_solve(a, l, s);
+            }
         }
         if (e == cudaSuccess) {
-            k_eim_residual<<<blocks, kEimThreads, sizeof(double2) * (size_t)(l > 0 ? l : 1), s>>>(a, l);
+            const size_t sh = sizeof(double2) * (size_t)(l > 0 ? l : 1);
+            if (v1) k_eim_residual<<<blocks, kEimThreads, sh, s>>>(a, l);
+            else k_eim_residual_w<<<blocks_w, kEimThreadsW, sh, s>>>(a, l);
             e = cudaGetLastError();
         }
     }
@@ -228,6 +460,7 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     dfree(a.Xi);
     dfree(a.T);
+    dfree(a.Tt);
     dfree(a.c);
     dfree(a.bm);
     dfree(a.bj);

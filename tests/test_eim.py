@@ -53,14 +53,22 @@ def test_degenerate_basis(orc):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["cfg1", "cfg4", "cfg0"])
-def test_gpu_eim_bit_exact(orc, case):
+@pytest.mark.parametrize("case", ["cfg1", "cfg4", "cfg0", "cfg4_k336", "gauss_k600"])
+def test_gpu_eim_bit_exact(orc, monkeypatch, case):
+    """GPU EIM nodes and node matrix equal the oracle's bit for bit, for the warp-level
+    forward substitution (1..32 register slots per lane: k up to 600 here) and for the first
+    block-barrier version (RBG_EIM=block)."""
     from paper_1805_06124_b200 import rbg
     if case == "cfg1":
         S, w, tol, k_max = inputs.config1(M=3000, N=2000)
         k_max = 120
     elif case == "cfg4":
         S, w, tol, k_max, _ = inputs.config4(M=4096, N=1024, r=256)
+    elif case == "cfg4_k336":
+        S, w, tol, k_max, _ = inputs.config4(M=2048, N=1024, r=400)   # RANK stop at k = 336
+    elif case == "gauss_k600":
+        rng = np.random.default_rng(600)
+        S, w, tol, k_max = rng.standard_normal((700, 1031)), rng.uniform(0.5, 1.5, 1031), 0.0, 600
     else:
         S, w, tol, k_max = inputs.config0()
     res = orc.greedy(S, w, tol, k_max)
@@ -68,5 +76,9 @@ def test_gpu_eim_bit_exact(orc, case):
     with rbg.Context(S, w, tol, k_max) as ctx:
         ctx.run()
         nodes, B = ctx.eim()
+        monkeypatch.setenv("RBG_EIM", "block")
+        nodes1, B1 = ctx.eim()
     np.testing.assert_array_equal(nodes, nodes_o)
     np.testing.assert_array_equal(B, B_o)
+    np.testing.assert_array_equal(nodes1, nodes_o)
+    np.testing.assert_array_equal(B1, B_o)
