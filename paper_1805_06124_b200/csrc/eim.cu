@@ -11,6 +11,9 @@
 // column (a barrier per column, rows in parallel -- the same per-row DAG as the row-wise
 // sequential sum), then a grid over the N rows forms xi_l, |xi_l|^2 and a deterministic
 // maxloc (last-block-done), and gathers row l of T.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -190,86 +193,115 @@ __global__ void __launch_bounds__(kEimThreads) k_eim_residual(EimArgs a, int l) 
 }
 
 // ---- warp-level forward substitution (default) -----------------------------------------
-// One warp; row a of the system lives in lane a % 32, register slot a / 32.  Per column b:
-// the owner of row b forms c_b = v_b / T_bb (den of T_bb precomputed: the same two IEEE
-// divisions as cdiv), one shuffle broadcasts it, and every lane subtracts c_b T_ab from its
-// rows a > b -- right-looking, so each row still receives its updates in increasing b, the
-// oracle's sequential sum.  Column b of T (contiguous in the column-major copy Tt) arrives in
-// a shared-memory ring through cp.async.bulk, kRing columns ahead.
-template <int SLOTS>
-struct EimRing {
-    static constexpr int kRows = SLOTS * 32;
-    static constexpr int kDepth = (196608 / (kRows * 16)) < 8 ? 8 : ((196608 / (kRows * 16)) > 64 ? 64 : 196608 / (kRows * 16));
-    static constexpr size_t kSmem = (size_t)kDepth * kRows * 16 + 2 * kDepth * sizeof(uint64_t);
-};
+// One solver warp; row a lives in lane a % 32, register slot a / 32.  Blocked right-looking
+// substitution, 32 columns b at a time (block sb = the columns whose rows are slot sb):
+//  * phase A (the serial chain): for b in the block, c_b = v_b / T_bb from the owner lane's
+//    numerators, the real and imaginary quotients divided by lanes 0 and 1 at once (a
+//    division of an exact zero is skipped: it would take the ~1,000-clock slow path,
+//    scripts/chain_probe.cu), two shuffles broadcast it and the lanes update slot sb's rows;
+//  * phase B (no per-column dependency): the rows of each later slot receive the block's 32
+//    updates in increasing b.
+// Every row still receives its updates in increasing b -- the oracle's sequential sum -- so
+// the bits are those of the unblocked substitution.  T arrives as 32 x 32 tiles of the
+// column-major copy Tt (tile (sb, s) = columns of block sb, rows of slot s), one 2D TMA box
+// each, in consumption order, through a shared-memory ring filled by a producer warp.
+constexpr int kEimRing = 8;                  // 16 KB tiles
+constexpr size_t kEimTile = 32 * 32 * 16;
+constexpr size_t kEimSmem = kEimRing * kEimTile + 2 * kEimRing * sizeof(uint64_t) + 32 * sizeof(double2);
 
-// Warp 0 solves; warp 1 is the producer: it refills ring slot b % kDepth with column
-// b + kDepth of Tt once warp 0 has released it (empty barrier), so the solver's per-column
-// work is a barrier wait, the division, one broadcast and its row updates.
+__device__ __forceinline__ void tma_tile_g2s(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int SLOTS>
-__global__ void __launch_bounds__(64) k_eim_solve_w(EimArgs a, int l) {
-    using G = EimRing<SLOTS>;
-    extern __shared__ __align__(128) unsigned char sm[];
-    double2 *ring = reinterpret_cast<double2 *>(sm);
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)G::kDepth * G::kRows * 16), *empty = full + G::kDepth;
+__global__ void __launch_bounds__(64) k_eim_solve_w(EimArgs a, int l, const __grid_constant__ CUtensorMap tmT) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const double2(*ring)[32][32] = reinterpret_cast<const double2(*)[32][32]>(sm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + kEimRing * kEimTile), *empty = full + kEimRing;
+    double2 *s_c = reinterpret_cast<double2 *>(empty + kEimRing);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t col_bytes = (uint32_t)l * 16u;
+    const int nblk = (l + 31) / 32;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < G::kDepth; i++) {
+        for (int i = 0; i < kEimRing; i++) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
     }
     __syncthreads();
-    if (warp == 1) {  // producer
+    if (warp == 1) {  // producer: tiles (sb, s), s = sb..nblk-1, in the solver's order
         if (lane == 0) {
-            for (int b = 0; b < l; b++) {
-                const int slot = b % G::kDepth;
-                if (b >= G::kDepth) mbar_wait(&empty[slot], (uint32_t)((b / G::kDepth - 1) & 1));
-                mbar_arrive_expect_tx(&full[slot], col_bytes);
-                bulk_g2s(ring + (size_t)slot * G::kRows, a.Tt + (long long)b * a.k, col_bytes, &full[slot]);
-            }
+            int n = 0;
+            for (int sb = 0; sb < nblk; sb++)
+                for (int s = sb; s < nblk; s++, n++) {
+                    const int slot = n % kEimRing;
+                    if (n >= kEimRing) mbar_wait(&empty[slot], (uint32_t)((n / kEimRing - 1) & 1));
+                    mbar_arrive_expect_tx(&full[slot], (uint32_t)kEimTile);
+                    // x = row offset in doubles (2 per complex row), y = column b
+                    tma_tile_g2s((void *)&ring[slot][0][0], &tmT, s * 64, sb * 32, &full[slot]);
+                }
         }
         return;
     }
-    double2 v[SLOTS], td[SLOTS];
-    double dd[SLOTS];
+    double2 v[SLOTS];
 #pragma unroll
     for (int s = 0; s < SLOTS; s++) {
         const int r = s * 32 + lane;
-        v[s] = make_double2(0.0, 0.0);
-        td[s] = make_double2(1.0, 0.0);
-        if (r < l) {
-            v[s] = load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]);   // rhs q_l(p_r)
-            td[s] = a.Tt[(long long)r * a.k + r];
-        }
-        dd[s] = fma(td[s].x, td[s].x, td[s].y * td[s].y);
+        v[s] = r < l ? load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]) : make_double2(0.0, 0.0);   // q_l(p_r)
     }
-    // b = sb * 32 + bl: the slot of row b is the compile-time sb, so no register selects.
-    // Only the owner lane divides: a lane dividing a zero (a padding row) would take the
-    // division's slow path (~1,000 clocks) and hold up the warp (scripts/chain_probe.cu).
+    int n = 0;   // tiles consumed
 #pragma unroll
     for (int sb = 0; sb < SLOTS; sb++) {
-        const int bl_end = l - sb * 32 < 32 ? l - sb * 32 : 32;
+        if (sb < nblk) {
+            const int b0 = sb * 32, bl_end = l - b0 < 32 ? l - b0 : 32;
+            const int r = b0 + lane;
+            const double2 td = r < l ? a.Tt[(long long)r * a.k + r] : make_double2(1.0, 0.0);
+            const double dd = fma(td.x, td.x, td.y * td.y);
+            // phase A on tile (sb, sb)
+            int slot = n % kEimRing;
+            mbar_wait(&full[slot], (uint32_t)((n / kEimRing) & 1));
 #pragma unroll 1
-        for (int bl = 0; bl < bl_end; bl++) {
-            const int b = sb * 32 + bl, slot = b % G::kDepth;
-            double cx = 0.0, cy = 0.0;
-            if (lane == bl) {
-                cx = fma(v[sb].x, td[sb].x, v[sb].y * td[sb].y) / dd[sb];   // cdiv(v_b, T_bb)
-                cy = fma(v[sb].y, td[sb].x, -(v[sb].x * td[sb].y)) / dd[sb];
-                a.c[b] = make_double2(cx, cy);
-            }
-            const double2 cb = make_double2(__shfl_sync(0xffffffffu, cx, bl), __shfl_sync(0xffffffffu, cy, bl));
-            mbar_wait(&full[slot], (uint32_t)((b / G::kDepth) & 1));
-            const double2 *col = ring + (size_t)slot * G::kRows;
-#pragma unroll
-            for (int s = sb; s < SLOTS; s++) {
-                const int r = s * 32 + lane;
-                if (r > b && r < l) v[s] = cmsub(v[s], cb, col[r]);
+            for (int bl = 0; bl < bl_end; bl++) {
+                // cdiv(v_b, T_bb): the owner's two numerators and den go to lanes 0 and 1, which
+                // divide at the same time (one division latency on the chain, not two); an
+                // exactly zero numerator is not divided (0 / den = +-0 exactly, den > 0), as it
+                // would take the division's slow path (real data: every imaginary part)
+                const double n1 = __shfl_sync(0xffffffffu, fma(v[sb].x, td.x, v[sb].y * td.y), bl);
+                const double n2 = __shfl_sync(0xffffffffu, fma(v[sb].y, td.x, -(v[sb].x * td.y)), bl);
+                const double den = __shfl_sync(0xffffffffu, dd, bl);
+                double q = 0.0;
+                if (lane < 2) {
+                    const double num = lane ? n2 : n1;
+                    q = num == 0.0 ? num : num / den;
+                }
+                const double2 cb = make_double2(__shfl_sync(0xffffffffu, q, 0), __shfl_sync(0xffffffffu, q, 1));
+                if (lane == bl) {
+                    a.c[b0 + bl] = cb;
+                    s_c[bl] = cb;
+                }
+                if (lane > bl && lane < bl_end) v[sb] = cmsub(v[sb], cb, ring[slot][bl][lane]);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);   // every read of the slot has been used
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            n++;
+            // phase B on tiles (sb, s), s > sb
+#pragma unroll
+            for (int s = sb + 1; s < SLOTS; s++) {
+                if (s < nblk) {
+                    slot = n % kEimRing;
+                    mbar_wait(&full[slot], (uint32_t)((n / kEimRing) & 1));
+                    double2 x = v[s];
+#pragma unroll 8
+                    for (int bl = 0; bl < bl_end; bl++) x = cmsub(x, s_c[bl], ring[slot][bl][lane]);
+                    v[s] = x;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[slot]);
+                    n++;
+                }
+            }
         }
     }
 }
@@ -374,30 +406,49 @@ __global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int 
 }
 
 template <int SLOTS>
-static cudaError_t launch_solve_w(const EimArgs &a, int l, cudaStream_t s) {
+static cudaError_t launch_solve_w(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_eim_solve_w<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)EimRing<SLOTS>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(k_eim_solve_w<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEimSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_eim_solve_w<SLOTS><<<1, 64, EimRing<SLOTS>::kSmem, s>>>(a, l);
+    k_eim_solve_w<SLOTS><<<1, 64, kEimSmem, s>>>(a, l, tm);
     return cudaGetLastError();
 }
 
-static cudaError_t launch_solve(const EimArgs &a, int l, cudaStream_t s) {
+static cudaError_t launch_solve(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
     const int slots = (l + 31) / 32;
-    if (slots <= 1) return launch_solve_w<1>(a, l, s);
-    if (slots <= 2) return launch_solve_w<2>(a, l, s);
-    if (slots <= 4) return launch_solve_w<4>(a, l, s);
-    if (slots <= 6) return launch_solve_w<6>(a, l, s);
-    if (slots <= 8) return launch_solve_w<8>(a, l, s);
-    if (slots <= 10) return launch_solve_w<10>(a, l, s);
-    if (slots <= 12) return launch_solve_w<12>(a, l, s);
-    if (slots <= 16) return launch_solve_w<16>(a, l, s);
-    if (slots <= 24) return launch_solve_w<24>(a, l, s);
-    return launch_solve_w<32>(a, l, s);
+    if (slots <= 1) return launch_solve_w<1>(a, l, tm, s);
+    if (slots <= 2) return launch_solve_w<2>(a, l, tm, s);
+    if (slots <= 4) return launch_solve_w<4>(a, l, tm, s);
+    if (slots <= 6) return launch_solve_w<6>(a, l, tm, s);
+    if (slots <= 8) return launch_solve_w<8>(a, l, tm, s);
+    if (slots <= 10) return launch_solve_w<10>(a, l, tm, s);
+    if (slots <= 12) return launch_solve_w<12>(a, l, tm, s);
+    if (slots <= 16) return launch_solve_w<16>(a, l, tm, s);
+    if (slots <= 24) return launch_solve_w<24>(a, l, tm, s);
+    return launch_solve_w<32>(a, l, tm, s);
+}
+
+// 2D view of Tt for the solver's tiles: inner dimension 2k doubles (rows a), outer k columns b.
+static cudaError_t make_tt_map(const EimArgs &a, CUtensorMap *tm) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * a.k), (cuuint64_t)a.k};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.k * 16};
+    const cuuint32_t box[2] = {64, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.Tt, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 // B_ab = q_b(p_a), column-major k x k (the EIM node matrix).
@@ -425,6 +476,9 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     cudaError_t e = dmalloc(&a.Xi, sizeof(double2) * (size_t)k * N);
     if (e == cudaSuccess) e = dmalloc(&a.T, sizeof(double2) * (size_t)k * k);
     if (e == cudaSuccess) e = dmalloc(&a.Tt, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.Tt, 0, sizeof(double2) * (size_t)k * k, s);
+    CUtensorMap tmT;
+    if (e == cudaSuccess) e = make_tt_map(a, &tmT);
     if (e == cudaSuccess) e = dmalloc(&a.c, sizeof(double2) * k);
     if (e == cudaSuccess) e = dmalloc(&a.bm, sizeof(double) * nrec);
     if (e == cudaSuccess) e = dmalloc(&a.bj, sizeof(long long) * nrec);
@@ -443,7 +497,7 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
                 k_eim_solve<<<1, (l + 31) / 32 * 32, 0, s>>>(a, l);
                 e = cudaGetLastError();
             } else {
-                e = launch_solve(a, l, s);
+                e = launch_solve(a, l, tmT, s);
             }
         }
         if (e == cudaSuccess) {

@@ -12,7 +12,15 @@ __global__ void chain(double *out, long long *cyc, int n, double seed) {
     long long t0 = clock64();
     for (int b = 0; b < n; b++) {
         double cx, cy;
-        if (MODE == 0 || MODE == 2) {      // IEEE division (the oracle's cdiv)
+        if (MODE == 3 || MODE == 4) {      // owner-only division (divergent branch)
+            cx = 0.0;
+            cy = 0.0;
+            if (lane == (b & 31)) {
+                cx = fma(vx, tx, vy * ty) / dd;
+                cy = fma(vy, tx, -(vx * ty)) / dd;
+                if (MODE == 4) out[32 + b] = cx + cy;
+            }
+        } else if (MODE == 0 || MODE == 2) {      // IEEE division (the oracle's cdiv)
             cx = fma(vx, tx, vy * ty) / dd;
             cy = fma(vy, tx, -(vx * ty)) / dd;
         } else {                           // multiply instead (timing only)
@@ -36,10 +44,10 @@ __global__ void chain(double *out, long long *cyc, int n, double seed) {
 int main() {
     double *out;
     long long *cyc, h;
-    cudaMalloc(&out, 32 * sizeof(double));
+    cudaMalloc(&out, (32 + 8192) * sizeof(double));
     cudaMalloc(&cyc, sizeof(long long));
     const int n = 4096;
-    const char *names[3] = {"div+shfl", "mul+shfl", "div only"};
+    const char *names[5] = {"div+shfl", "mul+shfl", "div only", "owner div", "owner div+st"};
     for (int rep = 0; rep < 2; rep++) {
         chain<0><<<1, 32>>>(out, cyc, n, 1e-3);
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
@@ -50,6 +58,12 @@ int main() {
         chain<2><<<1, 32>>>(out, cyc, n, 1e-3);
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         if (rep) printf("%-10s %.1f clk/step\n", names[2], (double)h / n);
+        chain<3><<<1, 32>>>(out, cyc, n, 1e-3);
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        if (rep) printf("%-10s %.1f clk/step\n", names[3], (double)h / n);
+        chain<4><<<1, 32>>>(out, cyc, n, 1e-3);
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        if (rep) printf("%-10s %.1f clk/step\n", names[4], (double)h / n);
     }
     return 0;
 }
