@@ -228,3 +228,37 @@ def test_gpu_coefficient_block_bit_exact(orc, monkeypatch, cplx, N, M_v, k):
     np.testing.assert_array_equal(C, C_o)
     np.testing.assert_array_equal(err_p, err)
     np.testing.assert_array_equal(C_p, C)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cplx,N,pad", [
+    (True, 400, 0),     # complex: column pitch = the padded layout -> read in place
+    (False, 256, 0),    # real, N even -> read in place
+    (False, 257, 0),    # real, N odd: the padded layout has one more row -> copied
+    (True, 400, 3),     # row stride N + 3 -> copied
+])
+def test_gpu_validate_device_blocks(orc, cplx, N, pad):
+    """A CUDA-tensor block is validated in place when its layout is the library's padded one
+    and copied otherwise; both give the oracle's bits, and a non-finite entry of a device
+    block is reported (ENONFINITE) in either case."""
+    import torch
+
+    from paper_1805_06124_b200 import rbg
+    rng = np.random.default_rng(N + pad)
+    S = rng.standard_normal((80, N)) + (1j * rng.standard_normal((80, N)) if cplx else 0)
+    V = rng.standard_normal((45, N)) + (1j * rng.standard_normal((45, N)) if cplx else 0)
+    w = rng.uniform(0.5, 1.5, N)
+    r = orc.greedy(S, w, 0.0, 30)
+    e_o, C_o, _ = orc.validate(r.Q, V, w)
+    dt = torch.complex128 if cplx else torch.float64
+    buf = torch.zeros((45, N + pad), dtype=dt, device="cuda")
+    buf[:, :N] = torch.from_numpy(V).to("cuda")
+    Vd = buf[:, :N]
+    with rbg.Context(S, w, 0.0, 30) as ctx:
+        ctx.run()
+        err, C = ctx.validate(Vd, coeffs=True)
+        np.testing.assert_array_equal(err, e_o)
+        np.testing.assert_array_equal(C, C_o)
+        buf[7, 3] = float("nan")
+        with pytest.raises(rbg.RbgError, match="ENONFINITE"):
+            ctx.validate(Vd)
