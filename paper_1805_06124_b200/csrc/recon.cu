@@ -301,6 +301,45 @@ constexpr int kJL = 2 * kJB;   // local problem size (one warp wide)
 __device__ __forceinline__ int blk_idx(int I, int J, int a) { return a < kJB ? I * kJB + a : J * kJB + (a - kJB); }
 
 constexpr int kBjThreads = 1024;  // 32 warps per SM: P2/P3 are latency-bound row/column passes
+constexpr int kJLoc = (kJL / 2) * (kJL / 2);   // threads of a local round: one per 2 x 2 block
+
+// Rotation of the local problem's pair (p, q): a = A_pp, b = A_qq (real), c = A_pq.  The
+// classical formulas (tau = (b - a) / 2|c|, t = sgn(tau) / (|tau| + sqrt(1 + tau^2)),
+// cs = 1 / sqrt(1 + t^2), sn = t cs, e = c / |c|) evaluated with three reciprocal square roots
+// instead of a chain of square roots and divisions: with r1 = 1 / sqrt(1 + tau^2),
+// cos 2theta = |tau| r1 and sin 2theta = sgn(tau) r1, and the half-angle forms give
+// cs = sqrt(h), sn = sin 2theta / (2 sqrt(h)), h = (1 + cos 2theta) / 2 in [1/2, 1] (no
+// cancellation).  Each result is within a few ulps of the classical one, which is all the
+// Jacobi iteration needs (a rotation orthogonal to working precision); the reconstruction is
+// checked against the oracle to a tolerance, not bit for bit (R30).
+__device__ __forceinline__ Rot rot_params(double a, double b, double2 c, int p, int q) {
+    Rot R;
+    R.p = p;
+    R.q = q;
+    const double ac2 = fma(c.x, c.x, c.y * c.y);
+    if (ac2 == 0.0) {
+        R.cs = 1.0;
+        R.sn = 0.0;
+        R.er = 1.0;
+        R.ei = 0.0;
+        return R;
+    }
+    const double ri = rsqrt(ac2);                 // 1 / |c|
+    R.er = c.x * ri;
+    R.ei = c.y * ri;
+    const double tau = 0.5 * (b - a) * ri;
+    if (fabs(tau) > 1e150) {                      // negligible rotation: theta = 1 / (2 tau)
+        R.cs = 1.0;
+        R.sn = 0.5 / tau;
+        return R;
+    }
+    const double r1 = rsqrt(fma(tau, tau, 1.0));
+    const double h = 0.5 * fma(fabs(tau), r1, 1.0);
+    const double rh = rsqrt(h);
+    R.cs = h * rh;
+    R.sn = (tau >= 0.0 ? r1 : -r1) * 0.5 * rh;
+    return R;
+}
 
 __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, int kp, double2 *Us,
                                                  unsigned long long *flags, int *sweeps_out,
@@ -339,32 +378,16 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
                         }
                     }
                 }
+                // the local rounds run on the first 256 threads only (one per 2 x 2 block of the
+                // update), synchronised by a named barrier: cheaper than a 1,024-thread barrier
+                if (tid < kJLoc)
                 for (int lr = 0; lr < kJL - 1; lr++) {
                     if (tid < kJL / 2) {
                         int p, q;
                         round_pair(lr, tid, kJL, p, q);
-                        const double a = A[p][p].x, b = A[q][q].x;
-                        const double2 c = A[p][q];
-                        const double ac = sqrt(c.x * c.x + c.y * c.y);
-                        Rot R;
-                        R.p = p;
-                        R.q = q;
-                        if (ac == 0.0) {
-                            R.cs = 1.0;
-                            R.sn = 0.0;
-                            R.er = 1.0;
-                            R.ei = 0.0;
-                        } else {
-                            const double tau = (b - a) / (2.0 * ac);
-                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                            R.cs = 1.0 / sqrt(1.0 + t * t);
-                            R.sn = t * R.cs;
-                            R.er = c.x / ac;
-                            R.ei = c.y / ac;
-                        }
-                        srot[tid] = R;
+                        srot[tid] = rot_params(A[p][p].x, A[q][q].x, A[p][q], p, q);
                     }
-                    __syncthreads();
+                    asm volatile("bar.sync 1, %0;" ::"r"(kJLoc) : "memory");
                     // A <- J^H A J and U <- U J, fused: the rotation pairs partition the indices,
                     // so thread (i, j) owns the 2 x 2 blocks (rows of pair i, columns of pair j)
                     // of A and U -- it reads all four entries before writing them and no other
@@ -400,8 +423,9 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
                             A[Ri.q][col] = nq;
                         }
                     }
-                    __syncthreads();
+                    asm volatile("bar.sync 1, %0;" ::"r"(kJLoc) : "memory");
                 }
+                __syncthreads();
                 double2 *Up = Us + (size_t)pr * kJL * kJL;   // column-major 32 x 32
                 for (int e = tid; e < kJL * kJL; e += blockDim.x) Up[e] = U[e % kJL][e / kJL];
                 __syncthreads();
