@@ -7,15 +7,17 @@
 // asymptotic FLOP count of O(2MN)" -- it streams all of S once and is HBM-bound.
 //
 // B200 design:
-//  * one CTA per SM (persistent over a contiguous block of columns), 16 warps;
+//  * one CTA per SM, 16 warps; the default kernel (k_sweep_dyn) hands columns to warps
+//    dynamically (a grid-wide counter claimed one column ahead), the static-block variants
+//    (k_sweep_ring, k_sweep) give each CTA a contiguous block of columns;
 //  * the weighted basis vector e~_k = w o q_k (N x 16 B, 160 KB at N = 10,000 complex) is
 //    staged once per CTA into shared memory with TMA bulk copies (cp.async.bulk) on an
 //    mbarrier;
 //  * one warp per column (L_S = 32 lanes): lane l owns the 16-byte vectors u = l (mod 32)
 //    of the column, streamed with 16-byte ld.global.nc.L1::no_allocate + L2 evict-first
-//    through a register ring of U loads in flight per lane (U = 12 on the 10,000-row case:
-//    ~96 KB outstanding per SM, the read-stream ceiling of scripts/hbm_probe.cu),
-//    accumulated with explicit fma() in increasing u;
+//    through a register ring of U loads in flight per lane (U = 16 on the 10,000-row case:
+//    128 KB outstanding per SM; the ring runs across column boundaries), accumulated with
+//    explicit fma() in increasing u;
 //  * xor-butterfly with ascending offsets (= the pairwise lane tree of the CAC);
 //  * lane 0 writes R(k, j), updates r2_j in place, and the warp keeps its maxloc;
 //  * per-CTA maxloc records, the last CTA to finish (atomic ticket) reduces them with the
