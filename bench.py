@@ -334,6 +334,9 @@ def run_ours(a):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if pk.get("hbm_gbs") else "fallback 6.65 TB/s",
             "traffic": ncu_traffic(), "algorithmic_bytes_per_launch": bytes_sweep,
             "sweep_ms_avg": sweep_avg_s * 1e3,
+            # SURVEY 8(d) quotes the median sweep over iterations k >= 3
+            "sweep_ms_median": float(np.median(sw)),
+            "achieved_at_median_gbs": bytes_sweep / (float(np.median(sw)) / 1e3) / 1e9,
             "share_of_step": float(np.sum(sw) / ms),
             # the same achieved bandwidth against the datasheet figure and the
             # measured read-only ceiling of the same access pattern
