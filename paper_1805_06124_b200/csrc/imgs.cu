@@ -126,18 +126,18 @@ struct ClusterReducerPre {
         if (sub) sub[2] = clock64();
         phase ^= 1u << par;
         if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[par], CTAS * 16);  // re-arm for n+2
-        // the tree over the CTAS CTA partials: lane l holds leaf l mod CTAS, xor-butterfly with
-        // ascending offsets inside each group of CTAS lanes (IEEE + is commutative: every lane
-        // ends with the same bits)
-        const double2 x0 = slots[par][lane % CTAS];
-        double x = x0.x, y = x0.y;
+        // the tree over the CTAS CTA partials, evaluated by every thread from shared memory
+        // (broadcast reads): leaf l = slots[par][l], pairwise with ascending offsets -- the
+        // nodes of the former xor-butterfly, without its dependent shuffles
+        double2 c[CTAS];
 #pragma unroll
-        for (int h = 1; h < CTAS; h <<= 1) {
-            x = x + __shfl_xor_sync(0xffffffffu, x, h);
-            y = y + __shfl_xor_sync(0xffffffffu, y, h);
-        }
+        for (int l = 0; l < CTAS; l++) c[l] = slots[par][l];
+#pragma unroll
+        for (int h = 1; h < CTAS; h <<= 1)
+#pragma unroll
+            for (int l = 0; l < CTAS; l += 2 * h) c[l] = make_double2(c[l].x + c[l + h].x, c[l].y + c[l + h].y);
         par ^= 1;
-        return make_double2(x, y);
+        return c[0];
     }
 };
 
