@@ -407,12 +407,9 @@ __global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int 
 
 template <int SLOTS>
 static cudaError_t launch_solve_w(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_eim_solve_w<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEimSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // set on every call: the attribute is per device, and a process may drive several
+    cudaError_t e = cudaFuncSetAttribute(k_eim_solve_w<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEimSmem);
+    if (e != cudaSuccess) return e;
     k_eim_solve_w<SLOTS><<<1, 64, kEimSmem, s>>>(a, l, tm);
     return cudaGetLastError();
 }
