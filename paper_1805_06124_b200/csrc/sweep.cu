@@ -659,7 +659,12 @@ static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStre
                                              (int)cfg.smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
+    // no more CTAs than the columns can occupy (one warp per column at least): a small M
+    // does not pay 296 CTAs' staging of e~ and a 296-record maxloc (same bits: the per-column
+    // arithmetic does not depend on the grid and the maxloc is a total order)
+    const long long need = (a.M + kSweepWarps - 1) / kSweepWarps;
+    const int grid = (int)(need < 1 ? 1 : (need < cfg.grid ? need : cfg.grid));
+    kern<<<grid, cfg.threads, cfg.smem, s>>>(a);
     return cudaGetLastError();
 }
 
