@@ -78,6 +78,51 @@ __global__ void __launch_bounds__(T) col_stream_dyn(const double2 *S, long long 
     if (acc == 12345.678) out[0] = acc;
 }
 
+// the same dynamic column stream with a bulk L2 prefetch PF batches (of 32*U vectors) ahead of
+// the register ring, issued by lane 0: DRAM -> L2 traffic in flight not bounded by registers
+template <int T, int U, int PF>
+__global__ void __launch_bounds__(T) col_stream_dyn_pf(const double2 *S, long long nvec, long long M, double *out,
+                                                       unsigned long long *ctr) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long nwg = (long long)gridDim.x * (T / 32);
+    const long long batch = 32 * U;
+    double acc = 0.0;
+    long long c = (long long)blockIdx.x * (T / 32) + warp;
+    unsigned long long raw = 0;
+    if (lane == 0) raw = atomicAdd(ctr, 1ull);
+    while (c < M) {
+        const double2 *col = S + c * nvec;
+        if (lane == 0)
+            for (int p = 0; p < PF; p++) {
+                const long long u0 = p * batch;
+                if (u0 < nvec) {
+                    const long long n = (nvec - u0 < batch ? nvec - u0 : batch) * 16;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col + u0), "r"((unsigned)n) : "memory");
+                }
+            }
+        double2 xa[U];
+#pragma unroll
+        for (int t = 0; t < U; t++) { long long u = t * 32 + lane; xa[t] = u < nvec ? ldnc(col + u) : make_double2(0, 0); }
+        for (long long b = 0; b < nvec; b += batch) {
+            if (lane == 0) {
+                const long long u0 = b + (long long)PF * batch;
+                if (u0 < nvec) {
+                    const long long n = (nvec - u0 < batch ? nvec - u0 : batch) * 16;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col + u0), "r"((unsigned)n) : "memory");
+                }
+            }
+            double2 xb[U];
+#pragma unroll
+            for (int t = 0; t < U; t++) { long long u = b + batch + t * 32 + lane; xb[t] = u < nvec ? ldnc(col + u) : make_double2(0, 0); }
+#pragma unroll
+            for (int t = 0; t < U; t++) { acc = fma(xa[t].x, xa[t].y, acc); xa[t] = xb[t]; }
+        }
+        c = (long long)__shfl_sync(0xffffffffu, raw, 0) + nwg;
+        if (lane == 0) raw = atomicAdd(ctr, 1ull);
+    }
+    if (acc == 12345.678) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t *b, uint32_t n) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
@@ -164,6 +209,13 @@ int main() {
 #define DYN(T, U, OCC) rep("col_stream_dyn T=" #T " U=" #U " ctas/SM=" #OCC, \
         timeit([&] { cudaMemsetAsync(ctr, 0, 8); col_stream_dyn<T, U><<<sms * OCC, T>>>(S, nvec, M, out, ctr); }), bytes);
     DYN(512, 12, 1) DYN(512, 16, 1) DYN(256, 16, 4) DYN(1024, 8, 1)
+#define DYNPF(T, U, PF, OCC) rep("col_stream_dyn_pf T=" #T " U=" #U " PF=" #PF " ctas/SM=" #OCC, \
+        timeit([&] { cudaMemsetAsync(ctr, 0, 8); col_stream_dyn_pf<T, U, PF><<<sms * OCC, T>>>(S, nvec, M, out, ctr); }), bytes);
+    for (int rep2 = 0; rep2 < 2; rep2++) {
+        DYNPF(512, 16, 2, 1) DYNPF(512, 16, 3, 1) DYNPF(512, 12, 3, 1) DYNPF(512, 12, 4, 1) DYNPF(512, 8, 4, 1)
+        DYNPF(512, 8, 6, 1) DYNPF(256, 16, 3, 4)
+        DYN(512, 16, 1) DYN(256, 16, 4)
+    }
 #define TMA(CH, ST, OCC) { \
         auto k = tma_stream<CH, ST>; const int smem = CH * ST; \
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
