@@ -131,6 +131,8 @@ typedef struct rbg_stats {
     double t_imgs_ms;       /* sum of pivot decision + IMGS (T_IMGS)                     */
     double t_total_ms;      /* first event to last event (T_j summed)      */
     double t_gap_ms;        /* launch gaps between iterations (part of C_j)              */
+    int64_t noop_iters;     /* iterations launched after the stop decision (early-exit
+                               kernels; 0 with rbg_run's device loop)                    */
 } rbg_stats;
 
 /* Fill *d with defaults: ld = 0, borrow = 0, w = NULL, device = -1, check_finite = 1,
@@ -173,7 +175,9 @@ rbg_status rbg_result_info(rbg_ctx *ctx, int64_t *k, int64_t *M_loc, rbg_stop *w
 
 /* Outputs (replicated on every rank unless noted).  Host buffers unless on_device. */
 rbg_status rbg_get_pivots(rbg_ctx *ctx, int64_t *out);        /* k global column ids   */
-rbg_status rbg_get_errors(rbg_ctx *ctx, double *out);         /* k+1: err_0 .. err_k   */
+/* errors: err_0 .. err_k (k+1 entries) once the greedy stopped; k entries (err_0 .. err_{k-1})
+ * while it is running or after PEER_TIMEOUT (the decision for err_k never ran).           */
+rbg_status rbg_get_errors(rbg_ctx *ctx, double *out);
 rbg_status rbg_get_nu(rbg_ctx *ctx, int32_t *out);            /* k IMGS sweep counts   */
 rbg_status rbg_get_rdiag(rbg_ctx *ctx, double *out);          /* k IMGS norms R(i,i)   */
 /* Q: N x k column-major, column i at out + i*ldq elements (ldq >= N).                   */
@@ -207,7 +211,9 @@ rbg_status rbg_validate(rbg_ctx *ctx, const void *V, int64_t M_v, int64_t ldv, r
  * single-GPU context.  Their R rows and residuals are computed with the greedy's own
  * arithmetic, the pivot search restarts over all columns and a stopped greedy may continue
  * (rbg_run / rbg_step).  The snapshot matrix becomes library-owned (a borrowed S is copied).
- * ESTATE on sharded contexts (see rbg_add_columns_ex).  Blocking.                          */
+ * ESTATE on sharded contexts (see rbg_add_columns_ex), and on a running greedy (started, no
+ * stop decision yet: the sweep with q_{k-1} is still pending) -- run it to its stop first.
+ * Blocking.                                                                                 */
 rbg_status rbg_add_columns(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem);
 /* Enrichment of a column-sharded context (also valid on one GPU): every rank calls it, in the
  * same round, with its own failing columns (M_f >= 0; F may be NULL when M_f = 0).  They get
@@ -217,14 +223,17 @@ rbg_status rbg_add_columns(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf
  * the ranks before), the result equals one context enriched with the concatenated columns bit
  * for bit.  The pivot search restarts on every rank (its candidate published to the exchange
  * with a new record epoch) and a stopped greedy may continue.  first_gid < 0 and
- * M_global_new <= 0 select the single-GPU defaults (M_global, M_global + M_f).  Blocking.   */
+ * M_global_new <= 0 select the single-GPU defaults (M_global, M_global + M_f).  ESTATE on a
+ * running greedy, as rbg_add_columns.  Blocking.                                            */
 rbg_status rbg_add_columns_ex(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem, int64_t first_gid,
                               int64_t M_global_new);
 
 /* Gram matrix G = R R^H of the k x M coefficient block (k = basis size): k x k Hermitian,
  * column-major with leading dimension ldg >= k, complex (16-byte) entries even for a real
  * dtype.  Summation order: columns in chunks of 4096, each chunk one sequential fma chain,
- * chunks added in order (reading R30).  Single-GPU contexts (ESTATE otherwise).   */
+ * chunks added in order (reading R30).  Single-GPU contexts (ESTATE otherwise).
+ * Like rbg_reconstruct and rbg_gram_fold it reads R rows 0..k-1: ESTATE on a running greedy
+ * (started, no stop decision yet), whose row k-1 is still pending.                        */
 rbg_status rbg_gram(rbg_ctx *ctx, void *G, int64_t ldg, int on_device);
 
 /* Algorithm 4 "Reconstruction": SVD of R(1:k, :) through its Gram

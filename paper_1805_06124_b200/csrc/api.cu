@@ -14,6 +14,7 @@
 // enqueues; steps after the stop decision return immediately on the device.  The cost
 // model T_j = T_pivot + T_IMGS + C_j is measured with CUDA events
 // around the three steps when timing is on.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -67,6 +68,9 @@ void free_ctx(rbg_ctx *c) {
         dfree(c->imgs_trace);
     }
     if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->while_exec) cudaGraphExecDestroy(c->while_exec);
+    if (c->poll_stream) cudaStreamDestroy(c->poll_stream);
+    if (c->poll_h) cudaFreeHost(c->poll_h);
     for (auto &p : c->ev)
         for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
     if (c->nccl) nccl_destroy(c->nccl);
@@ -131,6 +135,8 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     }
     a.peer_epoch = c->epoch;
     a.gid = c->gid;
+    a.cond = c->cond;
+    a.use_cond = c->in_while ? 1 : 0;
     return a;
 }
 
@@ -163,6 +169,8 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     for (int q = 0; q < kMaxPeers; q++) a.peer_send[q] = q < c->world ? c->peer_send[q] : nullptr;
     a.gid = c->gid;
     a.trace = (c->imgs_trace && c->iters == c->trace_iter) ? c->imgs_trace : nullptr;
+    a.cond = c->cond;
+    a.use_cond = c->in_while ? 1 : 0;
     return a;
 }
 
@@ -181,7 +189,8 @@ rbg_status enqueue_local(rbg_ctx *c) {
 rbg_status enqueue_xchg(rbg_ctx *c) {
     NvtxRange range("rbg.exchange");
     if (c->comm == RBG_COMM_PEER) {
-        CU(launch_peer_wait(c->peer_in, c->world, c->st, c->epoch, c->peer_timeout_ns, c->stream));
+        CU(launch_peer_wait(c->peer_in, c->world, c->st, c->epoch, c->peer_timeout_ns, c->cond, c->in_while ? 1 : 0,
+                            c->stream));
         return RBG_OK;
     }
     if (c->comm == RBG_COMM_NCCL) {
@@ -256,6 +265,91 @@ rbg_status enqueue_n(rbg_ctx *c, long long n) {
     return RBG_OK;
 }
 
+// rbg_run's device loop: a graph whose only node is a conditional WHILE node (condition 1 at
+// launch) with one steady-state iteration -- sweep with q_{k-1} [+ exchange wait] + decision and
+// IMGS -- as its body.  The kernels in the body carry the condition handle; the one that
+// records the stop decision, or first finds the greedy stopped, sets it to 0 (loop_exit in
+// common.cuh), so the loop ends after the stopping iteration: no host round trip per
+// iteration and no launches past the stop.  NCCL's collective (its own kernels) and the
+// per-phase timing events stay outside (rbg_run polls then), as does the IMGS debug trace.
+bool while_supported(const rbg_ctx *c) {
+    return !c->while_failed && !c->timing && !c->imgs_trace && (c->comm == RBG_COMM_NONE || c->comm == RBG_COMM_PEER) &&
+           !getenv("RBG_NO_DEVICE_LOOP");
+}
+
+rbg_status build_while(rbg_ctx *c) {
+    if (c->while_exec) return RBG_OK;
+    cudaGraph_t g = nullptr;
+    CU(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &p);
+    cudaGraph_t body = p.conditional.phGraph_out ? p.conditional.phGraph_out[0] : nullptr;
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    rbg_status s = RBG_OK;
+    if (e == cudaSuccess) {
+        c->cond = h;
+        c->in_while = true;
+        s = enqueue_local(c);
+        if (s == RBG_OK) s = enqueue_xchg(c);
+        if (s == RBG_OK) s = enqueue_finish(c);
+        c->in_while = false;
+        cudaGraph_t out = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(c->stream, &out);
+        if (e2 != cudaSuccess) e = e2;
+    }
+    if (e == cudaSuccess && s == RBG_OK) e = cudaGraphInstantiate(&c->while_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (s != RBG_OK) return s;
+    if (e != cudaSuccess) {
+        c->while_exec = nullptr;
+        return fail(RBG_ECUDA, "device loop graph: %s", cudaGetErrorString(e));
+    }
+    return RBG_OK;
+}
+
+// Polled rbg_run (timing mode, NCCL, or no device loop): batches of `graph_batch` (default 16)
+// iterations, one batch in flight ahead; before enqueuing the next batch the host reads the
+// stop flag as of the end of the batch before (side stream, pinned word), so at most two
+// batches run past the stop (as early-exit kernels).
+rbg_status run_polled(rbg_ctx *c) {
+    if (!c->poll_stream) CU(cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking));
+    if (!c->poll_h) CU(cudaHostAlloc(&c->poll_h, sizeof(int), cudaHostAllocDefault));
+    const long long B = c->graph_batch > 0 ? c->graph_batch : 16;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    rbg_status s = RBG_OK;
+    cudaError_t e = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    long long b = 0;
+    bool stopped = false;
+    while (e == cudaSuccess && s == RBG_OK && !stopped && c->iters < c->k_max + 1) {
+        s = enqueue_n(c, std::min<long long>(B, c->k_max + 1 - c->iters));
+        if (s != RBG_OK) break;
+        e = cudaEventRecord(ev[b & 1], c->stream);
+        if (e == cudaSuccess && b > 0) {
+            e = cudaStreamWaitEvent(c->poll_stream, ev[(b - 1) & 1], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(c->poll_h, &c->st->stop, sizeof(int), cudaMemcpyDeviceToHost, c->poll_stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(c->poll_stream);
+            stopped = e == cudaSuccess && *c->poll_h != 0;
+        }
+        b++;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    for (auto &x : ev)
+        if (x) cudaEventDestroy(x);
+    if (s != RBG_OK) return s;
+    if (e != cudaSuccess) return fail(RBG_ECUDA, "rbg_run: %s", cudaGetErrorString(e));
+    return RBG_OK;
+}
+
 rbg_status check_ctx(rbg_ctx *c) {
     if (!c) return fail(RBG_EINVAL, "null context");
     CU(cudaSetDevice(c->device));
@@ -265,6 +359,18 @@ rbg_status check_ctx(rbg_ctx *c) {
 rbg_status read_state(rbg_ctx *c, DevState *h) {
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaMemcpy(h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    return RBG_OK;
+}
+
+// Calls that read R (or change the column set) need every R row 0..k-1 filled: before the
+// first iteration, after a stop decision, or after rbg_add_columns (rows computed for the new
+// columns).  Between rbg_step calls of a running greedy the sweep with q_{k-1} is still
+// pending, i.e. R row k-1 is zero and r2 lacks |c_{k-1,j}|^2.
+rbg_status need_settled(const rbg_ctx *c, const DevState &h, const char *what) {
+    if (c->local_pending) return fail(RBG_ESTATE, "%s inside an EXTERNAL/PEER iteration", what);
+    if (c->started && h.stop == 0 && !c->resume_pending)
+        return fail(RBG_ESTATE, "%s on a running greedy (k=%lld, no stop decision yet): run it to its stop first",
+                    what, h.k);
     return RBG_OK;
 }
 
@@ -636,10 +742,24 @@ rbg_status rbg_run(rbg_ctx *c) {
     TRY(check_ctx(c));
     if (c->comm == RBG_COMM_EXTERNAL) return fail(RBG_ESTATE, "EXTERNAL contexts use rbg_iter_local/finish");
     if (c->comm == RBG_COMM_PEER && !c->peer_connected) return fail(RBG_ESTATE, "PEER context not connected (rbg_peer_connect)");
-    const long long need = c->k_max + 1 - c->iters;
-    if (need > 0) TRY(enqueue_n(c, need));
-    CU(cudaStreamSynchronize(c->stream));
-    return RBG_OK;
+    if (c->local_pending) return fail(RBG_ESTATE, "rbg_run inside an iteration (rbg_iter_local pending)");
+    DevState h;
+    TRY(read_state(c, &h));  // also waits for iterations enqueued by rbg_step
+    if (h.stop || c->iters >= c->k_max + 1) return RBG_OK;
+    if (while_supported(c)) {
+        // sweep 0 (or the restart after rbg_add_columns) is a different kernel: one plain
+        // iteration first, then the device loop over the steady-state body
+        if (!c->started || c->resume_pending) TRY(enqueue_iteration(c));
+        rbg_status s = build_while(c);
+        if (s == RBG_OK) {
+            CU(cudaGraphLaunch(c->while_exec, c->stream));
+            TRY(read_state(c, &h));
+            c->iters = h.k + 1;  // iterations 0..k ran; the loop ended at the stop decision
+            return RBG_OK;
+        }
+        c->while_failed = true;  // e.g. a driver without conditional nodes: poll instead
+    }
+    return run_polled(c);
 }
 
 rbg_status rbg_set_timing(rbg_ctx *c, int on) {
@@ -689,7 +809,8 @@ rbg_status rbg_get_errors(rbg_ctx *c, double *out) {
     if (!out) return fail(RBG_EINVAL, "null output");
     DevState h;
     TRY(read_state(c, &h));
-    const long long n = h.stop ? h.k + 1 : h.k;
+    // err_k exists once the decision kernel ran: not after PEER_TIMEOUT (the wait stopped first)
+    const long long n = (h.stop && h.stop != kStopPeer) ? h.k + 1 : h.k;
     if (n) CU(cudaMemcpy(out, c->errors, sizeof(double) * n, cudaMemcpyDeviceToHost));
     return RBG_OK;
 }
@@ -793,6 +914,7 @@ rbg_status rbg_get_stats(rbg_ctx *c, rbg_stats *o) {
     TRY(read_state(c, &h));
     std::memset(o, 0, sizeof *o);
     o->k = h.k;
+    o->noop_iters = h.noop;
     // iterations with events, restricted to those that did work: 0..k
     const long long last = std::min<long long>(h.k, (long long)c->ev.size() - 1);
     float ms;

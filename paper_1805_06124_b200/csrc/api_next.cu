@@ -66,6 +66,7 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
         return fail(RBG_EINVAL, "a single-GPU context appends at the end (ids M_global..M_global+M_f)");
     DevState h;
     TRY(read_state(c, &h));
+    TRY(need_settled(c, h, "add_columns"));
     const long long M0 = c->M, M1 = c->M + M_f;
     double2 *Fd = nullptr;
     bool f_owned = false;
@@ -146,6 +147,10 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
         cudaGraphExecDestroy(c->graph);
         c->graph = nullptr;
     }
+    if (c->while_exec) {  // its kernels hold the old column pointers and record epoch
+        cudaGraphExecDestroy(c->while_exec);
+        c->while_exec = nullptr;
+    }
     if (c->started) {
         CU(cudaMemsetAsync(&c->st->stop, 0, sizeof(int), c->stream));
         if (sharded) {
@@ -202,6 +207,7 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     if (c->world != 1) return fail(RBG_ESTATE, "gram needs a single-GPU context");
     DevState h;
     TRY(read_state(c, &h));
+    TRY(need_settled(c, h, "gram"));
     const int k = (int)h.k;
     if (!G || ldg < k) return fail(RBG_EINVAL, "null output or ldg < k");
     if (k == 0) return RBG_OK;
@@ -221,9 +227,9 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
 rbg_status rbg_gram_fold(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     TRY(check_ctx(c));
     if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
-    if (c->local_pending) return fail(RBG_ESTATE, "gram_fold inside an EXTERNAL/PEER iteration");
     DevState h;
     TRY(read_state(c, &h));
+    TRY(need_settled(c, h, "gram_fold"));
     const int k = (int)h.k;
     if (!G || ldg < k) return fail(RBG_EINVAL, "null G or ldg < k");
     if (k == 0) return RBG_OK;
@@ -257,6 +263,7 @@ rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_d
     if (X && ldx < c->N) return fail(RBG_EINVAL, "ldx < N");
     DevState h;
     TRY(read_state(c, &h));
+    if (!Gin) TRY(need_settled(c, h, "reconstruct"));
     const int k = (int)h.k;
     if (kr_out) *kr_out = 0;
     if (k == 0) return RBG_OK;

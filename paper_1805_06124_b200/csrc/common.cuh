@@ -43,7 +43,7 @@ struct __align__(32) PeerRec {
 struct DevState {
     long long k;        // basis vectors built so far
     int stop;           // rbg_stop
-    int pad;
+    int noop;           // decision/IMGS launches that found the greedy already stopped
     double m_loc;       // local maxloc after the last sweep
     long long j_loc;    // its GLOBAL column index
 };
@@ -205,6 +205,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// rbg_run's device-side loop: the iteration body is a CUDA-graph
+// conditional WHILE node; whichever kernel records the stop decision (or first sees it) sets
+// the loop condition to 0, so no iteration is launched after the stop.  use = 0 outside that
+// graph (plain launches, graph batches): the handle is then not touched.
+__device__ __forceinline__ void loop_exit(cudaGraphConditionalHandle h, int use) {
+    if (use) cudaGraphSetConditional(h, 0u);
 }
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {

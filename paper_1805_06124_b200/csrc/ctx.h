@@ -86,6 +86,16 @@ struct rbg_ctx {
     std::vector<long long> ev_iter;
     int graph_batch = 0;
     cudaGraphExec_t graph = nullptr;
+    // rbg_run's device loop: one iteration as the body of a conditional WHILE graph node; the
+    // kernel that records the stop sets the condition to 0 (loop_exit), so the host neither
+    // polls nor launches iterations past the stop.  in_while: capturing the body (kernels get
+    // use_cond = 1).  while_failed: the graph could not be built here, rbg_run polls instead.
+    cudaGraphExec_t while_exec = nullptr;
+    cudaGraphConditionalHandle cond = 0;
+    bool in_while = false;
+    bool while_failed = false;
+    cudaStream_t poll_stream = nullptr;  // polled rbg_run: reads the stop flag between batches
+    int *poll_h = nullptr;               // pinned host word for that read
     rbg_ortho ortho = RBG_ORTHO_MGS;
     bool xmode = false;          // explicit residuals (Algorithm 2 updates)
     double *w_true = nullptr;    // explicit mode: the caller's weights (w holds ones)
@@ -115,6 +125,7 @@ SweepArgs sweep_args(const rbg_ctx *c);
 ImgsArgs imgs_args(const rbg_ctx *c);
 rbg_status check_ctx(rbg_ctx *c);
 rbg_status read_state(rbg_ctx *c, DevState *h);
+rbg_status need_settled(const rbg_ctx *c, const DevState &h, const char *what);
 rbg_status upload_block(rbg_ctx *c, const void *src, long long Mb, long long ld, rbg_mem mem, double2 **out,
                         bool *owned);  // *owned = false: a device block read in place
 rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, long long ldr, double *r2,

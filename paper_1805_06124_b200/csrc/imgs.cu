@@ -34,16 +34,30 @@ namespace rbg {
 // data of reduction n+2 after all of its own warps have sent reduction n+1, i.e. after
 // they finished reading the buffers of reduction n.
 #include <cstdio>
-// Watchdog wait for the producer's off-critical-path waits: a protocol bug ends the kernel with
-// a message and a trap (a CUDA error the ABI reports) instead of hanging the GPU.
+// Producer-side waits.  Built with -DRBG_DEBUG_WATCHDOG (protocol debugging only), a wait that
+// exceeds ~2 s of clock64 prints where it hung and traps; release builds never trap (a trap is a
+// sticky error that poisons the process's CUDA context, and preemption or time slicing can
+// stretch a healthy wait).
+#ifdef RBG_DEBUG_WATCHDOG
+#define RBG_WATCHDOG(t0, ...)                              \
+    do {                                                   \
+        if (clock64() - (t0) > 4000000000LL) {             \
+            printf(__VA_ARGS__);                           \
+            __trap();                                      \
+        }                                                  \
+    } while (0)
+#else
+#define RBG_WATCHDOG(t0, ...) \
+    do {                      \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_wait_guarded(uint64_t *bar, uint32_t parity, int code, long long st) {
     const long long t0 = clock64();
-    while (!mbar_try_wait(bar, parity)) {
-        if (clock64() - t0 > 4000000000LL) {
-            printf("IMGS HANG code %d rank %u tid %d step %lld parity %u\n", code, cluster_ctarank(), threadIdx.x, st, parity);
-            __trap();
-        }
-    }
+    (void)t0;
+    while (!mbar_try_wait(bar, parity))
+        RBG_WATCHDOG(t0, "IMGS HANG code %d rank %u tid %d step %lld parity %u\n", code, cluster_ctarank(), threadIdx.x,
+                     st, parity);
 }
 
 template <int CTAS>
@@ -285,24 +299,19 @@ struct BasisPipe {
             const uint32_t par = (uint32_t)((issued / D - 1) & 1);
             bool ok = false;
             const long long tp = clock64();
+            (void)tp;
             while (!(ok = mbar_try_wait(&empty[issued % D], par))) {
                 if (*done >= 0) break;
-                if (clock64() - tp > 4000000000LL) {
-                    printf("IMGS HANG producer rank %u issued %lld par %u\n", cluster_ctarank(), issued, par);
-                    __trap();
-                }
+                RBG_WATCHDOG(tp, "IMGS HANG producer rank %u issued %lld par %u\n", cluster_ctarank(), issued, par);
             }
             if (!ok) break;
             issue(issued++);
         }
         long long consumed;
         const long long td = clock64();
-        while ((consumed = *done) < 0) {
-            if (clock64() - td > 4000000000LL) {
-                printf("IMGS HANG producer waits for done, rank %u issued %lld\n", cluster_ctarank(), issued);
-                __trap();
-            }
-        }
+        (void)td;
+        while ((consumed = *done) < 0)
+            RBG_WATCHDOG(td, "IMGS HANG producer waits for done, rank %u issued %lld\n", cluster_ctarank(), issued);
         for (long long s = consumed; s < issued; s++) mbar_wait_guarded(&full[s % D], (uint32_t)((s / D) & 1), 3, s);
     }
 };
@@ -319,7 +328,13 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     __shared__ long long s_done;
 
     const int stop0 = a.st->stop;
-    if (stop0) return;
+    if (stop0) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            loop_exit(a.cond, a.use_cond);
+            a.st->noop += 1;  // rbg_stats.noop_iters: iterations launched past the stop
+        }
+        return;
+    }
     const long long k = a.st->k;
     const uint32_t rank = cluster_ctarank();
     const int tid = threadIdx.x;
@@ -363,7 +378,10 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     const bool leader = (rank == 0 && tid == 0);
     if (leader) a.errors[k] = err;
     if (why != kStopNone) {
-        if (leader) a.st->stop = why;
+        if (leader) {
+            a.st->stop = why;
+            loop_exit(a.cond, a.use_cond);
+        }
         return;
     }
     if (producer) {
@@ -456,6 +474,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
         if (leader) {
             a.nu[k] = nu;
             a.st->stop = kStopRank;
+            loop_exit(a.cond, a.use_cond);
         }
         return;
     }

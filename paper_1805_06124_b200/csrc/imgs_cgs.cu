@@ -129,7 +129,13 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
     cg::grid_group grid = cg::this_grid();
     __shared__ double2 s_w[8];
     const int stop0 = a.st->stop;
-    if (stop0) return;
+    if (stop0) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            loop_exit(a.cond, a.use_cond);
+            a.st->noop += 1;  // rbg_stats.noop_iters: iterations launched past the stop
+        }
+        return;
+    }
     const long long k = a.st->k;
     const long long nvec = a.nvec;
     const bool odd_tail = !CPLX && (a.N & 1);
@@ -150,7 +156,10 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
     const bool leader = (blockIdx.x == 0 && threadIdx.x == 0);
     if (leader) a.errors[k] = err;
     if (why != kStopNone) {
-        if (leader) a.st->stop = why;
+        if (leader) {
+            a.st->stop = why;
+            loop_exit(a.cond, a.use_cond);
+        }
         return;
     }
 
@@ -200,6 +209,7 @@ __global__ void __launch_bounds__(kCgsThreads) k_imgs_cgs(const ImgsArgs a, doub
         if (leader) {
             a.nu[k] = nu;
             a.st->stop = kStopRank;
+            loop_exit(a.cond, a.use_cond);
         }
         return;
     }

@@ -39,6 +39,8 @@ struct SweepArgs {
     unsigned long long peer_epoch;  // bumped by every sharded rbg_add_columns_ex (record tags)
     const long long *gid;   // global index of each local column once columns were appended to a
                             // sharded context (sorted ascending), else NULL: col_offset + local
+    cudaGraphConditionalHandle cond;  // rbg_run's device loop (loop_exit), valid when use_cond
+    int use_cond;
 };
 
 // Global index of local column j (sweep records).
@@ -80,6 +82,8 @@ struct ImgsArgs {
     size_t peer_slot;
     const long long *gid;  // as SweepArgs::gid (the owner masks its selected local column)
     long long *trace;      // RBG_DEBUG_IMGS: per-phase clock64 of 32 MGS steps (else NULL)
+    cudaGraphConditionalHandle cond;  // rbg_run's device loop (loop_exit), valid when use_cond
+    int use_cond;
 };
 
 // Local index of global column J on this rank, -1 if another rank owns it.
@@ -141,7 +145,7 @@ __device__ __forceinline__ void pivot_decision(const ImgsArgs &a, long long k, d
 // PEER exchange wait (a4): until every rank's record of this iteration has arrived (tag), or
 // timeout_ns passed (then stop = PEER_TIMEOUT).  One warp; no-op once stopped.
 cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, unsigned long long epoch, long long timeout_ns,
-                             cudaStream_t s);
+                             cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s);
 // Pivot search restart after columns were added to a sharded context: the local maxloc of r2
 // (one CTA, the sweep's total order and global indices) into the state, the candidate column
 // packed into the send slot and, on a PEER context, the record published to every rank.

@@ -13,8 +13,11 @@
 namespace rbg {
 
 __global__ void k_peer_wait(const PeerRec *mine, int world, DevState *st, unsigned long long epoch,
-                            long long timeout_ns) {
-    if (st->stop) return;
+                            long long timeout_ns, cudaGraphConditionalHandle cond, int use_cond) {
+    if (st->stop) {
+        if (threadIdx.x == 0) loop_exit(cond, use_cond);
+        return;
+    }
     const unsigned long long tag = peer_tag(epoch, st->k);
     const int p = threadIdx.x;
     bool late = false;
@@ -29,12 +32,15 @@ __global__ void k_peer_wait(const PeerRec *mine, int world, DevState *st, unsign
             __nanosleep(100);
         }
     }
-    if (__any_sync(0xffffffffu, late) && p == 0) st->stop = kStopPeer;
+    if (__any_sync(0xffffffffu, late) && p == 0) {
+        st->stop = kStopPeer;
+        loop_exit(cond, use_cond);
+    }
 }
 
 cudaError_t launch_peer_wait(const PeerRec *mine, int world, DevState *st, unsigned long long epoch, long long timeout_ns,
-                             cudaStream_t s) {
-    k_peer_wait<<<1, 32, 0, s>>>(mine, world, st, epoch, timeout_ns);
+                             cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
+    k_peer_wait<<<1, 32, 0, s>>>(mine, world, st, epoch, timeout_ns, cond, use_cond);
     return cudaGetLastError();
 }
 

@@ -186,7 +186,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     __shared__ __align__(8) uint64_t mbar;
 
     const int stop = a.st->stop;
-    if (stop) return;
+    if (stop) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) loop_exit(a.cond, a.use_cond);
+        return;
+    }
     // sweep uses q_{k-1} (k >= 1) unless INIT; a validation pass names its basis vector
     const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -346,7 +349,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_ring(const SweepArgs
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar;
 
-    if (a.st->stop) return;
+    if (a.st->stop) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) loop_exit(a.cond, a.use_cond);
+        return;
+    }
     const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long nvec = a.nvec;
@@ -493,7 +499,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar;
 
-    if (a.st->stop) return;
+    if (a.st->stop) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) loop_exit(a.cond, a.use_cond);
+        return;
+    }
     const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long nvec = a.nvec;

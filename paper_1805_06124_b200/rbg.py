@@ -54,7 +54,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int64), ("sweeps", ctypes.c_int64), ("t_init_ms", ctypes.c_double),
                 ("t_sweep_ms", ctypes.c_double), ("t_xchg_ms", ctypes.c_double),
                 ("t_imgs_ms", ctypes.c_double), ("t_total_ms", ctypes.c_double),
-                ("t_gap_ms", ctypes.c_double)]
+                ("t_gap_ms", ctypes.c_double), ("noop_iters", ctypes.c_int64)]
 
 
 # (name, argtypes, restype) for every symbol include/rbg.h and include/rbg_gen.h declare
@@ -220,6 +220,13 @@ class Context:
             self._keep.append(S)
         if w is not None:
             if _is_torch(w) and w.is_cuda:
+                import torch
+                # the library reads N doubles from the pointer: hand it a float64, contiguous
+                # (N,) tensor on S's device (a converted copy is kept alive with the context)
+                if w.dim() != 1 or w.shape[0] != d.N:
+                    raise ValueError("w must have N entries")
+                dev = torch.device("cuda", d.device) if d.S_mem == MEM_DEVICE else w.device
+                w = w.to(device=dev, dtype=torch.float64).contiguous()
                 d.w = w.data_ptr()
                 d.w_mem = MEM_DEVICE
             else:
@@ -308,7 +315,7 @@ class Context:
 
     def errors(self) -> np.ndarray:
         k, _, why = self.info()
-        n = k + 1 if why != "NONE" else k
+        n = k + 1 if why not in ("NONE", "PEER_TIMEOUT") else k   # err_k exists once decided
         out = np.zeros(max(n, 1))
         _check(lib().rbg_get_errors(self.h, out.ctypes.data))
         return out[:n]

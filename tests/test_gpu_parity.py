@@ -154,6 +154,28 @@ def test_graph_batches_match_plain(rbg, orc):
         compare(ctx.result(), o)
 
 
+@pytest.mark.parametrize("ortho", ["mgs", "cgs"])
+def test_device_loop_stops_without_tail(rbg, orc, ortho):
+    """rbg_run's device loop (a conditional WHILE graph node over one iteration, the stopping
+    kernel clears the condition): the oracle's bits, and no iteration launched past the stop;
+    the polled path (timing mode) stops within two batches of 16."""
+    S, w, tol, k_max = inputs.config0()
+    lanes = orc.CANONICAL_CGS if ortho == "cgs" else orc.CANONICAL
+    o = orc.greedy(S, w, tol, k_max, lanes=lanes, ortho=ortho)
+    assert o.stop == "RANK" and o.k < k_max - 40       # a tail of > 40 iterations would exist
+    with rbg.Context(S, w, tol, k_max, ortho=ortho) as ctx:
+        ctx.run()
+        compare(ctx.result(), o)
+        assert ctx.stats().noop_iters == 0
+        ctx.run()                                      # already stopped: nothing launched
+        assert ctx.stats().noop_iters == 0
+    with rbg.Context(S, w, tol, k_max, ortho=ortho) as ctx:
+        ctx.set_timing(True)
+        ctx.run()
+        compare(ctx.result(), o)
+        assert 0 <= ctx.stats().noop_iters <= 32
+
+
 def test_step_api_and_timing_identity(rbg):
     """rbg_step enqueues iterations; the cost-model identity T = T_sweep + T_xchg + T_IMGS
      holds to 1% from the library's own events."""
@@ -328,6 +350,7 @@ def test_peer_setup_errors_and_timeout(rbg):
     a.iter_finish()
     k, _, why = a.info()
     assert (k, why) == (0, "PEER_TIMEOUT")
+    assert len(a.errors()) == 0                  # err_0 was never decided (no stale 0.0)
     a.close()
     b.close()
 

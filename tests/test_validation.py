@@ -114,6 +114,29 @@ def test_gpu_enrichment_bit_exact(orc, cplx):
     np.testing.assert_array_equal(g.R, res.R)
 
 
+@pytest.mark.gpu
+def test_gpu_running_greedy_refuses_r_readers(orc):
+    """Between rbg_step calls the sweep with q_{k-1} is still pending (R row k-1 not filled):
+    add_columns, gram and reconstruct return ESTATE; validate and EIM (basis only) work; after
+    the stop decision all of them do."""
+    from paper_1805_06124_b200 import rbg
+    S, V, w = _sets(M_train=60)
+    with rbg.Context(S, w, 0.0, 40) as ctx:
+        ctx.step(5)
+        assert ctx.info()[::2] == (5, "NONE")
+        for call in (lambda: ctx.add_columns(V[:3]), ctx.gram, ctx.reconstruct):
+            with pytest.raises(rbg.RbgError) as e:
+                call()
+            assert e.value.status == rbg.ESTATE
+        assert ctx.validate(V).shape == (V.shape[0],)
+        assert len(ctx.eim()[0]) == 5
+        ctx.run()
+        k = ctx.info()[0]
+        assert k >= 5 and ctx.gram().shape == (k, k)
+        ctx.add_columns(V[:3])
+        ctx.gram()                                   # settled: the new columns have all rows
+
+
 def _drive(rbg, ctxs, mode, n):
     for _ in range(n):
         for c in ctxs:
