@@ -70,6 +70,7 @@ void free_ctx(rbg_ctx *c) {
     if (c->graph) cudaGraphExecDestroy(c->graph);
     if (c->while_exec) cudaGraphExecDestroy(c->while_exec);
     if (c->poll_stream) cudaStreamDestroy(c->poll_stream);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->poll_h) cudaFreeHost(c->poll_h);
     for (auto &p : c->ev)
         for (int i = 0; i < 4; i++) cudaEventDestroy(p.e[i]);
@@ -231,17 +232,31 @@ rbg_status enqueue_iteration(rbg_ctx *c) {
     return RBG_OK;
 }
 
+// Graphs are captured on a private stream (the caller's stream may be the legacy default
+// stream, which cannot be captured) and launched on the context's stream.
+struct CaptureStream {
+    rbg_ctx *c;
+    cudaStream_t keep;
+    explicit CaptureStream(rbg_ctx *ctx) : c(ctx), keep(ctx->stream) { c->stream = c->cap_stream; }
+    ~CaptureStream() { c->stream = keep; }
+};
+
 rbg_status build_graph(rbg_ctx *c) {
     if (c->graph) return RBG_OK;
+    if (!c->cap_stream) CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t g;
-    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     rbg_status s = RBG_OK;
-    for (int i = 0; i < c->graph_batch && s == RBG_OK; i++) {
-        s = enqueue_local(c);
-        if (s == RBG_OK) s = enqueue_xchg(c);
-        if (s == RBG_OK) s = enqueue_finish(c);
+    cudaError_t e;
+    {
+        CaptureStream cs(c);
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < c->graph_batch && s == RBG_OK; i++) {
+            s = enqueue_local(c);
+            if (s == RBG_OK) s = enqueue_xchg(c);
+            if (s == RBG_OK) s = enqueue_finish(c);
+        }
+        e = cudaStreamEndCapture(c->stream, &g);
     }
-    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (s != RBG_OK) return s;
     CU(e);
     e = cudaGraphInstantiate(&c->graph, g, 0);
@@ -279,6 +294,8 @@ bool while_supported(const rbg_ctx *c) {
 
 rbg_status build_while(rbg_ctx *c) {
     if (c->while_exec) return RBG_OK;
+    if (!c->cap_stream) CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    CaptureStream cs(c);
     cudaGraph_t g = nullptr;
     CU(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle h;

@@ -94,6 +94,7 @@ struct rbg_ctx {
     cudaGraphConditionalHandle cond = 0;
     bool in_while = false;
     bool while_failed = false;
+    cudaStream_t cap_stream = nullptr;   // graphs are captured here, launched on `stream`
     cudaStream_t poll_stream = nullptr;  // polled rbg_run: reads the stop flag between batches
     int *poll_h = nullptr;               // pinned host word for that read
     rbg_ortho ortho = RBG_ORTHO_MGS;

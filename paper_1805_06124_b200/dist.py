@@ -47,6 +47,8 @@ def max_over_ranks(x: float, group=None, device=None) -> float:
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return float(x)
+    if dist.get_backend(group) == "gloo":
+        device = "cpu"                               # gloo reduces host tensors
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
@@ -99,6 +101,43 @@ def sharded_context(S_local, w, tol: float, k_max: int, M_global: int, group=Non
     uid = nccl_unique_id(group)
     return rbg.Context(S_local, w, tol, k_max, comm=rbg.COMM_NCCL, rank=rank, world=world,
                        col_offset=off, M_global=M_global, nccl_id=uid, **kw)
+
+
+class _DevPtr:
+    """A device byte range as a torch tensor (zero copy, __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def exchange_slots(ctx, group=None, stream=None):
+    """The a4 exchange of an EXTERNAL context driven over the process group: every rank's
+    {maxloc record, candidate column} send slot all-gathered into every rank's receive slots
+    (rank p's bytes at recv + p * bytes), then rbg_iter_finish decides on the same records
+    everywhere.  NCCL groups gather the device slots directly; gloo groups (CPU tests, several
+    ranks sharing one GPU) stage them through host memory.  Call between iter_local and
+    iter_finish; `stream` = the context's stream (the slot is read after it)."""
+    import torch
+    import torch.distributed as dist
+    send, recv, nbytes = ctx.xchg_buffers()
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s_t = torch.as_tensor(_DevPtr(send, nbytes), device=dev)
+    r_t = torch.as_tensor(_DevPtr(recv, nbytes * world), device=dev)
+    if stream is not None:
+        stream.synchronize()
+    else:
+        ctx.sync()
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(r_t, s_t, group=group)
+        torch.cuda.current_stream(dev).synchronize()
+        return
+    h = s_t.cpu()
+    parts = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(parts, h, group=group)
+    r_t.copy_(torch.cat(parts))
+    torch.cuda.current_stream(dev).synchronize()
 
 
 def fold_over_ranks(fold, k: int, group=None):
