@@ -10,9 +10,8 @@
 namespace rbg {
 
 constexpr int kLaneSweep = 32;      // L_S: one warp per column
-constexpr int kImgsCtas = 8;        // cluster size of the IMGS kernel
-constexpr int kImgsThreads = 256;   // threads per IMGS CTA
-constexpr int kLaneImgs = kImgsCtas * kImgsThreads;  // L_I = 2048
+constexpr int kLaneImgs = 2048;     // L_I: the IMGS cluster's lanes (16 CTAs x 128 by default,
+                                    // 8 x 256 with RBG_IMGS_CTAS=8; same lanes, same tree)
 constexpr int kNuMax = 5;           // IMGS sweep cap (R7)
 
 constexpr int kStopNone = 0, kStopTol = 1, kStopKmax = 2, kStopRank = 3, kStopAll = 4, kStopPeer = 5;

@@ -7,14 +7,14 @@
 //
 // B200 design: the method is a chain of 2*nu*k dependent
 // reductions of length N, so the kernel is latency-bound.  It runs as ONE thread-block
-// cluster of 8 CTAs x 256 threads (L_I = 2048 lanes); the candidate vector v lives in
-// registers (vector u on lane u mod 2048); each MGS step is a lane-local fma chain, a
-// warp xor-butterfly, an all-to-all of the 64 warp partials through distributed shared
-// memory (st.async + mbarrier transaction counts, no CTA or cluster barrier) and a
-// 64-leaf tree evaluated by every warp, after which every CTA holds the bit-identical
-// coefficient and updates its slice of v.  The next step's basis vectors are loaded
-// (L2 evict-last) before the reduction so their latency overlaps it.  The kernel is
-// replicated on every GPU of a sharded run (no broadcast of q needed).
+// cluster of 16 CTAs x 128 lanes (+ a producer warp each; 8 x 256 with RBG_IMGS_CTAS=8),
+// L_I = 2048 lanes; the candidate vector v lives in registers (vector u on lane u mod 2048);
+// each MGS step is a lane-local fma chain, a warp xor-butterfly, a CTA pre-reduction, an
+// all-to-all of the CTA partials through distributed shared memory (st.async + mbarrier
+// transaction counts, no cluster barrier) and the cross-CTA tree evaluated by every thread,
+// after which every CTA holds the bit-identical coefficient and updates its slice of v.  The
+// basis slices are prefetched several steps ahead by TMA bulk copies from a producer warp.
+// The kernel is replicated on every GPU of a sharded run (no broadcast of q needed).
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>

@@ -5,7 +5,7 @@
 //
 // The SVD is taken through the j x j Gram matrix G = R R^H = V Sigma^2 V^H (DESIGN.md
 // reading R30), in three deterministic kernels:
-//  * k_gram: G = R R^H over 32 x 32 tiles of (a, b) pairs (upper triangle of tiles), the
+//  * k_gram: G = R R^H over 64 x 64 tiles of (a, b) pairs (upper triangle of tiles), the
 //    column range cut into chunks of kGramChunk columns; within a chunk every pair is one
 //    sequential fma chain in increasing column index, chunk partials are summed in chunk
 //    order by k_gram_reduce (the order the oracle's orc_gram writes out);

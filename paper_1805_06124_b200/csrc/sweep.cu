@@ -8,8 +8,8 @@
 //
 // B200 design:
 //  * one CTA per SM, 16 warps; the default kernel (k_sweep_dyn) hands columns to warps
-//    dynamically (a grid-wide counter claimed one column ahead), the static-block variants
-//    (k_sweep_ring, k_sweep) give each CTA a contiguous block of columns;
+//    dynamically (a grid-wide counter claimed one column ahead); k_sweep (the explicit-
+//    residual mode's kernel, RBG_SWEEP_KIND=percol) gives each CTA a contiguous block;
 //  * the weighted basis vector e~_k = w o q_k (N x 16 B, 160 KB at N = 10,000 complex) is
 //    staged once per CTA into shared memory with TMA bulk copies (cp.async.bulk) on an
 //    mbarrier;
@@ -337,124 +337,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
 }
 
-// Continuous-ring variant of k_sweep for the recurrence (a0/a2): a warp's columns form one
-// stream of 16-byte trips (column c0, c0+16, ...; ceil(nvec/32) trips each), and the ring of
-// U loads in flight runs across column boundaries, so the next column's first vectors are
-// already in flight while the current column is reduced (xor-butterfly), its r2 updated and
-// its R entry stored.  The per-lane chains, the lane tree and the visiting order are those
-// of k_sweep: results are bit-identical.  r2 of the next column is prefetched one column
-// ahead so its load latency never stalls the warp.
-template <bool CPLX, bool INIT, bool ESMEM, int U>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_ring(const SweepArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t mbar;
-
-    if (a.st->stop) {
-        if (threadIdx.x == 0 && blockIdx.x == 0) loop_exit(a.cond, a.use_cond);
-        return;
-    }
-    const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long nvec = a.nvec;
-    const bool odd_tail = !CPLX && (a.N & 1);
-
-    const double2 *Eg = INIT ? reinterpret_cast<const double2 *>(a.w) : a.WQ + (k - 1) * a.ldq_v;
-    const double2 *E = Eg;
-    const double *Ew = a.w;
-    if (ESMEM) {
-        const size_t bytes = (INIT && CPLX) ? ((size_t)nvec * 8 + 15) / 16 * 16 : (size_t)nvec * 16;
-        if (tid == 0) {
-            mbar_init(&mbar, 1);
-            mbar_arrive_expect_tx(&mbar, (uint32_t)bytes);
-            const unsigned char *src = reinterpret_cast<const unsigned char *>(Eg);
-            for (size_t off = 0; off < bytes; off += kBulkChunk) {
-                uint32_t n = (uint32_t)((bytes - off) < kBulkChunk ? (bytes - off) : kBulkChunk);
-                bulk_g2s(smem + off, src + off, n, &mbar);
-            }
-        }
-        __syncthreads();
-        E = reinterpret_cast<const double2 *>(smem);
-        Ew = reinterpret_cast<const double *>(smem);
-    }
-
-    const long long c_begin = (long long)blockIdx.x * a.M / gridDim.x;
-    const long long c_end = (long long)(blockIdx.x + 1) * a.M / gridDim.x;
-    const uint64_t pol = policy_evict_first();
-    // a column is gpc groups of U trips (32 vectors per trip); the last group is ragged
-    const int nv = (int)nvec;
-    const int gpc = (int)((nvec + 32 * U - 1) / (32 * U));
-    const long long c0 = c_begin + warp;
-    const long long ncols = c0 < c_end ? (c_end - c0 + kSweepWarps - 1) / kSweepWarps : 0;
-    const long long G = ncols * gpc;  // groups of this warp
-
-    // load cursor: group lg of the column whose first vector (+ lane) is lcol
-    const double2 *lcol = a.S + c0 * a.ldv + lane;
-    int lg = 0;
-    double2 xr[U];
-#pragma unroll
-    for (int t = 0; t < U; t++)
-        xr[t] = (G > 0 && t * 32 + lane < nv) ? ld_stream(lcol + t * 32, pol) : make_double2(0.0, 0.0);
-    if (++lg == gpc) { lg = 0; lcol += (long long)kSweepWarps * a.ldv; }
-    if (ESMEM) mbar_wait(&mbar, 0);  // loads are in flight; now e~ must have landed
-
-    double best_m = -INFINITY;
-    long long best_j = 0x7fffffffffffffffLL;
-    double re = 0.0, im = 0.0;
-    long long c = c0;
-    int cg = 0;  // group of column c being consumed
-    double old = (!INIT && ncols > 0) ? a.r2[c0] : 0.0;  // r2 of the current column
-
-    for (long long g = 0; g < G; g++) {
-        const bool more = g + 1 < G;
-        const int lu0 = lg * 32 * U + lane;  // first vector of the group being issued
-        const int cu0 = cg * 32 * U + lane;  // first vector of the group being consumed
-        const double2 *lp = lcol + lg * 32 * U;
-#pragma unroll
-        for (int t = 0; t < U; t++) {
-            double2 x = xr[t];
-            // refill slot t with the same slot of the next group (possibly the next column)
-            xr[t] = (more && lu0 + t * 32 < nv) ? ld_stream(lp + t * 32, pol) : make_double2(0.0, 0.0);
-            const int u = cu0 + t * 32;
-            if (u < nv) {
-                if (odd_tail && u == nv - 1) x.y = 0.0;  // row N is padding
-                accum<CPLX, INIT>(re, im, x, load_e<CPLX, INIT, ESMEM>(E, Ew, u));
-            }
-        }
-        if (++lg == gpc) { lg = 0; lcol += (long long)kSweepWarps * a.ldv; }
-        if (++cg == gpc) {  // column c complete (warp-uniform)
-            cg = 0;
-#pragma unroll
-            for (int h = 1; h < 32; h <<= 1) {  // CAC rule 3
-                re = re + __shfl_xor_sync(0xffffffffu, re, h);
-                if (CPLX && !INIT) im = im + __shfl_xor_sync(0xffffffffu, im, h);
-            }
-            double r2n;
-            if (INIT) {
-                r2n = re;
-                if (lane == 0) a.r2[c] = r2n;
-            } else {
-                const double cc = CPLX ? fma(re, re, im * im) : re * re;  // CAC rule 5
-                r2n = old - cc;                                            // CAC rule 6
-                if (lane == 0) {
-                    if (CPLX) reinterpret_cast<double2 *>(a.R)[(k - 1) * a.ldr + c] = make_double2(re, im);
-                    else a.R[(k - 1) * a.ldr + c] = re;
-                    a.r2[c] = r2n;
-                }
-                const long long cn = c + kSweepWarps;
-                old = cn < c_end ? a.r2[cn] : 0.0;
-            }
-            if (r2n > best_m) {  // columns visited in increasing order: first max wins
-                best_m = r2n;
-                best_j = c;
-            }
-            c += kSweepWarps;
-            re = 0.0;
-            im = 0.0;
-        }
-    }
-    sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
-}
-
 // Pivot search restart (sharded rbg_add_columns_ex): one CTA; thread t scans r2[t], r2[t + T],
 // ... (increasing index: first max wins), warp maxloc, then sweep_finish (grid of one CTA: it
 // is the last CTA) writes the state, packs the candidate and publishes the PEER record.
@@ -486,13 +368,14 @@ cudaError_t launch_restart(const SweepArgs &a, bool cplx, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// Dynamically scheduled ring sweep (default for the recurrence): the ring of k_sweep_ring, but a
-// warp's columns come from a grid-wide counter instead of a static block, so SMs that stream
+// Dynamically scheduled ring sweep (default for the recurrence): a ring of U loads in flight per
+// lane that runs across column boundaries, and a warp's columns come from a grid-wide counter
+// instead of a static block, so SMs that stream
 // faster take more columns (ncu on the static kernel: SMs active 91.8-100 % of the launch,
 // 95.6 % on average).  The first column of a warp is its global warp index; each later one is
 // one atomicAdd (lane 0) taken a column ahead of use, so its latency never stalls the ring.  A
 // warp's columns increase, so "first max wins" keeps the lowest index among a warp's ties and
-// the CTA / grid maxloc uses the total order: results are bit-identical to k_sweep_ring.  The
+// the CTA / grid maxloc uses the total order: results are bit-identical to k_sweep.  The
 // counter (a.next_col) returns to 0 in the last CTA.
 template <bool CPLX, bool INIT, bool ESMEM, int U>
 __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs a) {
@@ -642,25 +525,23 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
 using SweepKernel = void (*)(const SweepArgs);
 
 template <bool CPLX, bool INIT, bool ESMEM, int U>
-static SweepKernel pick_kernel(bool ring, bool dyn) {
+static SweepKernel pick_kernel(bool dyn) {
     // the explicit mode (a.V) re-reads and rewrites each column: per-column loop of k_sweep;
-    // the recurrence: the dynamically scheduled ring (default) or the static-block ring
-    if (dyn) return k_sweep_dyn<CPLX, INIT, ESMEM, U>;
-    return ring ? k_sweep_ring<CPLX, INIT, ESMEM, U> : k_sweep<CPLX, INIT, ESMEM, U>;
+    // the recurrence: the dynamically scheduled ring (k_sweep_dyn)
+    return dyn ? k_sweep_dyn<CPLX, INIT, ESMEM, U> : k_sweep<CPLX, INIT, ESMEM, U>;
 }
 
 template <bool CPLX, bool INIT, bool ESMEM>
 static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStream_t s) {
-    // RBG_SWEEP_KIND = dyn (default) | ring (static blocks) | percol (per-column ring)
+    // RBG_SWEEP_KIND = dyn (default) | percol (k_sweep, static column blocks; the explicit mode's kernel)
     const char *kind = getenv("RBG_SWEEP_KIND");
-    const bool ring = a.V == nullptr && !(kind && std::strcmp(kind, "percol") == 0);
-    const bool dyn = ring && a.next_col != nullptr && !(kind && std::strcmp(kind, "ring") == 0);
-    auto kern = pick_kernel<CPLX, INIT, ESMEM, 4>(ring, dyn);
+    const bool dyn = a.V == nullptr && a.next_col != nullptr && !(kind && std::strcmp(kind, "percol") == 0);
+    auto kern = pick_kernel<CPLX, INIT, ESMEM, 4>(dyn);
     const int unroll = (a.V && cfg.unroll > 12) ? 12 : cfg.unroll;
     switch (unroll) {
-        case 8: kern = pick_kernel<CPLX, INIT, ESMEM, 8>(ring, dyn); break;
-        case 12: kern = pick_kernel<CPLX, INIT, ESMEM, 12>(ring, dyn); break;
-        case 16: kern = pick_kernel<CPLX, INIT, ESMEM, 16>(ring, dyn); break;
+        case 8: kern = pick_kernel<CPLX, INIT, ESMEM, 8>(dyn); break;
+        case 12: kern = pick_kernel<CPLX, INIT, ESMEM, 12>(dyn); break;
+        case 16: kern = pick_kernel<CPLX, INIT, ESMEM, 16>(dyn); break;
         default: break;
     }
     if (cfg.smem > 48 * 1024) {

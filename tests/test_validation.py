@@ -76,6 +76,50 @@ def test_enrichment_converges_and_is_monotone(orc):
     assert np.max(np.abs(G - np.eye(res.k))) <= 1e-12
 
 
+@pytest.mark.parametrize("mode", ["canonical", "plain"])
+def test_oracle_resume_branch_cor56_on_enlarged_set(orc, mode):
+    """The oracle's resume branch (rbg_oracle.c, k0 >= 0: enrichment, reading
+    R32) pinned directly, in both lane modes.  After every enrichment round, for every k from the
+    resume point k0 to the new stop:
+      * Cor. 5.6 on the ENLARGED column set: err_k = max_j of the direct
+        projection residual ||(I - P_k) s~_j||, computed by explicit projection (brute.py), within
+        the recurrence floor (reading R8);
+      * the pivot taken at k maximises that direct residual up to the same floor;
+      * err is non-increasing from k0 on (slack = the floor)."""
+    L = orc.CANONICAL if mode == "canonical" else orc.PLAIN
+    S, V, w = _sets(M_train=60)
+    tol = 1e-5
+    res = orc.greedy(S, w, tol, 150, lanes=L)
+    scale = np.sqrt(np.max(np.sum(w * np.abs(np.concatenate([S, V])) ** 2, axis=1)))
+    atol = 1e-7 * scale                                  # recurrence floor (R8), as above
+    added = np.zeros(V.shape[0], bool)
+    rounds = 0
+    for _ in range(4):
+        err, _, _ = orc.validate(res.Q, V, w, L[0])
+        fail = (err >= tol) & ~added
+        if not fail.any():
+            break
+        added |= fail
+        _, C, e2 = orc.validate(res.Q, V[fail], w, L[0])
+        S = np.concatenate([S, V[fail]])
+        res.R = np.concatenate([res.R, C], axis=1)
+        res.r2 = np.concatenate([res.r2, e2])
+        k0, piv0 = res.k, res.pivots.copy()
+        res = orc.greedy(S, w, tol, 150, lanes=L, resume=res)
+        rounds += 1
+        assert res.k > k0 and np.array_equal(res.pivots[:k0], piv0)     # continued, not restarted
+        St = brute.weighted(S, w)
+        Qt = brute.weighted(res.Q, w)                    # W^{1/2} q_i: orthonormal in l2
+        for k in range(k0, res.k + 1):
+            d = brute.direct_residuals(St, Qt[:, :k])
+            assert abs(res.errors[k] - d.max()) <= atol, (k, res.errors[k], d.max())
+            if k < res.k:
+                assert d[res.pivots[k]] >= d.max() - atol
+        assert np.all(np.diff(res.errors[k0:]) <= atol)
+        assert len(set(res.pivots.tolist())) == res.k    # a permutation prefix (R10)
+    assert rounds >= 1
+
+
 # ------------------------------------------------------------------------------ GPU parity
 
 @pytest.mark.gpu
