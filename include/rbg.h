@@ -210,7 +210,9 @@ rbg_status rbg_validate(rbg_ctx *ctx, const void *V, int64_t M_v, int64_t ldv, r
  * append the N x M_f block F (column stride ldf, 0 => N) to the training columns of a
  * single-GPU context.  Their R rows and residuals are computed with the greedy's own
  * arithmetic, the pivot search restarts over all columns and a stopped greedy may continue
- * (rbg_run / rbg_step).  The snapshot matrix becomes library-owned (a borrowed S is copied).
+ * (rbg_run / rbg_step).  The caller's S is not copied (a borrowed S stays borrowed): appended
+ * columns live in a library-owned second segment that the sweep streams after the first;
+ * only R's rows (k_max x M) and the per-column vectors are reallocated.
  * ESTATE on sharded contexts (see rbg_add_columns_ex), and on a running greedy (started, no
  * stop decision yet: the sweep with q_{k-1} is still pending) -- run it to its stop first.
  * Blocking.                                                                                 */

@@ -44,26 +44,66 @@ void free_ctx(rbg_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->imgs_trace) {  // RBG_DEBUG_IMGS: mean cycles per phase over the traced MGS steps
         long long t[32 * 8];
-        if (cudaMemcpy(t, c->imgs_trace, sizeof t, cudaMemcpyDeviceToHost) == cudaSuccess && t[4] > 0) {
-            double ph[4] = {0, 0, 0, 0}, step = 0;
+        if (cudaMemcpy(t, c->imgs_trace, sizeof t, cudaMemcpyDeviceToHost) == cudaSuccess && t[5] > 0) {
+            // t: 0 step start, 1 after dot, 2 after reduction start (butterfly, CTA tree, send),
+            // 3 after the loads overlapped with the round trip, 4 coefficient known, 5 after
+            // axpy; 7 = remote partials arrived (PRE reducer)
+            double ph[5] = {0, 0, 0, 0, 0}, step = 0, remote = 0;
             int n = 0;
-            double sb[3] = {0, 0, 0};
-            for (int i = 0; i < 32 && t[i * 8 + 4] > 0; i++, n++) {
-                for (int p = 0; p < 4; p++) ph[p] += (double)(t[i * 8 + p + 1] - t[i * 8 + p]);
-                if (t[i * 8 + 5]) {
-                    sb[0] += (double)(t[i * 8 + 5] - t[i * 8 + 2]);
-                    sb[1] += (double)(t[i * 8 + 6] - t[i * 8 + 5]);
-                    sb[2] += (double)(t[i * 8 + 7] - t[i * 8 + 6]);
-                }
+            for (int i = 0; i < 32 && t[i * 8 + 5] > 0; i++, n++) {
+                for (int p = 0; p < 5; p++) ph[p] += (double)(t[i * 8 + p + 1] - t[i * 8 + p]);
+                if (t[i * 8 + 7]) remote += (double)(t[i * 8 + 7] - t[i * 8 + 3]);
                 if (i + 1 < 32 && t[(i + 1) * 8] > 0) step += (double)(t[(i + 1) * 8] - t[i * 8]);
             }
-            if (n > 1 && sb[0] > 0)
-                fprintf(stderr, "rbg: imgs reduce: butterfly %.0f, CTA tree %.0f, remote wait %.0f, rest %.0f cycles\n",
-                        sb[0] / n, sb[1] / n, sb[2] / n, ph[2] / n - (sb[0] + sb[1] + sb[2]) / n);
             if (n > 1)
-                fprintf(stderr, "rbg: imgs iteration %lld, %d steps: wait-stage %.0f, dot %.0f, reduce %.0f, axpy %.0f, "
-                                "step %.0f cycles\n", c->trace_iter, n, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n,
+                fprintf(stderr, "rbg: imgs iteration %lld, %d steps: dot %.0f, reduce-start %.0f, overlapped loads %.0f, "
+                                "reduce-finish %.0f (remote wait %.0f), axpy %.0f, step %.0f cycles\n",
+                        c->trace_iter, n, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, remote / n, ph[4] / n,
                         step / (n - 1));
+        }
+        // every CTA's step timestamps (steps 64..71): send skew across CTAs and the latency from
+        // the last CTA's send to each CTA's coefficient
+        unsigned long long gt[16 * 8 * 3];
+        if (cudaMemcpy(gt, c->imgs_trace + 512, sizeof gt, cudaMemcpyDeviceToHost) == cudaSuccess && gt[2]) {
+            double skew = 0, lat = 0, busy = 0, step = 0;
+            int n = 0;
+            for (int st = 0; st < 8; st++) {
+                unsigned long long smin = ~0ull, smax = 0, cmax = 0, c0max = 0;
+                int have = 0;
+                double b = 0;
+                for (int r = 0; r < 16; r++) {
+                    const unsigned long long *g = gt + (r * 8 + st) * 3;
+                    if (!g[1]) continue;
+                    have++;
+                    smin = std::min(smin, g[1]);
+                    smax = std::max(smax, g[1]);
+                    cmax = std::max(cmax, g[2]);
+                    c0max = std::max(c0max, g[0]);
+                    b += (double)(g[1] - g[0]);
+                }
+                if (!have) continue;
+                skew += (double)(smax - smin);
+                lat += (double)(cmax - smax);
+                if (st + 1 < 8) {
+                    unsigned long long nmax = 0;
+                    for (int r = 0; r < 16; r++) nmax = std::max(nmax, gt[(r * 8 + st + 1) * 3]);
+                    if (nmax) step += (double)(nmax - c0max);
+                }
+                n++;
+                busy += b / have;
+            }
+            if (n > 1)
+                fprintf(stderr, "rbg: imgs cluster (ns/step): send skew across CTAs %.0f, last send -> last coefficient %.0f, "
+                                "step start -> send %.0f, step %.0f\n", skew / n, lat / n, busy / n, step / (n - 1));
+        }
+        // %globaltimer (ns): [256] sweep's last CTA done, [257] IMGS entry, [258] cluster synced,
+        // [259] after grid_dep_wait, [260] n0 known, [261] MGS sweeps done, [262] q stored
+        unsigned long long g[8];
+        if (cudaMemcpy(g, c->imgs_trace + 256, sizeof g, cudaMemcpyDeviceToHost) == cudaSuccess && g[1] && g[6]) {
+            auto d = [&](int a, int b) { return (g[a] && g[b]) ? (double)(long long)(g[b] - g[a]) * 1e-3 : -1.0; };
+            fprintf(stderr, "rbg: imgs iteration %lld phases (us): sweep-end->entry %.2f, entry->cluster sync %.2f, "
+                            "->grid_dep_wait %.2f, ->n0 %.2f, ->MGS done %.2f, ->q stored %.2f (entry->end %.2f)\n",
+                    c->trace_iter, d(0, 1), d(1, 2), d(2, 3), d(3, 4), d(4, 5), d(5, 6), d(1, 6));
         }
         dfree(c->imgs_trace);
     }
@@ -83,6 +123,7 @@ void free_ctx(rbg_ctx *c) {
     dfree(c->peer_in);
     dfree(c->gid);
     if (c->own_S) dfree(c->S);
+    dfree(c->S1);
     dfree(c->w);
     dfree(c->Q);
     dfree(c->WQ);
@@ -105,10 +146,20 @@ void free_ctx(rbg_ctx *c) {
     delete c;
 }
 
+// Programmatic dependent launches (sweep after the decision kernel, decision/IMGS after the
+// sweep): not with per-phase events between the kernels (timing mode), and the IMGS side only
+// on one GPU (its predecessor there is the sweep, never the exchange wait that can set stop).
+static bool pdl_enabled(const rbg_ctx *c) {
+    static const bool off = getenv("RBG_NO_PDL") != nullptr;
+    return !off && !c->timing;
+}
+
 SweepArgs sweep_args(const rbg_ctx *c) {
     SweepArgs a;
     a.S = c->S;
     a.ldv = c->ldv;
+    a.S1 = c->S1;
+    a.M0 = c->M0;
     a.M = c->M;
     a.N = c->N;
     a.nvec = c->nvec;
@@ -138,6 +189,11 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.gid = c->gid;
     a.cond = c->cond;
     a.use_cond = c->in_while ? 1 : 0;
+    a.pdl = pdl_enabled(c) ? 1 : 0;
+    static const bool no_tail_pf = getenv("RBG_NO_TAIL_PF") != nullptr;
+    a.tail_pf = no_tail_pf ? 0 : 1;
+    a.tstamp = (c->imgs_trace && c->iters == c->trace_iter) ? reinterpret_cast<unsigned long long *>(c->imgs_trace) + 256
+                                                          : nullptr;
     return a;
 }
 
@@ -145,6 +201,8 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     ImgsArgs a;
     a.S = c->S;
     a.ldv = c->ldv;
+    a.S1 = c->S1;
+    a.M0 = c->M0;
     a.N = c->N;
     a.nvec = c->nvec;
     a.w = c->w;
@@ -172,6 +230,7 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.trace = (c->imgs_trace && c->iters == c->trace_iter) ? c->imgs_trace : nullptr;
     a.cond = c->cond;
     a.use_cond = c->in_while ? 1 : 0;
+    a.pdl = (pdl_enabled(c) && c->comm == RBG_COMM_NONE && c->started) ? 1 : 0;
     return a;
 }
 
@@ -337,8 +396,6 @@ rbg_status build_while(rbg_ctx *c) {
 // stop flag as of the end of the batch before (side stream, pinned word), so at most two
 // batches run past the stop (as early-exit kernels).
 rbg_status run_polled(rbg_ctx *c) {
-    if (!c->poll_stream) CU(cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking));
-    if (!c->poll_h) CU(cudaHostAlloc(&c->poll_h, sizeof(int), cudaHostAllocDefault));
     const long long B = c->graph_batch > 0 ? c->graph_batch : 16;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     rbg_status s = RBG_OK;
@@ -364,6 +421,9 @@ rbg_status run_polled(rbg_ctx *c) {
         if (x) cudaEventDestroy(x);
     if (s != RBG_OK) return s;
     if (e != cudaSuccess) return fail(RBG_ECUDA, "rbg_run: %s", cudaGetErrorString(e));
+    DevState h;
+    TRY(read_state(c, &h));
+    c->stopped = h.stop != 0 || c->iters >= c->k_max + 1;
     return RBG_OK;
 }
 
@@ -456,6 +516,8 @@ rbg_status coeff_passes(rbg_ctx *c, const double2 *V, long long Mv, double *R, l
     SweepArgs a = sweep_args(c);
     a.S = V;
     a.ldv = c->nvec;
+    a.S1 = nullptr;
+    a.M0 = Mv;
     a.M = Mv;
     a.R = R;
     a.ldr = ldr;
@@ -607,6 +669,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     c->se = cplx ? 16 : 8;
     c->N = d->N;
     c->M = d->M;
+    c->M0 = d->M;
     c->nvec = nvec;
     c->ldq_v = nvec;
     c->tol = d->tol;
@@ -693,8 +756,8 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     }
     if (const char *ti = getenv("RBG_DEBUG_IMGS")) {
         c->trace_iter = atoll(ti);
-        CUB(dmalloc(&c->imgs_trace, 32 * 8 * sizeof(long long)));
-        CUB(cudaMemsetAsync(c->imgs_trace, 0, 32 * 8 * sizeof(long long), c->stream));
+        CUB(dmalloc(&c->imgs_trace, 1024 * sizeof(long long)));
+        CUB(cudaMemsetAsync(c->imgs_trace, 0, 1024 * sizeof(long long), c->stream));
     }
     c->cfg_init = sweep_config(cplx, true, nvec, c->num_sms, c->device);
     c->cfg_sweep = sweep_config(cplx, false, nvec, c->num_sms, c->device);
@@ -727,6 +790,11 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
                 return bail(fail(RBG_ENCCL, "ncclCommInitRank: %s", msg ? msg : "?"));
         }
     }
+    // rbg_run's helpers, allocated here so that no run pays cudaHostAlloc / stream creation
+    // (both synchronise with the device) between its iterations
+    CUB(cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking));
+    CUB(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    CUB(cudaHostAlloc(&c->poll_h, sizeof(int), cudaHostAllocDefault));
     CUB(cudaStreamSynchronize(c->stream));
 #undef CUB
     *out = c;
@@ -760,9 +828,13 @@ rbg_status rbg_run(rbg_ctx *c) {
     if (c->comm == RBG_COMM_EXTERNAL) return fail(RBG_ESTATE, "EXTERNAL contexts use rbg_iter_local/finish");
     if (c->comm == RBG_COMM_PEER && !c->peer_connected) return fail(RBG_ESTATE, "PEER context not connected (rbg_peer_connect)");
     if (c->local_pending) return fail(RBG_ESTATE, "rbg_run inside an iteration (rbg_iter_local pending)");
+    if (c->stopped || c->iters >= c->k_max + 1) {  // a previous rbg_run saw the stop
+        CU(cudaStreamSynchronize(c->stream));
+        return RBG_OK;
+    }
+    // no host synchronisation here: iterations enqueued by rbg_step run first in stream order
+    // (and a greedy they stopped makes the loop below exit at its first kernel)
     DevState h;
-    TRY(read_state(c, &h));  // also waits for iterations enqueued by rbg_step
-    if (h.stop || c->iters >= c->k_max + 1) return RBG_OK;
     if (while_supported(c)) {
         // sweep 0 (or the restart after rbg_add_columns) is a different kernel: one plain
         // iteration first, then the device loop over the steady-state body
@@ -772,6 +844,7 @@ rbg_status rbg_run(rbg_ctx *c) {
             CU(cudaGraphLaunch(c->while_exec, c->stream));
             TRY(read_state(c, &h));
             c->iters = h.k + 1;  // iterations 0..k ran; the loop ended at the stop decision
+            c->stopped = true;
             return RBG_OK;
         }
         c->while_failed = true;  // e.g. a driver without conditional nodes: poll instead

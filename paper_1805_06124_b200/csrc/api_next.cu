@@ -68,23 +68,28 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     TRY(read_state(c, &h));
     TRY(need_settled(c, h, "add_columns"));
     const long long M0 = c->M, M1 = c->M + M_f;
+    const long long ext0 = c->M - c->M0;  // columns already in the appended segment
     double2 *Fd = nullptr;
     bool f_owned = false;
     if (M_f > 0) TRY(upload_block(c, F, M_f, ldf, F_mem, &Fd, &f_owned));
+    // The caller's columns stay where they are (a borrowed S is never copied): the appended
+    // columns go to a library-owned second segment that the sweep streams after the first
+    // (scol in kernels.h).  Only that segment, R (k_max x M row-major: rows get longer) and the
+    // per-column vectors are reallocated.
     const size_t pitch = (size_t)c->nvec * 16;
-    double2 *S1 = c->S;
+    double2 *S1n = c->S1;
     double *R1 = c->R, *r21 = c->r2;
     long long *gid1 = c->gid;
     cudaError_t e = cudaSuccess;
     if (M_f > 0) {
-        S1 = nullptr;
+        S1n = nullptr;
         R1 = nullptr;
         r21 = nullptr;
-        e = dmalloc(&S1, pitch * M1);
+        e = dmalloc(&S1n, pitch * (ext0 + M_f));
+        if (e == cudaSuccess && ext0) e = cudaMemcpyAsync(S1n, c->S1, pitch * ext0, cudaMemcpyDeviceToDevice, c->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(S1n + ext0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
         if (e == cudaSuccess) e = dmalloc(&R1, (size_t)c->k_max * M1 * c->se);
         if (e == cudaSuccess) e = dmalloc(&r21, sizeof(double) * M1);
-        if (e == cudaSuccess) e = cudaMemcpy2DAsync(S1, pitch, c->S, (size_t)c->ldv * 16, pitch, M0, cudaMemcpyDeviceToDevice, c->stream);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(S1 + M0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(R1, 0, (size_t)c->k_max * M1 * c->se, c->stream);
         if (e == cudaSuccess && h.k)
             e = cudaMemcpy2DAsync(R1, (size_t)M1 * c->se, c->R, (size_t)M0 * c->se, (size_t)M0 * c->se, h.k,
@@ -106,7 +111,7 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     if (f_owned) dfree(Fd);
     auto drop_new = [&]() {
         if (M_f > 0) {
-            dfree(S1);
+            dfree(S1n);
             dfree(R1);
             dfree(r21);
             if (gid1 != c->gid) dfree(gid1);
@@ -119,20 +124,18 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     if (c->started && M_f > 0) {
         // the new columns get R rows 0..k-1 and the recurrence residual, then the pivot
         // search restarts over all columns and the next iteration begins at the decision
-        rbg_status st = coeff_passes(c, S1 + M0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), M1, r21 + M0, h.k);
+        rbg_status st = coeff_passes(c, S1n + ext0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), M1, r21 + M0, h.k);
         if (st != RBG_OK) {
             drop_new();
             return st;
         }
     }
     if (M_f > 0) {
-        if (c->own_S) dfree(c->S);
+        dfree(c->S1);
         dfree(c->R);
         dfree(c->r2);
         if (gid1 != c->gid) dfree(c->gid);
-        c->S = S1;
-        c->own_S = true;
-        c->ldv = c->nvec;
+        c->S1 = S1n;
         c->R = R1;
         c->r2 = r21;
         c->gid = gid1;
@@ -162,6 +165,7 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
             CU(launch_maxloc(c->r2, M1, 0, c->st, c->stream));
         }
         c->resume_pending = true;
+        c->stopped = false;
         c->iters = h.k;
     }
     CU(cudaStreamSynchronize(c->stream));

@@ -55,8 +55,10 @@ struct rbg_ctx {
     bool cplx = true;
     long long N = 0, M = 0, nvec = 0, ldv = 0, ldq_v = 0;
     size_t se = 16;  // bytes per element
-    double2 *S = nullptr;
+    double2 *S = nullptr;   // the caller's columns 0..M0-1 (borrowed or a library copy)
     bool own_S = false;
+    double2 *S1 = nullptr;  // columns M0..M-1 appended by enrichment (library-owned, pitch nvec)
+    long long M0 = 0;
     double *w = nullptr;
     double2 *Q = nullptr, *WQ = nullptr;
     double *R = nullptr, *r2 = nullptr;
@@ -94,6 +96,7 @@ struct rbg_ctx {
     cudaGraphConditionalHandle cond = 0;
     bool in_while = false;
     bool while_failed = false;
+    bool stopped = false;        // the last rbg_run ended at a stop decision (host-side)
     cudaStream_t cap_stream = nullptr;   // graphs are captured here, launched on `stream`
     cudaStream_t poll_stream = nullptr;  // polled rbg_run: reads the stop flag between batches
     int *poll_h = nullptr;               // pinned host word for that read

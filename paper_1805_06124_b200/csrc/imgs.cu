@@ -69,7 +69,9 @@ struct ClusterReducer {
     int warp, lane, par;
     uint32_t phase;  // bit p: parity of the next phase to wait for on bars[p]
 
-    __device__ __forceinline__ double2 sum(double re, double im) {
+    // start: this warp's partial leaves for every CTA; finish: wait for all 64, then the tree.
+    // Work placed between the two (loads for the next steps) overlaps the DSMEM round trip.
+    __device__ __forceinline__ void start(double re, double im) {
 #pragma unroll
         for (int h = 1; h < 32; h <<= 1) {
             re = re + __shfl_xor_sync(0xffffffffu, re, h);
@@ -80,9 +82,19 @@ struct ClusterReducer {
             const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
             st_async_v2(dst, re, im, bar);
         }
+    }
+
+    __device__ __forceinline__ double2 sum(double re, double im) {
+        start(re, im);
+        return finish();
+    }
+
+    __device__ __forceinline__ double2 finish() {
         mbar_wait(&bars[par], (phase >> par) & 1u);
         phase ^= 1u << par;
-        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[par], 64 * 16);  // re-arm for n+2
+        // re-arm for n+2 by a lane that sent nothing: an arrive has release semantics, so a
+        // sender's arrive would first wait for its own st.async to land in the remote CTA
+        if (warp == 0 && lane == 31) mbar_arrive_expect_tx(&bars[par], 64 * 16);
         const double2 a = slots[par][2 * lane], b = slots[par][2 * lane + 1];
         double x = a.x + b.x, y = a.y + b.y;
 #pragma unroll
@@ -115,6 +127,14 @@ struct ClusterReducerPre {
     long long *sub = nullptr;  // RBG_DEBUG_IMGS: clocks after butterfly / CTA tree / remote wait
 
     __device__ __forceinline__ double2 sum(double re, double im) {
+        start(re, im);
+        return finish();
+    }
+
+    // start: warp butterfly, CTA pre-reduction, the CTA partial leaves for every CTA;
+    // finish: wait for the CTAS partials, then the cross-CTA tree.  Work placed between the two
+    // (loads for the next steps) overlaps the DSMEM round trip.
+    __device__ __forceinline__ void start(double re, double im) {
 #pragma unroll
         for (int h = 1; h < 32; h <<= 1) {
             re = re + __shfl_xor_sync(0xffffffffu, re, h);
@@ -136,10 +156,15 @@ struct ClusterReducerPre {
             const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
             st_async_v2(dst, t[0].x, t[0].y, bar);
         }
+    }
+
+    __device__ __forceinline__ double2 finish() {
         mbar_wait(&bars[par], (phase >> par) & 1u);
         if (sub) sub[2] = clock64();
         phase ^= 1u << par;
-        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[par], CTAS * 16);  // re-arm for n+2
+        // re-arm for n+2 by a warp that sent nothing (warp 0 sends): an arrive has release
+        // semantics and would first wait for the sender's own st.async to land remotely
+        if (warp == WPC - 1 && lane == 31) mbar_arrive_expect_tx(&bars[par], CTAS * 16);
         // the tree over the CTAS CTA partials, evaluated by every thread from shared memory
         // (broadcast reads): leaf l = slots[par][l], pairwise with ascending offsets -- the
         // nodes of the former xor-butterfly, without its dependent shuffles
@@ -246,6 +271,54 @@ __device__ __forceinline__ void axpy(double2 (&v)[MAXV], const double2 *q, int s
     }
 }
 
+// Register-operand forms (the staged slices loaded ahead of the step that uses them).
+template <bool CPLX, int MAXV>
+__device__ __forceinline__ void dot_regs(const double2 (&v)[MAXV], const double2 (&e)[MAXV], int nm, double &pr,
+                                         double &pi) {
+    pr = 0.0;
+    pi = 0.0;
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) {
+        if (m < nm) {  // DOT(WQ_i, v), CAC rule 2
+            if (CPLX) {
+                pr = fma(e[m].x, v[m].x, pr);
+                pr = fma(e[m].y, v[m].y, pr);
+                pi = fma(e[m].x, v[m].y, pi);
+                pi = fma(-e[m].y, v[m].x, pi);
+            } else {
+                pr = fma(e[m].x, v[m].x, pr);
+                pr = fma(e[m].y, v[m].y, pr);
+            }
+        }
+    }
+}
+
+template <bool CPLX, int MAXV>
+__device__ __forceinline__ void axpy_regs(double2 (&v)[MAXV], const double2 (&q)[MAXV], int nm, double2 c) {
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) {
+        if (m < nm) {  // v <- v - c q_i, CAC rule 9
+            if (CPLX) {
+                double vr = v[m].x, vi = v[m].y;
+                vr = fma(-c.x, q[m].x, vr);
+                vr = fma(c.y, q[m].y, vr);
+                vi = fma(-c.x, q[m].y, vi);
+                vi = fma(-c.y, q[m].x, vi);
+                v[m] = make_double2(vr, vi);
+            } else {
+                v[m].x = fma(-c.x, q[m].x, v[m].x);
+                v[m].y = fma(-c.x, q[m].y, v[m].y);
+            }
+        }
+    }
+}
+
+template <int MAXV>
+__device__ __forceinline__ void load_slice(double2 (&r)[MAXV], const double2 *p, int stride, int nm) {
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) r[m] = (m < nm) ? p[m * stride] : make_double2(0.0, 0.0);
+}
+
 // Basis-vector pipeline.  STAGED (D > 0): the CTA's slices of w o q_b and q_b (MAXV chunks of
 // 256 vectors: chunk m starts at vector 2048 m + 256 rank) are prefetched D MGS steps ahead
 // into shared memory by TMA bulk copies issued by a dedicated producer warp (warp 8), one
@@ -327,6 +400,10 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     __shared__ __align__(8) uint64_t s_full[DD], s_empty[DD];
     __shared__ long long s_done;
 
+    // state written by the previous decision kernel (stop, k) and the basis q_1..q_k are final
+    // before this kernel starts even as a programmatic dependent of the sweep (the sweep waits
+    // for its predecessor before it lets this grid launch); the sweep's maxloc is read only
+    // after grid_dep_wait
     const int stop0 = a.st->stop;
     if (stop0) {
         if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -339,10 +416,41 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     const uint32_t rank = cluster_ctarank();
     const int tid = threadIdx.x;
     const bool producer = tid >= THREADS;   // the last warp (D > 0 only)
+    // RBG_DEBUG_IMGS: %globaltimer of this kernel's phases (CTA 0, thread 0) at trace[257 + p]
+    unsigned long long *ts = (a.trace && rank == 0 && tid == 0) ? reinterpret_cast<unsigned long long *>(a.trace) + 257 : nullptr;
+    if (ts) ts[0] = globaltimer_ns();
     const int nvec = (int)a.nvec;
     const int u0 = (int)rank * THREADS + tid;                  // this lane's first vector
     const int nm = (!producer && u0 < nvec) ? (nvec - u0 + kLaneImgs - 1) / kLaneImgs : 0;
     const bool odd_tail = !CPLX && (a.N & 1);
+
+    const BasisPipe<MAXV, DD, THREADS> pipe{dsm, s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec};
+    const long long limit = (long long)kNuMax * k;  // MGS steps that can ever be needed
+    // stages issued before the cluster barrier (the rest by the producer loop, off the
+    // critical path: each stage is 2 MAXV bulk copies issued by one thread)
+    const long long first = k < a.k_max ? (limit < 2 ? limit : (DD < 2 ? DD : 2)) : 0;
+    if (tid == 0) {
+        mbar_init_nofence(&s_bars[0], 1);
+        mbar_init_nofence(&s_bars[1], 1);
+        fence_mbarrier_init();
+        mbar_arrive_expect_tx(&s_bars[0], (PRE ? CTAS : 64) * 16);
+        mbar_arrive_expect_tx(&s_bars[1], (PRE ? CTAS : 64) * 16);
+        s_done = -1;
+    }
+    if (D > 0 && tid == THREADS) {
+        for (int i = 0; i < DD; i++) {
+            mbar_init_nofence(&s_full[i], 1);
+            mbar_init_nofence(&s_empty[i], THREADS / 32);
+        }
+        fence_mbarrier_init();
+        for (long long s = 0; s < first; s++) pipe.issue(s);
+    }
+    // every CTA has read the state before rank 0 changes it, and every CTA's mbarriers are
+    // initialised before any remote st.async can target them
+    cluster_sync_all();
+    if (ts) ts[1] = globaltimer_ns();
+    grid_dep_wait();
+    if (ts) ts[2] = globaltimer_ns();
 
     // ---- a3: pivot decision (identical in every CTA and on every rank) ------------------
     double m;
@@ -355,26 +463,6 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     else if (err < a.tol) why = kStopTol;
     else if (k == a.k_max) why = kStopKmax;
 
-    const BasisPipe<MAXV, DD, THREADS> pipe{dsm, s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec};
-    const long long limit = (long long)kNuMax * k;  // MGS steps that can ever be needed
-    if (tid == 0) {
-        mbar_init(&s_bars[0], 1);
-        mbar_init(&s_bars[1], 1);
-        mbar_arrive_expect_tx(&s_bars[0], (PRE ? CTAS : 64) * 16);
-        mbar_arrive_expect_tx(&s_bars[1], (PRE ? CTAS : 64) * 16);
-        s_done = -1;
-    }
-    if (D > 0 && tid == THREADS) {
-        for (int i = 0; i < DD; i++) {
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], THREADS / 32);
-        }
-        if (why == kStopNone)
-            for (long long s = 0; s < DD && s < limit; s++) pipe.issue(s);
-    }
-    // every CTA has read the state before rank 0 changes it, and every CTA's mbarriers are
-    // initialised before any remote st.async can target them
-    cluster_sync_all();
     const bool leader = (rank == 0 && tid == 0);
     if (leader) a.errors[k] = err;
     if (why != kStopNone) {
@@ -382,10 +470,12 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
             a.st->stop = why;
             loop_exit(a.cond, a.use_cond);
         }
+        if (D > 0 && tid == THREADS)  // no copy may outlive the CTA
+            for (long long s = 0; s < first; s++) mbar_wait_guarded(&s_full[s], 0u, 4, s);
         return;
     }
     if (producer) {
-        if (D > 0 && tid == THREADS) pipe.produce(DD < limit ? DD : limit, limit, &s_done);
+        if (D > 0 && tid == THREADS) pipe.produce(first, limit, &s_done);
         return;
     }
 
@@ -403,6 +493,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     Red red = make_reducer<Red>(s_slots, s_wp, s_bars, rank, warp, lane);
     const uint64_t keep = policy_evict_last();
     const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
+    if (ts) ts[3] = globaltimer_ns();
     double n_prev = n0, nn = 0.0;
     int nu = 0;
     bool accepted = false;
@@ -416,6 +507,13 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
             q[mm] = (mm < nm) ? ld_keep(a.Q + u0 + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
         }
     }
+    // staged path: the slice of w o q_s is in registers before step s begins (loaded while the
+    // partials of step s - 1 were in flight), q_s is loaded while those of step s travel
+    double2 wqr[MAXV];
+    if (D > 0 && k > 0) {
+        mbar_wait(&s_full[0], 0u);
+        load_slice<MAXV>(wqr, pipe.wq_stage(0) + tid, THREADS, nm);
+    }
     while (nu < kNuMax) {
         nu++;
         for (long long i = 0; i < k; i++, s++) {
@@ -424,23 +522,41 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
             if (D > 0) {
                 // RBG_DEBUG_IMGS: clock64 at the phase boundaries of steps 64..95 (CTA 0, tid 0)
                 const bool tr = a.trace && rank == 0 && tid == 0 && s >= 64 && s < 96;
-                long long c0 = tr ? clock64() : 0;
-                mbar_wait(&s_full[s % DD], (uint32_t)((s / DD) & 1));
-                long long c1 = tr ? clock64() : 0;
-                dot_partial<CPLX, MAXV>(v, pipe.wq_stage(s) + tid, THREADS, nm, pr, pi);
-                long long c2 = tr ? clock64() : 0;
+                // every CTA's %globaltimer at step start / partial sent / coefficient known for
+                // steps 64..71 (trace[512 + (rank*8 + step)*3 + p]): the cluster's critical path
+                unsigned long long *gt = (a.trace && tid == 0 && s >= 64 && s < 72)
+                                             ? reinterpret_cast<unsigned long long *>(a.trace) + 512 + (rank * 8 + (s - 64)) * 3
+                                             : nullptr;
+                if (gt) gt[0] = globaltimer_ns();
+                const long long c0 = tr ? clock64() : 0;
+                dot_regs<CPLX, MAXV>(v, wqr, nm, pr, pi);
+                const long long c1 = tr ? clock64() : 0;
                 long long sb[3] = {0, 0, 0};
                 if constexpr (PRE) red.sub = tr ? sb : nullptr;
-                c = red.sum(pr, pi);
-                long long c3 = tr ? clock64() : 0;
-                axpy<CPLX, MAXV>(v, pipe.q_stage(s) + tid, THREADS, nm, c);
+                red.start(pr, pi);
+                if (gt) gt[1] = globaltimer_ns();
+                const long long c2 = tr ? clock64() : 0;
+                // while the partials travel: q_s and the next stage's w o q into registers
+                double2 qr[MAXV];
+                load_slice<MAXV>(qr, pipe.q_stage(s) + tid, THREADS, nm);
+                if (s + 1 < limit) {
+                    mbar_wait(&s_full[(s + 1) % DD], (uint32_t)(((s + 1) / DD) & 1));
+                    load_slice<MAXV>(wqr, pipe.wq_stage(s + 1) + tid, THREADS, nm);
+                }
+                const long long c3 = tr ? clock64() : 0;
+                c = red.finish();
+                if (gt) gt[2] = globaltimer_ns();
+                const long long c4 = tr ? clock64() : 0;
+                axpy_regs<CPLX, MAXV>(v, qr, nm, c);
+                // stage s consumed (the axpy used q_s); lane 31 never issues st.async, so its
+                // release-arrive does not wait for a remote store
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&s_empty[s % DD]);  // this warp is done with the stage
+                if (lane == 31) mbar_arrive(&s_empty[s % DD]);
                 if (tr) {
-                    const long long c4 = clock64();
+                    const long long c5 = clock64();
                     long long *t = a.trace + (s - 64) * 8;
-                    t[0] = c0; t[1] = c1; t[2] = c2; t[3] = c3; t[4] = c4;
-                    t[5] = sb[0]; t[6] = sb[1]; t[7] = sb[2];
+                    t[0] = c0; t[1] = c1; t[2] = c2; t[3] = c3; t[4] = c4; t[5] = c5;
+                    t[6] = sb[1]; t[7] = sb[2];
                 }
             } else {
                 dot_partial<CPLX, MAXV>(v, wq, 1, nm, pr, pi);
@@ -469,6 +585,10 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
         n_prev = nn;
     }
     if (tid == 0) s_done = s;  // release the producer: it drains the copies it issued
+    if (ts) ts[4] = globaltimer_ns();
+    // the next sweep may now take the SMs this cluster does not use (earlier, its first loads
+    // would compete with the latency-bound reductions for the memory system)
+    grid_dep_launch();
     const double delta = 1000.0 * 0x1p-52;
     if (!accepted || !(nn >= delta * n0) || nn == 0.0) {
         if (leader) {
@@ -497,6 +617,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
         }
     }
     if (leader) {
+        if (ts) ts[5] = globaltimer_ns();
         a.piv[k] = J;
         a.nu[k] = nu;
         a.rdiag[k] = nn;
@@ -560,13 +681,18 @@ static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
     cfg.blockDim = dim3(THREADS + 32, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CTAS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch after the sweep: the cluster's prologue (barriers, the
+    // producer's first basis copies) runs while the sweep drains; grid_dep_wait before the
+    // decision reads the sweep's maxloc
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = a.pdl ? 2 : 1;
     e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -12,8 +12,10 @@ namespace rbg {
 
 // Fused column sweep (a0 init norms / a2 coefficient sweep + residual update + maxloc).
 struct SweepArgs {
-    const double2 *S;      // snapshot block as 16-byte vectors, column j at S + j*ldv
+    const double2 *S;      // snapshot block as 16-byte vectors, column j < M0 at S + j*ldv
     long long ldv;         // column stride in vectors
+    const double2 *S1;     // columns appended by enrichment (j >= M0) at S1 + (j - M0)*nvec
+    long long M0;          // columns of the first segment (== M when nothing was appended)
     long long M;           // local columns
     long long N;           // rows (elements)
     long long nvec;        // vectors per column: complex N, real ceil(N/2)
@@ -41,7 +43,17 @@ struct SweepArgs {
                             // sharded context (sorted ascending), else NULL: col_offset + local
     cudaGraphConditionalHandle cond;  // rbg_run's device loop (loop_exit), valid when use_cond
     int use_cond;
+    int pdl;  // launch as a programmatic dependent of the preceding kernel (k_sweep_dyn only)
+    int tail_pf;  // k_sweep_dyn: warps out of columns prefetch the last columns into L2
+    unsigned long long *tstamp;  // RBG_DEBUG_IMGS: %globaltimer when the last CTA finished (else NULL)
 };
+
+// Column j of the local snapshot block: the caller's matrix for j < M0, the library-owned
+// segment of appended columns (enrichment) after it -- so an append never copies S.
+__device__ __forceinline__ const double2 *scol(const double2 *S, long long ldv, const double2 *S1, long long M0,
+                                               long long nvec, long long j) {
+    return j < M0 ? S + j * ldv : S1 + (j - M0) * nvec;
+}
 
 // Global index of local column j (sweep records).
 __device__ __forceinline__ long long global_col(const SweepArgs &a, long long j) {
@@ -58,6 +70,8 @@ __host__ __device__ inline unsigned long long peer_tag(unsigned long long epoch,
 struct ImgsArgs {
     const double2 *S;
     long long ldv;
+    const double2 *S1;  // appended columns (see SweepArgs)
+    long long M0;
     long long N, nvec;
     const double *w;
     double2 *Q, *WQ;
@@ -81,9 +95,11 @@ struct ImgsArgs {
     const unsigned char *peer_send[kMaxPeers];
     size_t peer_slot;
     const long long *gid;  // as SweepArgs::gid (the owner masks its selected local column)
-    long long *trace;      // RBG_DEBUG_IMGS: per-phase clock64 of 32 MGS steps (else NULL)
+    long long *trace;      // RBG_DEBUG_IMGS: per-phase clock64 of 32 MGS steps, then the
+                           // %globaltimer of the kernel's phases at trace[257..] (else NULL)
     cudaGraphConditionalHandle cond;  // rbg_run's device loop (loop_exit), valid when use_cond
     int use_cond;
+    int pdl;  // launch as a programmatic dependent of the preceding sweep (MGS kernel)
 };
 
 // Local index of global column J on this rank, -1 if another rank owns it.
@@ -125,7 +141,7 @@ __device__ __forceinline__ void pivot_decision(const ImgsArgs &a, long long k, d
     } else if (!a.xchg) {
         m = a.st->m_loc;
         J = a.st->j_loc;
-        src = a.S + (J - a.col_offset) * a.ldv;
+        src = scol(a.S, a.ldv, a.S1, a.M0, a.nvec, J - a.col_offset);
     } else {
         m = -INFINITY;
         J = 0x7fffffffffffffffLL;

@@ -24,9 +24,12 @@
 //    total order (value desc, index asc) into the device state, and on a sharded run packs
 //    the local candidate column into the exchange slot.
 // Sweep 0 (INIT) is the same kernel with e~ = w and the weighted norm of CAC rule 4.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "kernels.h"
 
@@ -139,6 +142,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
             const long long jg = global_col(a, bj);
             a.st->m_loc = bm;
             a.st->j_loc = jg;
+            if (a.tstamp) *a.tstamp = globaltimer_ns();
             *a.ticket = 0u;
             if (a.next_col) *a.next_col = 0ull;  // every warp has taken its last column
             if (a.send) {
@@ -148,6 +152,14 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
             }
             s_m[1] = bm;
             s_j[1] = jg;
+            if (!a.send && bj >= 0 && bj < a.M) {
+                // one GPU: the decision kernel's first read is this column (streamed with
+                // evict-first a while ago): pull it into L2 now (16-byte aligned, whole column)
+                const char *col = reinterpret_cast<const char *>(scol(a.S, a.ldv, a.S1, a.M0, a.nvec, bj));
+                const size_t bytes = (size_t)nvec * 16;
+                for (size_t off = 0; off < bytes; off += 32768)
+                    prefetch_l2(col + off, (uint32_t)((bytes - off) < 32768 ? (bytes - off) : 32768));
+            }
         }
         if (a.send) s_j[0] = bj;
     }
@@ -157,7 +169,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, double best_m, 
         double2 *dst = reinterpret_cast<double2 *>(send_slot(a) + sizeof(Rec));
         const bool valid = bj >= 0 && bj < a.M;
         for (long long u = tid; u < nvec; u += blockDim.x) {
-            double2 x = valid ? a.S[bj * a.ldv + u] : make_double2(0.0, 0.0);
+            double2 x = valid ? scol(a.S, a.ldv, a.S1, a.M0, a.nvec, bj)[u] : make_double2(0.0, 0.0);
             if (odd_tail && u == nvec - 1) x.y = 0.0;
             dst[u] = x;
         }
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const SweepArgs a) {
     bool waited = !ESMEM;
 
     for (long long c = c_begin + warp; c < c_end; c += kSweepWarps) {
-        const double2 *col = a.S + c * a.ldv;
+        const double2 *col = scol(a.S, a.ldv, a.S1, a.M0, a.nvec, c);
         double re = 0.0, im = 0.0;
         // ring of U 16-byte loads in flight per lane: slot t is consumed, then immediately
         // refilled with the vector U*32 further down the column
@@ -382,14 +394,30 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar;
 
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long nvec = a.nvec;
+    const bool odd_tail = !CPLX && (a.N & 1);
+    const uint64_t pol = policy_evict_first();
+    const int nv = (int)nvec;
+    const long long M = a.M;
+    // the first column of this warp and its first group of U loads: the snapshot matrix is
+    // never written by the greedy, so with a programmatic dependent launch these loads are in
+    // flight while the predecessor (the decision / IMGS kernel) is still running
+    long long colA = (long long)blockIdx.x * kSweepWarps + warp;
+    double2 xr[U];
+    {
+        const double2 *lp = scol(a.S, a.ldv, a.S1, a.M0, a.nvec, colA) + lane;
+#pragma unroll
+        for (int t = 0; t < U; t++)
+            xr[t] = (colA < M && t * 32 + lane < nv) ? ld_stream(lp + t * 32, pol) : make_double2(0.0, 0.0);
+    }
+    grid_dep_wait();  // the state, q_{k-1}, r2 and the column counter are the predecessor's
     if (a.st->stop) {
         if (threadIdx.x == 0 && blockIdx.x == 0) loop_exit(a.cond, a.use_cond);
         return;
     }
+    grid_dep_launch();
     const long long k = a.qi >= 0 ? a.qi + 1 : a.st->k;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long nvec = a.nvec;
-    const bool odd_tail = !CPLX && (a.N & 1);
 
     const double2 *Eg = INIT ? reinterpret_cast<const double2 *>(a.w) : a.WQ + (k - 1) * a.ldq_v;
     const double2 *E = Eg;
@@ -410,14 +438,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
         Ew = reinterpret_cast<const double *>(smem);
     }
 
-    const uint64_t pol = policy_evict_first();
-    const int nv = (int)nvec;
     const int gpc = (int)((nvec + 32 * U - 1) / (32 * U));  // groups of U trips per column
-    const long long M = a.M;
     const long long nwg = (long long)gridDim.x * kSweepWarps;
     // column window of this warp: A = being consumed, B = next, pend = the one after (raw
     // counter value held by lane 0, shuffled out only at the next shift)
-    long long colA = (long long)blockIdx.x * kSweepWarps + warp;
     unsigned long long raw = 0;
     if (lane == 0) raw = atomicAdd(a.next_col, 1ull);
     long long colB = (long long)__shfl_sync(0xffffffffu, raw, 0) + nwg;
@@ -425,14 +449,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
     if (lane == 0) praw = atomicAdd(a.next_col, 1ull);
 
     // the issue cursor is always exactly one group ahead of the consume cursor (group cg of
-    // colA): group cg + 1 of colA, or group 0 of colB when cg is colA's last group
-    double2 xr[U];
-    {
-        const double2 *lp = a.S + colA * a.ldv + lane;
-#pragma unroll
-        for (int t = 0; t < U; t++)
-            xr[t] = (colA < M && t * 32 + lane < nv) ? ld_stream(lp + t * 32, pol) : make_double2(0.0, 0.0);
-    }
+    // colA): group cg + 1 of colA, or group 0 of colB when cg is colA's last group (group 0 of
+    // colA was issued before grid_dep_wait)
     if (ESMEM) mbar_wait(&mbar, 0);
 
     double best_m = -INFINITY;
@@ -447,7 +465,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
         const int lgrp = last ? 0 : cg + 1;
         const int lu0 = lgrp * 32 * U + lane;
         const int cu0 = cg * 32 * U + lane;
-        const double2 *lp = a.S + lc * a.ldv + lu0;
+        const double2 *lp = scol(a.S, a.ldv, a.S1, a.M0, a.nvec, lc) + lu0;
         const bool lvalid = lc < M;
 #pragma unroll
         for (int t = 0; t < U; t++) {
@@ -496,6 +514,20 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
         colB = (long long)__shfl_sync(0xffffffffu, praw, 0) + nwg;
         if (lane == 0) praw = atomicAdd(a.next_col, 1ull);
     }
+    // Tail: this warp's column claims are exhausted; colA is its first claim past M (claims are
+    // handed out in order, so X = colA - M earlier claims were also past M).  The columns claimed
+    // last, M-1, M-2, ..., are being started by their warps about now, and a lone warp streams
+    // a column at its latency-bound rate: pull column 2M-1-colA (one per exhausted claim, the
+    // last claimed first) into L2 so its owner's loads hit L2.  No arithmetic changes.
+    if (a.tail_pf && lane == 0) {
+        const long long P = 2 * M - 1 - colA;
+        if (P >= 0 && P < M && P >= M - nwg) {
+            const char *col = reinterpret_cast<const char *>(scol(a.S, a.ldv, a.S1, a.M0, a.nvec, P));
+            const size_t bytes = (size_t)nvec * 16 < 65536 ? (size_t)nvec * 16 : 65536;
+            for (size_t off = 0; off < bytes; off += 32768)
+                prefetch_l2(col + off, (uint32_t)((bytes - off) < 32768 ? (bytes - off) : 32768));
+        }
+    }
     sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
 }
 
@@ -505,8 +537,9 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
     const size_t ebytes = (init && cplx) ? ((size_t)nvec * 8 + 15) / 16 * 16 : (size_t)nvec * 16;
     c.esmem = ebytes <= kSmemLimit;
     c.smem = c.esmem ? ebytes : 0;
+    // at most two CTAs per SM when the staged vector is small enough; launch_t clamps this to
+    // the kernel's real occupancy (a 512-thread CTA at 128 registers fills the register file)
     int per_sm = 1;
-    // more CTAs per SM only when the staged vector is small enough
     if (c.smem * 2 + 4096 <= 227 * 1024) per_sm = 2;
     (void)device;
     c.grid = num_sms * per_sm;
@@ -531,6 +564,25 @@ static SweepKernel pick_kernel(bool dyn) {
     return dyn ? k_sweep_dyn<CPLX, INIT, ESMEM, U> : k_sweep<CPLX, INIT, ESMEM, U>;
 }
 
+// CTAs of `kern` that fit on the device at once (occupancy x SMs), cached per kernel and
+// shared-memory size; `cap` if the query fails.
+static int resident_ctas(const void *kern, int threads, size_t smem, int cap) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, size_t>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(kern, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int dev = 0, sms = 0, occ = 0;
+    int r = cap;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) == cudaSuccess && occ > 0)
+        r = sms * occ;
+    cache[key] = r;
+    return r;
+}
+
 template <bool CPLX, bool INIT, bool ESMEM>
 static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStream_t s) {
     // RBG_SWEEP_KIND = dyn (default) | percol (k_sweep, static column blocks; the explicit mode's kernel)
@@ -551,10 +603,29 @@ static cudaError_t launch_t(const SweepArgs &a, const SweepConfig &cfg, cudaStre
     }
     // no more CTAs than the columns can occupy (one warp per column at least): a small M
     // does not pay 296 CTAs' staging of e~ and a 296-record maxloc (same bits: the per-column
-    // arithmetic does not depend on the grid and the maxloc is a total order)
+    // arithmetic does not depend on the grid and the maxloc is a total order); and no more than
+    // one wave: CTAs of a second wave would find the dynamic column counter exhausted
     const long long need = (a.M + kSweepWarps - 1) / kSweepWarps;
-    const int grid = (int)(need < 1 ? 1 : (need < cfg.grid ? need : cfg.grid));
-    kern<<<grid, cfg.threads, cfg.smem, s>>>(a);
+    int grid = (int)(need < 1 ? 1 : (need < cfg.grid ? need : cfg.grid));
+    grid = std::min(grid, resident_ctas((const void *)kern, cfg.threads, cfg.smem, cfg.grid));
+    if (!(a.pdl && dyn && !INIT)) {
+        kern<<<grid, cfg.threads, cfg.smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    // programmatic dependent launch: the first loads of S are issued while the preceding
+    // decision / IMGS kernel finishes (k_sweep_dyn waits for it in grid_dep_wait)
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid, 1, 1);
+    lc.blockDim = dim3(cfg.threads, 1, 1);
+    lc.dynamicSmemBytes = cfg.smem;
+    lc.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -189,7 +189,11 @@ def sharded_enrich(ctx, V_local, tol: float, rounds: int = 3, group=None, M_glob
     Returns (per-round max validation error over all ranks, passed)."""
     import numpy as np
     import torch.distributed as dist
-    Vh = V_local.cpu().numpy() if hasattr(V_local, "cpu") else np.asarray(V_local)
+    from . import rbg
+    if hasattr(V_local, "is_cuda") and V_local.is_cuda:
+        Vh = V_local                                   # validated in place, gathered on the device
+    else:
+        Vh = V_local.cpu().numpy() if hasattr(V_local, "cpu") else np.asarray(V_local)
     added = np.zeros(Vh.shape[0], bool)
     history = []
     total = M_global if M_global is not None else ctx.M_global
@@ -206,7 +210,7 @@ def sharded_enrich(ctx, V_local, tol: float, rounds: int = 3, group=None, M_glob
             passed = all(all_gather_bytes(bool(np.all(err < tol)), group))
             return history, passed
         first, total_new = enrich_plan(counts, dist.get_rank(group), total)
-        ctx.add_columns(Vh[fail], first_gid=first, M_global=total_new)
+        ctx.add_columns(rbg._rows(Vh, fail), first_gid=first, M_global=total_new)
         total = total_new
         added |= fail
         ctx.run()

@@ -478,11 +478,21 @@ class Context:
                       R=self.R() if full else None, r2=self.r2() if full else None)
 
 
+def _rows(V, mask: np.ndarray):
+    """The rows of V selected by a host boolean mask (gathered on V's device)."""
+    if _is_torch(V):
+        import torch
+        return V[torch.as_tensor(np.nonzero(mask)[0], device=V.device)]
+    return V[mask]
+
+
 def enrich(ctx: Context, V, tol: float, rounds: int = 3):
     """Iterative refinement (SPEC enrich): validate V against the basis,
     append every failing column (err >= tol) not appended before, continue the greedy, and
-    repeat up to `rounds` times.  Returns (per-round max validation error, passed)."""
-    Vh = V.cpu().numpy() if _is_torch(V) else np.asarray(V)
+    repeat up to `rounds` times.  A CUDA tensor V stays on the device: it is validated in
+    place and its failing columns are gathered on the device.  Returns (per-round max
+    validation error, passed)."""
+    Vh = V if (_is_torch(V) and V.is_cuda) else (V.cpu().numpy() if _is_torch(V) else np.asarray(V))
     added = np.zeros(Vh.shape[0], bool)
     history = []
     for _ in range(rounds):
@@ -491,7 +501,7 @@ def enrich(ctx: Context, V, tol: float, rounds: int = 3):
         fail = (err >= tol) & ~added
         if not fail.any():
             return history, bool(np.all(err < tol))
-        ctx.add_columns(Vh[fail])
+        ctx.add_columns(_rows(Vh, fail))
         added |= fail
         ctx.run()
     err = ctx.validate(Vh)

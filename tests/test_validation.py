@@ -181,6 +181,44 @@ def test_gpu_running_greedy_refuses_r_readers(orc):
         ctx.gram()                                   # settled: the new columns have all rows
 
 
+@pytest.mark.gpu
+def test_gpu_enrichment_device_v_borrowed_s_not_copied(orc):
+    """Enrichment with a device validation set and a borrowed device S: the
+    appended columns go to a second, library-owned segment that the sweep streams after the
+    caller's columns -- S is never copied (device memory grows by the appended columns and the
+    longer R rows only) -- and the run equals the oracle's enrichment bit for bit."""
+    import torch
+
+    from paper_1805_06124_b200 import rbg
+    S, V, w = _sets(M_train=60)
+    tol = 1e-5
+    res, _, hist_o, ok_o = orc.enrich(S, V, w, tol, 150, rounds=4)
+    St = torch.as_tensor(S, device="cuda")
+    Vt = torch.as_tensor(V, device="cuda")
+    with rbg.Context(St, w, tol, 150) as ctx:
+        ctx.run()
+        hist, ok = rbg.enrich(ctx, Vt, tol, rounds=4)
+        g = ctx.result()
+    assert ok == ok_o and hist == hist_o
+    assert (g.k, g.stop) == (res.k, res.stop)
+    for key in ("pivots", "errors", "nu", "Q", "R", "r2"):
+        np.testing.assert_array_equal(getattr(g, key), getattr(res, key))
+    # memory: a 1.3 GB borrowed S, 64 appended columns
+    N, M = 2000, 40960
+    big, wb, _, _ = inputs.config1(M=M, N=N)
+    Bt = torch.as_tensor(big, device="cuda")
+    F = Bt[:64].clone() * (1.0 + 1e-3)
+    with rbg.Context(Bt, wb, 0.0, 20) as ctx:
+        ctx.run()
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        ctx.add_columns(F)
+        free1 = torch.cuda.mem_get_info()[0]
+        ctx.run()
+        assert ctx.info()[0] == 20 and ctx.R().shape == (20, M + 64)
+    assert free0 - free1 < 0.1 * Bt.numel() * 16, (free0 - free1) / 1e9
+
+
 def _drive(rbg, ctxs, mode, n):
     for _ in range(n):
         for c in ctxs:
