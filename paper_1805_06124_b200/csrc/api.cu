@@ -92,9 +92,28 @@ void free_ctx(rbg_ctx *c) {
                 n++;
                 busy += b / have;
             }
-            if (n > 1)
+            if (n > 1) {
                 fprintf(stderr, "rbg: imgs cluster (ns/step): send skew across CTAs %.0f, last send -> last coefficient %.0f, "
                                 "step start -> send %.0f, step %.0f\n", skew / n, lat / n, busy / n, step / (n - 1));
+                // per CTA: mean send time and coefficient time relative to the step's first send
+                fprintf(stderr, "rbg: imgs per CTA (ns after the first send: send / coefficient):");
+                for (int r = 0; r < 16; r++) {
+                    double ds = 0, dc = 0;
+                    int m = 0;
+                    for (int st = 0; st < 8; st++) {
+                        unsigned long long smin = ~0ull;
+                        for (int q = 0; q < 16; q++)
+                            if (gt[(q * 8 + st) * 3 + 1]) smin = std::min(smin, gt[(q * 8 + st) * 3 + 1]);
+                        const unsigned long long *g = gt + (r * 8 + st) * 3;
+                        if (!g[1] || smin == ~0ull) continue;
+                        ds += (double)(g[1] - smin);
+                        dc += (double)(g[2] - smin);
+                        m++;
+                    }
+                    if (m) fprintf(stderr, " %d:%.0f/%.0f", r, ds / m, dc / m);
+                }
+                fprintf(stderr, "\n");
+            }
         }
         // %globaltimer (ns): [256] sweep's last CTA done, [257] IMGS entry, [258] cluster synced,
         // [259] after grid_dep_wait, [260] n0 known, [261] MGS sweeps done, [262] q stored
