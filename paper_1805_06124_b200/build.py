@@ -17,7 +17,7 @@ INC = os.path.join(ROOT, "include")
 OUT = os.path.join(PKG, "librbg.so")
 BUILD = os.path.join(PKG, "build")
 
-SOURCES = ["sweep.cu", "imgs.cu", "imgs_cta.cu", "imgs_cgs.cu", "recon.cu", "eim.cu", "coeff.cu", "api.cu", "api_next.cu", "gen.cu", "peer.cu", "devmem.cu", "comm.cpp"]
+SOURCES = ["sweep.cu", "imgs.cu", "imgs_cgs.cu", "recon.cu", "eim.cu", "coeff.cu", "api.cu", "api_next.cu", "gen.cu", "peer.cu", "devmem.cu", "comm.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",

@@ -284,8 +284,6 @@ rbg_status enqueue_finish(rbg_ctx *c) {
     NvtxRange range("rbg.imgs");
     if (c->ortho == RBG_ORTHO_CGS)
         CU(launch_imgs_cgs(imgs_args(c), c->cplx, c->cgs_v, c->cgs_c, c->cgs_grid, c->stream));
-    else if (c->imgs_cta && !c->imgs_trace)
-        CU(launch_imgs_cta(imgs_args(c), c->cplx, c->cta_maps, c->stream));
     else
         CU(launch_imgs(imgs_args(c), c->cplx, c->stream));
     return RBG_OK;
@@ -770,11 +768,6 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(dmalloc(&c->nu, sizeof(int) * c->k_max));
     CUB(cudaMemsetAsync(c->nu, 0, sizeof(int) * c->k_max, c->stream));
     c->ortho = d->ortho;
-    // short vectors (configs 0, 1, 4): IMGS in one CTA (same lanes and tree, same bits)
-    if (c->ortho == RBG_ORTHO_MGS && imgs_cta_fits(nvec)) {
-        CUB(make_imgs_cta_maps(c->WQ, c->Q, nvec, c->ldq_v, c->k_max, c->cta_maps));
-        c->imgs_cta = true;
-    }
     if (c->ortho == RBG_ORTHO_CGS) {
         CUB(dmalloc(&c->cgs_v, (size_t)nvec * 16));
         CUB(dmalloc(&c->cgs_c, sizeof(double2) * (size_t)c->k_max));

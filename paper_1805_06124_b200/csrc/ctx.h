@@ -101,8 +101,6 @@ struct rbg_ctx {
     cudaStream_t poll_stream = nullptr;  // polled rbg_run: reads the stop flag between batches
     int *poll_h = nullptr;               // pinned host word for that read
     rbg_ortho ortho = RBG_ORTHO_MGS;
-    bool imgs_cta = false;                      // short vectors: the single-CTA IMGS kernel
-    alignas(64) unsigned char cta_maps[256] = {};  // its tensor maps of WQ and Q
     bool xmode = false;          // explicit residuals (Algorithm 2 updates)
     double *w_true = nullptr;    // explicit mode: the caller's weights (w holds ones)
     double2 *cgs_v = nullptr, *cgs_c = nullptr;

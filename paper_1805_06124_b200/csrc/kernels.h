@@ -182,12 +182,6 @@ int imgs_maxv(long long nvec);  // 0 if unsupported
 int cgs_grid(int num_sms);
 cudaError_t launch_imgs_cgs(const ImgsArgs &a, bool cplx, double2 *vbuf, double2 *cbuf, int grid, cudaStream_t s);
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s);
-// Single-CTA IMGS for nvec <= 2048, nvec % 8 == 0 (imgs_cta.cu): the same bits as launch_imgs.
-// maps: 2 CUtensorMap (256 bytes, 64-byte aligned) of WQ and Q, from make_imgs_cta_maps.
-bool imgs_cta_fits(long long nvec);
-cudaError_t make_imgs_cta_maps(const double2 *WQ, const double2 *Q, long long nvec, long long ldq_v, long long k_max,
-                               void *maps);
-cudaError_t launch_imgs_cta(const ImgsArgs &a, bool cplx, const void *maps, cudaStream_t s);
 // Explicit mode: V = W^{1/2} S and Q = Q~ / W^{1/2} (sweep.cu).
 cudaError_t launch_scale_sqrtw(double2 *V, long long ldv, const double2 *S, long long lds, long long M, long long nvec,
                                long long N, const double *w, bool cplx, cudaStream_t s);

@@ -176,35 +176,6 @@ def test_device_loop_stops_without_tail(rbg, orc, ortho):
         assert 0 <= ctx.stats().noop_iters <= 32
 
 
-def test_imgs_single_cta_and_cluster_agree(rbg, orc, tmp_path):
-    """Short vectors (nvec <= 2048, nvec % 8 == 0) take the single-CTA IMGS kernel
-    (csrc/imgs_cta.cu: same 2048 lanes and tree, another thread mapping); RBG_IMGS_CLUSTER=1
-    forces the 16-CTA cluster kernel.  Both give the oracle's bits (complex and real, with the
-    nvec = 2048 edge and a RANK stop)."""
-    import os
-    import subprocess
-    import sys
-    cases = {"cplx": inputs.config1(M=3000, N=2000), "real": inputs.config0(),
-             "real2048": inputs.make(4, M=3000, N=4096, r=400)}
-    for name, (S, w, tol, k_max) in cases.items():
-        np.save(tmp_path / f"{name}_S.npy", S)
-        np.save(tmp_path / f"{name}_w.npy", w)
-        g = rbg.greedy(S, w, tol, k_max)
-        o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
-        compare(g, o)
-        code = (f"import sys, numpy as np; sys.path.insert(0, {repr(os.getcwd())}); "
-                "from paper_1805_06124_b200 import rbg; "
-                f"S = np.load({repr(str(tmp_path / f'{name}_S.npy'))}); w = np.load({repr(str(tmp_path / f'{name}_w.npy'))}); "
-                f"r = rbg.greedy(S, w, {tol!r}, {k_max}); "
-                f"np.savez({repr(str(tmp_path / f'{name}_out.npz'))}, pivots=r.pivots, errors=r.errors, Q=r.Q, R=r.R, nu=r.nu)")
-        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RBG_IMGS_CLUSTER="1"),
-                             capture_output=True, text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        c = np.load(tmp_path / f"{name}_out.npz")
-        for key in ("pivots", "errors", "Q", "R", "nu"):
-            np.testing.assert_array_equal(c[key], getattr(g, key))
-
-
 def test_step_api_and_timing_identity(rbg):
     """rbg_step enqueues iterations; the cost-model identity T = T_sweep + T_xchg + T_IMGS
      holds to 1% from the library's own events."""
