@@ -519,13 +519,16 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_dyn(const SweepArgs 
     // last, M-1, M-2, ..., are being started by their warps about now, and a lone warp streams
     // a column at its latency-bound rate: pull column 2M-1-colA (one per exhausted claim, the
     // last claimed first) into L2 so its owner's loads hit L2.  No arithmetic changes.
-    if (a.tail_pf && lane == 0) {
+    // Only for columns of <= 64 KB (configs 0, 1, 4: a column is a few us of one warp's stream):
+    // on config 2's 160 KB columns the owners are mid-column by then and a whole-column prefetch
+    // re-reads their first part (ncu: +110 MB per sweep, no gain).
+    if (a.tail_pf && lane == 0 && nvec * 16 <= 65536) {
         const long long P = 2 * M - 1 - colA;
         if (P >= 0 && P < M && P >= M - nwg) {
             const char *col = reinterpret_cast<const char *>(scol(a.S, a.ldv, a.S1, a.M0, a.nvec, P));
-            const size_t bytes = (size_t)nvec * 16 < 65536 ? (size_t)nvec * 16 : 65536;
-            for (size_t off = 0; off < bytes; off += 32768)
-                prefetch_l2(col + off, (uint32_t)((bytes - off) < 32768 ? (bytes - off) : 32768));
+            const uint32_t bytes = (uint32_t)(nvec * 16);
+            for (uint32_t off = 0; off < bytes; off += 32768)
+                prefetch_l2(col + off, (bytes - off) < 32768u ? (bytes - off) : 32768u);
         }
     }
     sweep_finish<CPLX>(a, best_m, best_j, odd_tail);
