@@ -250,8 +250,6 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.cond = c->cond;
     a.use_cond = c->in_while ? 1 : 0;
     a.pdl = (pdl_enabled(c) && c->comm == RBG_COMM_NONE && c->started) ? 1 : 0;
-    static const bool late = getenv("RBG_PDL_LATE") != nullptr;
-    a.late_launch = late ? 1 : 0;
     return a;
 }
 

@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     if (ts) ts[4] = globaltimer_ns();
     // the next sweep may now take the SMs this cluster does not use (earlier, its first loads
     // would compete with the latency-bound reductions for the memory system)
-    if (!a.late_launch) grid_dep_launch();
+    grid_dep_launch();
     const double delta = 1000.0 * 0x1p-52;
     if (!accepted || !(nn >= delta * n0) || nn == 0.0) {
         if (leader) {
@@ -616,7 +616,6 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
             }
         }
     }
-    if (a.late_launch) grid_dep_launch();
     if (leader) {
         if (ts) ts[5] = globaltimer_ns();
         a.piv[k] = J;

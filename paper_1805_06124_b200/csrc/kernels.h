@@ -100,7 +100,6 @@ struct ImgsArgs {
     cudaGraphConditionalHandle cond;  // rbg_run's device loop (loop_exit), valid when use_cond
     int use_cond;
     int pdl;  // launch as a programmatic dependent of the preceding sweep (MGS kernel)
-    int late_launch;  // let the next sweep launch only after q is stored (RBG_PDL_LATE A/B)
 };
 
 // Local index of global column J on this rank, -1 if another rank owns it.
