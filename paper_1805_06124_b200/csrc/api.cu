@@ -63,7 +63,7 @@ void free_ctx(rbg_ctx *c) {
         }
         // every CTA's step timestamps (steps 64..71): send skew across CTAs and the latency from
         // the last CTA's send to each CTA's coefficient
-        unsigned long long gt[16 * 8 * 3];
+        unsigned long long gt[16 * 8 * 4];
         if (cudaMemcpy(gt, c->imgs_trace + 512, sizeof gt, cudaMemcpyDeviceToHost) == cudaSuccess && gt[2]) {
             double skew = 0, lat = 0, busy = 0, step = 0;
             int n = 0;
@@ -72,7 +72,7 @@ void free_ctx(rbg_ctx *c) {
                 int have = 0;
                 double b = 0;
                 for (int r = 0; r < 16; r++) {
-                    const unsigned long long *g = gt + (r * 8 + st) * 3;
+                    const unsigned long long *g = gt + (r * 8 + st) * 4;
                     if (!g[1]) continue;
                     have++;
                     smin = std::min(smin, g[1]);
@@ -86,7 +86,7 @@ void free_ctx(rbg_ctx *c) {
                 lat += (double)(cmax - smax);
                 if (st + 1 < 8) {
                     unsigned long long nmax = 0;
-                    for (int r = 0; r < 16; r++) nmax = std::max(nmax, gt[(r * 8 + st + 1) * 3]);
+                    for (int r = 0; r < 16; r++) nmax = std::max(nmax, gt[(r * 8 + st + 1) * 4]);
                     if (nmax) step += (double)(nmax - c0max);
                 }
                 n++;
@@ -96,23 +96,42 @@ void free_ctx(rbg_ctx *c) {
                 fprintf(stderr, "rbg: imgs cluster (ns/step): send skew across CTAs %.0f, last send -> last coefficient %.0f, "
                                 "step start -> send %.0f, step %.0f\n", skew / n, lat / n, busy / n, step / (n - 1));
                 // per CTA: mean send time and coefficient time relative to the step's first send
-                fprintf(stderr, "rbg: imgs per CTA (ns after the first send: send / coefficient):");
+                fprintf(stderr, "rbg: imgs per CTA (ns after the first send: send / stage ready / coefficient):");
                 for (int r = 0; r < 16; r++) {
-                    double ds = 0, dc = 0;
+                    double ds = 0, dc = 0, dg = 0;
                     int m = 0;
                     for (int st = 0; st < 8; st++) {
                         unsigned long long smin = ~0ull;
                         for (int q = 0; q < 16; q++)
-                            if (gt[(q * 8 + st) * 3 + 1]) smin = std::min(smin, gt[(q * 8 + st) * 3 + 1]);
-                        const unsigned long long *g = gt + (r * 8 + st) * 3;
+                            if (gt[(q * 8 + st) * 4 + 1]) smin = std::min(smin, gt[(q * 8 + st) * 4 + 1]);
+                        const unsigned long long *g = gt + (r * 8 + st) * 4;
                         if (!g[1] || smin == ~0ull) continue;
                         ds += (double)(g[1] - smin);
                         dc += (double)(g[2] - smin);
+                        dg += (double)(g[3] - smin);
                         m++;
                     }
-                    if (m) fprintf(stderr, " %d:%.0f/%.0f", r, ds / m, dc / m);
+                    if (m) fprintf(stderr, " %d:%.0f/%.0f/%.0f", r, ds / m, dg / m, dc / m);
                 }
                 fprintf(stderr, "\n");
+                // producer: stage s+1 issued how long before the consumers had it (ns)
+                unsigned long long ti[16 * 8];
+                if (cudaMemcpy(ti, c->imgs_trace + 320, sizeof ti, cudaMemcpyDeviceToHost) == cudaSuccess) {
+                    fprintf(stderr, "rbg: imgs per CTA stage s+1: issued -> ready (ns):");
+                    for (int r = 0; r < 16; r++) {
+                        double d = 0;
+                        int m = 0;
+                        for (int st = 0; st < 8; st++) {
+                            const unsigned long long iss = ti[r * 8 + st], rdy = gt[(r * 8 + st) * 4 + 3];
+                            if (iss && rdy) {
+                                d += (double)(long long)(rdy - iss);
+                                m++;
+                            }
+                        }
+                        if (m) fprintf(stderr, " %d:%.0f", r, d / m);
+                    }
+                    fprintf(stderr, "\n");
+                }
             }
         }
         // %globaltimer (ns): [256] sweep's last CTA done, [257] IMGS entry, [258] cluster synced,
@@ -250,6 +269,8 @@ ImgsArgs imgs_args(const rbg_ctx *c) {
     a.cond = c->cond;
     a.use_cond = c->in_while ? 1 : 0;
     a.pdl = (pdl_enabled(c) && c->comm == RBG_COMM_NONE && c->started) ? 1 : 0;
+    a.tm = c->imgs_tm_ok ? c->imgs_tm : nullptr;
+    a.use_tm = c->imgs_tm_ok ? 1 : 0;
     return a;
 }
 
@@ -751,11 +772,13 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     }
     CUB(dmalloc(&c->w, sizeof(double) * wpad.size()));
     CUB(cudaMemcpyAsync(c->w, wpad.data(), sizeof(double) * wpad.size(), cudaMemcpyHostToDevice, c->stream));
-    const size_t qbytes = (size_t)c->k_max * nvec * 16;
+    // + imgs_basis_pad: the IMGS tensor-map boxes of the last basis vector stay in bounds
+    const size_t qbytes = ((size_t)c->k_max * nvec + (size_t)imgs_basis_pad(nvec)) * 16;
     CUB(dmalloc(&c->Q, qbytes));
     CUB(dmalloc(&c->WQ, qbytes));
     CUB(cudaMemsetAsync(c->Q, 0, qbytes, c->stream));
     CUB(cudaMemsetAsync(c->WQ, 0, qbytes, c->stream));
+    c->imgs_tm_ok = make_imgs_maps(c->WQ, c->Q, nvec, c->ldq_v, c->k_max, c->imgs_tm);
     CUB(dmalloc(&c->R, (size_t)c->k_max * c->M * c->se));
     CUB(cudaMemsetAsync(c->R, 0, (size_t)c->k_max * c->M * c->se, c->stream));
     CUB(dmalloc(&c->r2, sizeof(double) * c->M));

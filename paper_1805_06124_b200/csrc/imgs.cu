@@ -15,6 +15,9 @@
 // after which every CTA holds the bit-identical coefficient and updates its slice of v.  The
 // basis slices are prefetched several steps ahead by TMA bulk copies from a producer warp.
 // The kernel is replicated on every GPU of a sharded run (no broadcast of q needed).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>
@@ -325,6 +328,15 @@ __device__ __forceinline__ void load_slice(double2 (&r)[MAXV], const double2 *p,
 // full-mbarrier (TMA bytes) and one empty-mbarrier (8 consumer warps) per stage, so issuing
 // copies never delays a warp on the reduction's critical path.  D = 0: the slices are loaded
 // straight from global memory one step ahead (large N only).
+// 4D tensor-map TMA: (x, rank, chunk, basis index) -> one CTA's MAXV chunk slices in one copy.
+__device__ __forceinline__ void tma_4d_g2s(void *dst, const CUtensorMap *map, int x, int y, int z, int w, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int MAXV, int D, int THREADS>
 struct BasisPipe {
     unsigned char *smem;
@@ -332,6 +344,12 @@ struct BasisPipe {
     const double2 *WQ, *Q;
     long long ldq_v;
     int k, rank, nvec;
+    // 16 x 128 lanes: one tensor-map copy per array and stage (tmW / tmQ view the basis as
+    // [basis][chunk][rank][128 vectors]; the allocations are padded so that the box of the last
+    // chunk stays in bounds, its vectors past nvec are never read); else MAXV bulk copies each.
+    // Per-SM TMA work is what limits the prefetch: with 10 bulk copies per stage a stage was
+    // issued only ~1.3 us (~1.6 MGS steps) before it was needed (RBG_DEBUG_IMGS).
+    const CUtensorMap *tmW, *tmQ;
 
     static constexpr int kStageBytes = 2 * MAXV * THREADS * 16;
 
@@ -342,6 +360,13 @@ struct BasisPipe {
 
     __device__ void issue(long long s) const {  // one producer thread
         const int b = (int)(s % k);
+        if (tmW) {
+            uint64_t *bar = &full[s % D];
+            mbar_arrive_expect_tx(bar, (uint32_t)kStageBytes);
+            tma_4d_g2s(wq_stage(s), tmW, 0, rank, 0, b, bar);
+            tma_4d_g2s(q_stage(s), tmQ, 0, rank, 0, b, bar);
+            return;
+        }
         uint32_t bytes = 0;
         int len[MAXV];
 #pragma unroll
@@ -367,7 +392,8 @@ struct BasisPipe {
 
     // Producer loop: steps D.. until the consumers publish their final step count in *done
     // (>= 0); then wait for every copy still in flight so none outlives the CTA.
-    __device__ void produce(long long issued, long long limit, volatile long long *done) const {
+    __device__ void produce(long long issued, long long limit, volatile long long *done,
+                            unsigned long long *tissue = nullptr) const {
         while (issued < limit) {
             const uint32_t par = (uint32_t)((issued / D - 1) & 1);
             bool ok = false;
@@ -378,6 +404,8 @@ struct BasisPipe {
                 RBG_WATCHDOG(tp, "IMGS HANG producer rank %u issued %lld par %u\n", cluster_ctarank(), issued, par);
             }
             if (!ok) break;
+            // RBG_DEBUG_IMGS: when stages 65..72 were issued (consumers need them at steps 64..71)
+            if (tissue && issued >= 65 && issued < 73) tissue[issued - 65] = globaltimer_ns();
             issue(issued++);
         }
         long long consumed;
@@ -390,7 +418,8 @@ struct BasisPipe {
 };
 
 template <bool CPLX, int MAXV, int D, int CTAS, bool PRE>
-__global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArgs a) {
+__global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
+    k_imgs(const ImgsArgs a, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmQ) {
     constexpr int THREADS = kLaneImgs / CTAS;  // consumer threads per CTA (one lane each)
     constexpr int DD = D > 0 ? D : 1;
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -424,7 +453,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
     const int nm = (!producer && u0 < nvec) ? (nvec - u0 + kLaneImgs - 1) / kLaneImgs : 0;
     const bool odd_tail = !CPLX && (a.N & 1);
 
-    const BasisPipe<MAXV, DD, THREADS> pipe{dsm, s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec};
+    const BasisPipe<MAXV, DD, THREADS> pipe{dsm,       s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec,
+                                            a.use_tm ? &tmW : nullptr, a.use_tm ? &tmQ : nullptr};
     const long long limit = (long long)kNuMax * k;  // MGS steps that can ever be needed
     // stages issued before the cluster barrier (the rest by the producer loop, off the
     // critical path: each stage is 2 MAXV bulk copies issued by one thread)
@@ -475,7 +505,9 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
         return;
     }
     if (producer) {
-        if (D > 0 && tid == THREADS) pipe.produce(first, limit, &s_done);
+        if (D > 0 && tid == THREADS)
+            pipe.produce(first, limit, &s_done,
+                         a.trace ? reinterpret_cast<unsigned long long *>(a.trace) + 320 + rank * 8 : nullptr);
         return;
     }
 
@@ -523,9 +555,10 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
                 // RBG_DEBUG_IMGS: clock64 at the phase boundaries of steps 64..95 (CTA 0, tid 0)
                 const bool tr = a.trace && rank == 0 && tid == 0 && s >= 64 && s < 96;
                 // every CTA's %globaltimer at step start / partial sent / coefficient known for
-                // steps 64..71 (trace[512 + (rank*8 + step)*3 + p]): the cluster's critical path
+                // steps 64..71 (trace[512 + (rank*8 + step)*4 + p]; p = 3: the next stage is in
+                // shared memory): the cluster's critical path
                 unsigned long long *gt = (a.trace && tid == 0 && s >= 64 && s < 72)
-                                             ? reinterpret_cast<unsigned long long *>(a.trace) + 512 + (rank * 8 + (s - 64)) * 3
+                                             ? reinterpret_cast<unsigned long long *>(a.trace) + 512 + (rank * 8 + (s - 64)) * 4
                                              : nullptr;
                 if (gt) gt[0] = globaltimer_ns();
                 const long long c0 = tr ? clock64() : 0;
@@ -543,6 +576,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
                     mbar_wait(&s_full[(s + 1) % DD], (uint32_t)(((s + 1) / DD) & 1));
                     load_slice<MAXV>(wqr, pipe.wq_stage(s + 1) + tid, THREADS, nm);
                 }
+                if (gt) gt[3] = globaltimer_ns();
                 const long long c3 = tr ? clock64() : 0;
                 c = red.finish();
                 if (gt) gt[2] = globaltimer_ns();
@@ -628,6 +662,35 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1) k_imgs(const ImgsArg
 }
 
 // (MAXV, D): vectors per lane and prefetch depth, D * MAXV * 32 KB / CTAS of shared memory.
+// Tensor maps of WQ and Q for the 16 x 128 staged path (BasisPipe); false if not applicable.
+bool make_imgs_maps(const double2 *WQ, const double2 *Q, long long nvec, long long ldq_v, long long k_max, void *maps) {
+    const int maxv = imgs_maxv(nvec);
+    if (maxv == 0 || maxv > 8 || getenv("RBG_IMGS_BULK")) return false;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap *tm = static_cast<CUtensorMap *>(maps);
+    const void *base[2] = {WQ, Q};
+    for (int i = 0; i < 2; i++) {
+        // (256 doubles = 128 vectors) x 16 ranks x maxv chunks (2,048 vectors apart) x k_max
+        const cuuint64_t dims[4] = {256, 16, (cuuint64_t)maxv, (cuuint64_t)k_max};
+        const cuuint64_t strides[3] = {2048, 32768, (cuuint64_t)ldq_v * 16};
+        const cuuint32_t box[4] = {256, 1, (cuuint32_t)maxv, 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (encode(&tm[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void *>(base[i]), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
 int imgs_maxv(long long nvec) {
     const long long per = (nvec + kLaneImgs - 1) / kLaneImgs;
     if (per <= 6) return (int)(per < 1 ? 1 : per);
@@ -693,7 +756,12 @@ static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.pdl ? 2 : 1;
-    e = cudaLaunchKernelEx(&cfg, kern, a);
+    // the tensor maps cut 128-vector slices: the 16 x 128 staged path only
+    ImgsArgs b = a;
+    b.use_tm = (a.use_tm && a.tm && CTAS == 16 && D > 0) ? 1 : 0;
+    const CUtensorMap *tm = static_cast<const CUtensorMap *>(a.tm);
+    static const CUtensorMap zero{};
+    e = cudaLaunchKernelEx(&cfg, kern, b, tm ? tm[0] : zero, tm ? tm[1] : zero);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
