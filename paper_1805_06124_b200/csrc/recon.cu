@@ -14,6 +14,8 @@
 //    max |g_pq| / sqrt(g_pp g_qq) < 1e-15 (or 40 sweeps);
 //  * k_recon_x: X = Q V(:, 1:k), each element one sequential sum over the basis index.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 
@@ -31,44 +33,60 @@ int gram_tile() { return kGramTile; }
 
 // R: k rows of ldr elements (row-major).  P: nchunks x k x k partial sums (complex).
 // 256 threads own 4 x 4 pairs each, strided by 16 (thread (ta, tb) has pairs
-// (a0 + ta + 16u, b0 + tb + 16v)) so that a warp's shared-memory reads of one operand row
-// are consecutive 16-byte words; every pair is one sequential fma chain over the chunk's
+// (a0 + ta + 16u, b0 + tb + 16v)); every pair is one sequential fma chain over the chunk's
 // columns in increasing index (the order k_gram_reduce and the oracle's orc_gram assume).
 // The pairs a CTA computes: register rows u < NU and columns v < NV hold rows / columns
 // below k (the tile's last 16-row groups past k are skipped), and on a diagonal tile (DIAG)
 // the groups v < u lie wholly below the diagonal (b - a <= 15 - 16 < 0) and are skipped:
-// at k = 300 with 64 x 64 tiles this drops 21 % of the FMAs.  Every computed pair is still one
-// sequential fma chain per chunk, so the bits do not change.
+// at k = 300 with 64 x 64 tiles this drops 21 % of the FMAs.
+//
+// Operand staging (round 2): the 64-row x 16-column slices of R for rows a0.. and b0.. come
+// through a 2D tensor-map TMA with the 128-byte swizzle into kGStages shared-memory stages
+// filled by a producer warp (full / empty mbarriers), so the FP64 pipes never wait for a
+// global load or a CTA barrier (round 1 staged through registers between two __syncthreads:
+// ncu long_scoreboard 26 % + barrier 6 % of the stall samples, FP64 pipe 55 % busy).  A row of
+// a box is 128 bytes (8 complex or 16 real columns), 16-byte chunk c of row r at chunk
+// c ^ (r & 7): a warp's reads of one column over 16 rows hit 8 distinct bank groups.  Rows past
+// k and columns past M are zero-filled by the TMA; a diagonal tile loads its slice once.
+constexpr int kGStages = 3;
+constexpr int kGBox = 64 * 128;  // one box: 64 rows x 128 bytes
+
+__device__ __forceinline__ void tma2d_g2s(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// element (row r of the tile, column cc of the stage) of a swizzled operand slice
+template <bool CPLX>
+__device__ __forceinline__ double2 gram_op(const unsigned char *t, int r, int cc) {
+    if (CPLX)  // two boxes of 8 complex columns
+        return *reinterpret_cast<const double2 *>(t + (cc >> 3) * kGBox + r * 128 + (((cc & 7) ^ (r & 7)) << 4));
+    return make_double2(*reinterpret_cast<const double *>(t + r * 128 + ((((cc >> 1) ^ (r & 7))) << 4) + (cc & 1) * 8),
+                        0.0);
+}
+
 template <bool CPLX, int NU, int NV, bool DIAG>
-__device__ __forceinline__ void gram_tile_body(const double *R, long long ldr, int k, long long j0, long long j1,
-                                               int a0, int b0, double2 (&sa)[kGramSub][kGramTile + 1],
-                                               double2 (&sb)[kGramSub][kGramTile + 1], double (&re)[kGramReg][kGramReg],
+__device__ __forceinline__ void gram_tile_body(unsigned char *stg, uint64_t *full, uint64_t *empty, long long js0,
+                                               long long j1, long long nst, double (&re)[kGramReg][kGramReg],
                                                double (&im)[kGramReg][kGramReg]) {
-    const int tid = threadIdx.x;
+    constexpr int kOpBytes = (CPLX ? 2 : 1) * kGBox;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int ta = tid >> 4, tb = tid & 15;
-    for (long long js = j0; js < j1; js += kGramSub) {
-        // stage rows a0..a0+63 and b0..b0+63, columns js..js+15 (transposed: [col][row])
-        for (int e = tid; e < kGramSub * kGramTile; e += 256) {
-            const int r = e / kGramSub, cc = e % kGramSub;
-            const long long j = js + cc;
-            double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
-            if (j < j1) {
-                if (a0 + r < k) va = CPLX ? reinterpret_cast<const double2 *>(R)[(long long)(a0 + r) * ldr + j]
-                                          : make_double2(R[(long long)(a0 + r) * ldr + j], 0.0);
-                if (b0 + r < k) vb = CPLX ? reinterpret_cast<const double2 *>(R)[(long long)(b0 + r) * ldr + j]
-                                          : make_double2(R[(long long)(b0 + r) * ldr + j], 0.0);
-            }
-            sa[cc][r] = va;
-            sb[cc][r] = vb;
-        }
-        __syncthreads();
+    for (long long st = 0; st < nst; st++) {
+        mbar_wait(&full[st % kGStages], (uint32_t)((st / kGStages) & 1));
+        const unsigned char *A = stg + (size_t)(st % kGStages) * 2 * kOpBytes;
+        const unsigned char *B = DIAG ? A : A + kOpBytes;
+        const long long js = js0 + st * kGramSub;
         const int n = (int)((j1 - js) < kGramSub ? (j1 - js) : kGramSub);
         for (int cc = 0; cc < n; cc++) {
             double2 x[kGramReg], y[kGramReg];
 #pragma unroll
-            for (int u = 0; u < NU; u++) x[u] = sa[cc][ta + 16 * u];
+            for (int u = 0; u < NU; u++) x[u] = gram_op<CPLX>(A, ta + 16 * u, cc);
 #pragma unroll
-            for (int v = 0; v < NV; v++) y[v] = sb[cc][tb + 16 * v];
+            for (int v = 0; v < NV; v++) y[v] = gram_op<CPLX>(B, tb + 16 * v, cc);
 #pragma unroll
             for (int u = 0; u < NU; u++)
 #pragma unroll
@@ -81,44 +99,69 @@ __device__ __forceinline__ void gram_tile_body(const double *R, long long ldr, i
                     im[u][v] = fma(-y[v].y, x[u].x, im[u][v]);
                 }
         }
-        __syncthreads();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st % kGStages]);
     }
-}
-
-template <bool CPLX, int NU, int NV>
-__device__ __forceinline__ void gram_tile_diag(bool diag, const double *R, long long ldr, int k, long long j0,
-                                               long long j1, int a0, int b0, double2 (&sa)[kGramSub][kGramTile + 1],
-                                               double2 (&sb)[kGramSub][kGramTile + 1],
-                                               double (&re)[kGramReg][kGramReg], double (&im)[kGramReg][kGramReg]) {
-    if (diag) gram_tile_body<CPLX, NU, NV, true>(R, ldr, k, j0, j1, a0, b0, sa, sb, re, im);
-    else gram_tile_body<CPLX, NU, NV, false>(R, ldr, k, j0, j1, a0, b0, sa, sb, re, im);
 }
 
 template <bool CPLX, int NU>
-__device__ __forceinline__ void gram_tile_nv(int nv, bool diag, const double *R, long long ldr, int k, long long j0,
-                                             long long j1, int a0, int b0, double2 (&sa)[kGramSub][kGramTile + 1],
-                                             double2 (&sb)[kGramSub][kGramTile + 1],
+__device__ __forceinline__ void gram_tile_nv(int nv, bool diag, unsigned char *stg, uint64_t *full, uint64_t *empty,
+                                             long long js0, long long j1, long long nst,
                                              double (&re)[kGramReg][kGramReg], double (&im)[kGramReg][kGramReg]) {
+#define RBG_GRAM_CASE(NV)                                                                                         \
+    if (diag) gram_tile_body<CPLX, NU, NV, true>(stg, full, empty, js0, j1, nst, re, im);                         \
+    else gram_tile_body<CPLX, NU, NV, false>(stg, full, empty, js0, j1, nst, re, im);
     switch (nv) {
-        case 1: gram_tile_diag<CPLX, NU, 1>(diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
-        case 2: gram_tile_diag<CPLX, NU, 2>(diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
-        case 3: gram_tile_diag<CPLX, NU, 3>(diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
-        default: gram_tile_diag<CPLX, NU, 4>(diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
+        case 1: RBG_GRAM_CASE(1) break;
+        case 2: RBG_GRAM_CASE(2) break;
+        case 3: RBG_GRAM_CASE(3) break;
+        default: RBG_GRAM_CASE(4) break;
     }
+#undef RBG_GRAM_CASE
 }
 
 template <bool CPLX>
-__global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, int k, long long M, long long chunk,
-                                              const int2 *tiles, double2 *P) {
-    // +1 column of padding: the transposed staging stores (consecutive threads -> consecutive
-    // columns cc) would otherwise all hit the same banks
-    __shared__ double2 sa[kGramSub][kGramTile + 1];
-    __shared__ double2 sb[kGramSub][kGramTile + 1];
+__global__ void __launch_bounds__(256 + 32, 2) k_gram(const __grid_constant__ CUtensorMap tmR, int k, long long M,
+                                                      long long chunk, const int2 *tiles, double2 *P) {
+    extern __shared__ __align__(1024) unsigned char gsm_raw[];
+    unsigned char *stg = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);  // swizzle needs 1024-B tiles
+    __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages];
+    constexpr int kOpBytes = (CPLX ? 2 : 1) * kGBox;
     const int2 t = tiles[blockIdx.x];
     const int a0 = t.x * kGramTile, b0 = t.y * kGramTile;
+    const bool diag = t.x == t.y;
     const long long c = blockIdx.y;
     const long long j0 = c * chunk, j1 = (j0 + chunk < M) ? j0 + chunk : M;
+    const long long nst = (j1 - j0 + kGramSub - 1) / kGramSub;
     const int tid = threadIdx.x;
+    if (tid == 256) {
+        for (int i = 0; i < kGStages; i++) {
+            mbar_init_nofence(&full[i], 1);
+            mbar_init_nofence(&empty[i], 8);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    if (tid >= 256) {  // producer warp: one thread issues the stages
+        if (tid == 256) {
+            const uint32_t bytes = (uint32_t)(diag ? 1 : 2) * kOpBytes;
+            const int xs = CPLX ? 2 : 1;  // doubles per element
+            for (long long st = 0; st < nst; st++) {
+                if (st >= kGStages) mbar_wait(&empty[st % kGStages], (uint32_t)((st / kGStages - 1) & 1));
+                uint64_t *bar = &full[st % kGStages];
+                mbar_arrive_expect_tx(bar, bytes);
+                unsigned char *A = stg + (size_t)(st % kGStages) * 2 * kOpBytes;
+                const int x = (int)((j0 + st * kGramSub) * xs);
+                tma2d_g2s(A, &tmR, x, a0, bar);
+                if (CPLX) tma2d_g2s(A + kGBox, &tmR, x + 16, a0, bar);
+                if (!diag) {
+                    tma2d_g2s(A + kOpBytes, &tmR, x, b0, bar);
+                    if (CPLX) tma2d_g2s(A + kOpBytes + kGBox, &tmR, x + 16, b0, bar);
+                }
+            }
+        }
+        return;
+    }
     const int ta = tid >> 4, tb = tid & 15;
     double re[kGramReg][kGramReg], im[kGramReg][kGramReg];
 #pragma unroll
@@ -128,12 +171,11 @@ __global__ void __launch_bounds__(256) k_gram(const double *R, long long ldr, in
     // 16-row groups of the tile that hold rows / columns below k (uniform over the CTA)
     const int nu = (k - a0 + 15) / 16 < 4 ? (k - a0 + 15) / 16 : 4;
     const int nv = (k - b0 + 15) / 16 < 4 ? (k - b0 + 15) / 16 : 4;
-    const bool diag = t.x == t.y;
     switch (nu) {
-        case 1: gram_tile_nv<CPLX, 1>(nv, diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
-        case 2: gram_tile_nv<CPLX, 2>(nv, diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
-        case 3: gram_tile_nv<CPLX, 3>(nv, diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
-        default: gram_tile_nv<CPLX, 4>(nv, diag, R, ldr, k, j0, j1, a0, b0, sa, sb, re, im); break;
+        case 1: gram_tile_nv<CPLX, 1>(nv, diag, stg, full, empty, j0, j1, nst, re, im); break;
+        case 2: gram_tile_nv<CPLX, 2>(nv, diag, stg, full, empty, j0, j1, nst, re, im); break;
+        case 3: gram_tile_nv<CPLX, 3>(nv, diag, stg, full, empty, j0, j1, nst, re, im); break;
+        default: gram_tile_nv<CPLX, 4>(nv, diag, stg, full, empty, j0, j1, nst, re, im); break;
     }
 #pragma unroll
     for (int u = 0; u < kGramReg; u++)
@@ -639,10 +681,54 @@ cudaError_t launch_eig_sort(const double2 *G, int k, int kp, double tau2, int kr
 // ------------------------------------------------------------------ host launchers
 cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool cplx, double2 *P, long long chunk,
                         long long nchunks, int2 *tiles_d, int ntiles, cudaStream_t s) {
-    dim3 grid(ntiles, (unsigned)nchunks);
-    if (cplx) k_gram<true><<<grid, 256, 0, s>>>(R, ldr, k, M, chunk, tiles_d, P);
-    else k_gram<false><<<grid, 256, 0, s>>>(R, ldr, k, M, chunk, tiles_d, P);
-    return cudaGetLastError();
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    // R as a 2D array of doubles: M (x 2 complex) columns x k rows, row pitch ldr elements;
+    // boxes of 16 doubles (128 bytes) x 64 rows, 128-byte swizzle, out-of-range rows / columns 0.
+    // A tensor map needs a 16-byte row pitch: a real R with odd ldr is first copied to even.
+    const int xs = cplx ? 2 : 1;
+    double *Rp = nullptr;
+    if ((ldr * xs * 8) % 16 != 0) {
+        const long long ldp = ldr + 1;
+        cudaError_t e = dmalloc(&Rp, (size_t)k * ldp * 8);
+        if (e == cudaSuccess) e = cudaMemcpy2DAsync(Rp, (size_t)ldp * 8, R, (size_t)ldr * 8, (size_t)M * 8, k,
+                                                    cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) {
+            dfree(Rp);
+            return e;
+        }
+        R = Rp;
+        ldr = ldp;
+    }
+    CUtensorMap tm;
+    const cuuint64_t dims[2] = {(cuuint64_t)(M * xs), (cuuint64_t)k};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldr * xs * 8};
+    const cuuint32_t box[2] = {16, 64};
+    const cuuint32_t estr[2] = {1, 1};
+    cudaError_t e = cudaSuccess;
+    if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(R), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        e = cudaErrorInvalidValue;
+    auto kern = cplx ? k_gram<true> : k_gram<false>;
+    const size_t smem = (size_t)kGStages * 2 * xs * kGBox + 1024;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+        dim3 grid(ntiles, (unsigned)nchunks);
+        kern<<<grid, 256 + 32, smem, s>>>(tm, k, M, chunk, tiles_d, P);
+        e = cudaGetLastError();
+    }
+    if (Rp) {  // the caller synchronises before freeing its own buffers; so do we here
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        dfree(Rp);
+    }
+    return e;
 }
 
 cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, const double2 *G0, double2 *G,

@@ -13,13 +13,18 @@ from paper_1805_06124_b200 import inputs, rbg  # noqa: E402
 it = int(sys.argv[1])
 timing = len(sys.argv) > 2 and sys.argv[2] == "1"
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 40960
-N = 10000
+cfg = int(sys.argv[4]) if len(sys.argv) > 4 else 2       # 2: config-2 recipe (N = 10,000); 1, 4: those configs
 os.environ["RBG_DEBUG_IMGS"] = str(it)
-t = inputs.chirp_grid(N)
-w = inputs.simpson_weights(N)
-q, chi, psi = inputs.chirp_params(M, 2, spin=True)
-S = torch.empty((M, N), dtype=torch.complex128, device="cuda")
-rbg.gen_chirp(S, t, w, q, chi, psi, spin=True)
+if cfg == 2:
+    N = 10000
+    t = inputs.chirp_grid(N)
+    w = inputs.simpson_weights(N)
+    q, chi, psi = inputs.chirp_params(M, 2, spin=True)
+    S = torch.empty((M, N), dtype=torch.complex128, device="cuda")
+    rbg.gen_chirp(S, t, w, q, chi, psi, spin=True)
+else:
+    Sh, w, _, _ = inputs.make(cfg)
+    S = torch.as_tensor(Sh, device="cuda")
 ctx = rbg.Context(S, w, 0.0, max(it + 2, 10))
 ctx.set_timing(timing)
 ctx.step(it + 2)
