@@ -7,6 +7,8 @@ are compared exactly and Q, R, errors, r2 bit for bit.  BASELINE.json's toleranc
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -163,12 +165,14 @@ def test_device_loop_stops_without_tail(rbg, orc, ortho):
     lanes = orc.CANONICAL_CGS if ortho == "cgs" else orc.CANONICAL
     o = orc.greedy(S, w, tol, k_max, lanes=lanes, ortho=ortho)
     assert o.stop == "RANK" and o.k < k_max - 40       # a tail of > 40 iterations would exist
+    loop = not os.environ.get("RBG_NO_DEVICE_LOOP")   # the A/B switch selects the polled path
     with rbg.Context(S, w, tol, k_max, ortho=ortho) as ctx:
         ctx.run()
         compare(ctx.result(), o)
-        assert ctx.stats().noop_iters == 0
+        n0 = ctx.stats().noop_iters
+        assert n0 == 0 or not loop
         ctx.run()                                      # already stopped: nothing launched
-        assert ctx.stats().noop_iters == 0
+        assert ctx.stats().noop_iters == n0
     with rbg.Context(S, w, tol, k_max, ortho=ortho) as ctx:
         ctx.set_timing(True)
         ctx.run()
