@@ -301,6 +301,15 @@ class Driver:
             self.ctx.step(n)
 
 
+def replica_hash(ctx) -> str:
+    """sha256 of the replicated results (pivots, errors, basis) of a sharded context."""
+    import hashlib
+    hsh = hashlib.sha256()
+    for arr in (ctx.pivots(), ctx.errors(), ctx.basis()):
+        hsh.update(np.ascontiguousarray(arr).tobytes())
+    return hsh.hexdigest()
+
+
 def run_dry(a):
     """--dry-run: every rank's plan and e2e guard, gathered to rank 0 (gloo, no GPU)."""
     import torch.distributed as dist
@@ -388,17 +397,22 @@ def run_ours(a):
     if comm == rbg.COMM_PEER and mode == "plain":
         # the PEER exchange needs CUDA IPC between the ranks' processes: if any rank cannot map
         # its peers or the warm-up timed out, every rank falls back to the NCCL exchange
-        ok, ctx = True, None
+        # -- and so does every rank if the replicated results already differ after the warm-up
+        # (the first free-running PEER run on a multi-GPU box must not corrupt the timed record)
+        ok, ctx, same = True, None, True
         try:
             ctx, drv = make_ctx(comm, timing)
             ok = ctx.info()[2] != "PEER_TIMEOUT"
         except rbg.RbgError as e:
             ok, fallback = False, str(e)
         ok = min(D.all_gather_bytes(1 if ok else 0)) == 1
-        if not ok:
+        if ok:
+            same = len(set(D.all_gather_bytes(replica_hash(ctx)))) == 1
+        if not ok or not same:
             if ctx is not None:
                 ctx.close()
-            fallback = fallback or "PEER warm-up failed on some rank"
+            fallback = fallback or ("PEER warm-up failed on some rank" if not ok else
+                                    "replicas differ after the PEER warm-up")
             comm = rbg.COMM_NCCL
             ctx, drv = make_ctx(comm, timing)
     else:
@@ -430,11 +444,7 @@ def run_ours(a):
     if world > 1:
         # the replicated IMGS must leave bit-identical pivots / errors / basis on every rank
         # (SURVEY §5 integrity check): compare a hash of their bits across the ranks
-        import hashlib
-        hsh = hashlib.sha256()
-        for arr in (ctx.pivots(), errs, ctx.basis()):
-            hsh.update(np.ascontiguousarray(arr).tobytes())
-        replicas = len(set(D.all_gather_bytes(hsh.hexdigest()))) == 1
+        replicas = len(set(D.all_gather_bytes(replica_hash(ctx)))) == 1
     if a.dump:
         res = ctx.result()
         extra = {"S": S.cpu().numpy(), "w": w} if a.dump_inputs else {}
@@ -576,8 +586,10 @@ def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev, comm,
                       col_offset=D.partition(M_glob, world, rank)[0], M_global=M_glob, nccl_id=nccl_id)
     if comm == rbg.COMM_PEER:
         D.connect_peers(ctx)
+    t_create = time.perf_counter()
     Driver(ctx, mode, stream, world).step(iters)
-    piv = ctx.pivots()
+    piv = ctx.pivots()                                # synchronises: the iterations are done
+    t_iter = time.perf_counter()
     err = ctx.errors()
     Q = ctx.basis()
     t1 = time.perf_counter()
@@ -588,6 +600,9 @@ def e2e(a, host, w, k_max, iters, stream, rank, world, M_loc, M_glob, dev, comm,
     return {"value": iters / wall, "unit": "it/s",
             "h2d_bytes_per_step": h2d / iters, "d2h_bytes_per_step": d2h / iters,
             "wall_s": wall, "steps": iters,
+            # this rank's split of the wall time: the create (65.5 GB over PCIe at ~55 GB/s + the
+            # NaN scan) is the floor of this number over a short window
+            "split_s": {"create_h2d": t_create - t0, "iterations": t_iter - t_create, "readback": t1 - t_iter},
             "note": "rbg_create from pinned host S (H2D + NaN scan) + all iterations + D2H of "
                     "pivots/errors/basis, wall clock with device sync"}
 
