@@ -230,6 +230,19 @@ rbg_status rbg_add_columns(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf
 rbg_status rbg_add_columns_ex(rbg_ctx *ctx, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem, int64_t first_gid,
                               int64_t M_global_new);
 
+/* Checkpoint / resume.  A checkpoint is the state the getters return once the
+ * greedy stopped: k, pivots[k], errors[k+1] (err_k may be dropped), nu[k], rdiag[k], Q (N x k,
+ * column stride ldq >= N), R (k x M row-major, row stride ldr >= M) and r2[M].  rbg_restore
+ * loads it into a FRESH single-GPU context created on the same S and w (k < k_max, e.g. a run
+ * continued to a larger k_max): w o Q is recomputed with the IMGS kernel's multiplication, the
+ * pivot search runs over r2, and the next rbg_run / rbg_step begins at the decision for k --
+ * the continued greedy equals an uninterrupted one bit for bit.  Arrays in host memory
+ * (mem = HOST) or device memory (DEVICE).  EINVAL on bad sizes or pivots; ESTATE on a started,
+ * sharded or explicit-residual context.  k = 0 restores nothing.  Blocking.                */
+rbg_status rbg_restore(rbg_ctx *ctx, int64_t k, const int64_t *pivots, const double *errors, const int32_t *nu,
+                       const double *rdiag, const void *Q, int64_t ldq, const void *R, int64_t ldr, const double *r2,
+                       rbg_mem mem);
+
 /* Gram matrix G = R R^H of the k x M coefficient block (k = basis size): k x k Hermitian,
  * column-major with leading dimension ldg >= k, complex (16-byte) entries even for a real
  * dtype.  Summation order: columns in chunks of 4096, each chunk one sequential fma chain,

@@ -172,6 +172,50 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     return RBG_OK;
 }
 
+rbg_status rbg_restore(rbg_ctx *c, int64_t k, const int64_t *pivots, const double *errors, const int32_t *nu,
+                       const double *rdiag, const void *Q, int64_t ldq, const void *R, int64_t ldr, const double *r2,
+                       rbg_mem mem) {
+    TRY(check_ctx(c));
+    if (c->xmode) return fail(RBG_ESTATE, "not available with explicit residuals");
+    if (c->comm != RBG_COMM_NONE) return fail(RBG_ESTATE, "restore needs a single-GPU context");
+    if (c->started || c->iters) return fail(RBG_ESTATE, "restore into a fresh context only");
+    if (k < 0 || k >= c->k_max || k > c->M)
+        return fail(RBG_EINVAL, "k=%lld outside [0, k_max=%lld) or above M", (long long)k, c->k_max);
+    if (k == 0) return RBG_OK;  // nothing to restore: the greedy starts with sweep 0
+    if (!pivots || !errors || !nu || !rdiag || !Q || !R || !r2) return fail(RBG_EINVAL, "null state array");
+    if (ldq < c->N || ldr < c->M) return fail(RBG_EINVAL, "ldq < N or ldr < M");
+    std::vector<long long> hp((size_t)k);
+    const cudaMemcpyKind kind = mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CU(cudaMemcpy(hp.data(), pivots, sizeof(long long) * k,
+                  mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    for (long long i = 0; i < k; i++)
+        if (hp[(size_t)i] < 0 || hp[(size_t)i] >= c->M) return fail(RBG_EINVAL, "pivot %lld out of range", hp[(size_t)i]);
+    const size_t col = (size_t)c->N * c->se, pitch = (size_t)c->nvec * 16;
+    cudaError_t e = cudaSuccess;
+    if (pitch != col) e = cudaMemsetAsync(c->Q, 0, pitch * k, c->stream);  // real, odd N: padding row
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(c->Q, pitch, Q, (size_t)ldq * c->se, col, k, kind, c->stream);
+    if (e == cudaSuccess) e = launch_weight_basis(c->WQ, c->Q, k, c->ldq_v, c->nvec, c->w, c->cplx, c->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(c->R, (size_t)c->M * c->se, R, (size_t)ldr * c->se, (size_t)c->M * c->se, k, kind, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->r2, r2, sizeof(double) * c->M, kind, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->piv, pivots, sizeof(long long) * k, kind, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->errors, errors, sizeof(double) * k, kind, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->nu, nu, sizeof(int) * k, kind, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->rdiag, rdiag, sizeof(double) * k, kind, c->stream);
+    DevState h{};
+    h.k = k;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream);
+    // the pivot search over the restored residuals; the next iteration begins at the decision
+    if (e == cudaSuccess) e = launch_maxloc(c->r2, c->M, 0, c->st, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(RBG_ECUDA, "restore: %s", cudaGetErrorString(e));
+    c->started = true;
+    c->resume_pending = true;
+    c->stopped = false;
+    c->iters = k;
+    return RBG_OK;
+}
+
 rbg_status rbg_add_columns(rbg_ctx *c, const void *F, int64_t M_f, int64_t ldf, rbg_mem F_mem) {
     TRY(check_ctx(c));
     if (c->world != 1 || c->comm != RBG_COMM_NONE)

@@ -193,6 +193,9 @@ cudaError_t launch_scale_sqrtw(double2 *V, long long ldv, const double2 *S, long
                                long long N, const double *w, bool cplx, cudaStream_t s);
 cudaError_t launch_unscale_sqrtw(double2 *Q, const double2 *Qt, long long k, long long nvec, const double *w, bool cplx,
                                  cudaStream_t s);
+// WQ = w o Q for basis vectors 0..k-1 (rbg_restore), the IMGS kernel's multiplication.
+cudaError_t launch_weight_basis(double2 *WQ, const double2 *Q, long long k, long long ldq_v, long long nvec,
+                                const double *w, bool cplx, cudaStream_t s);
 // Deterministic maxloc of r2[0..M) (value desc, index asc) into st->m_loc / st->j_loc.
 cudaError_t launch_maxloc(const double *r2, long long M, long long col_offset, DevState *st,
                           cudaStream_t s);

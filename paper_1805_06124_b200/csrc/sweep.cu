@@ -691,6 +691,24 @@ cudaError_t launch_unscale_sqrtw(double2 *Q, const double2 *Qt, long long k, lon
     return cudaGetLastError();
 }
 
+// WQ = w o Q for k basis vectors (rbg_restore): per component the one multiplication the IMGS
+// kernel performs when it stores q_{k+1} and w o q_{k+1}, so the bits are the ones IMGS writes.
+__global__ void k_weight_basis(double2 *WQ, const double2 *Q, long long k, long long ldq_v, long long nvec,
+                               const double *w, bool cplx) {
+    const long long total = k * nvec;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const long long i = t / nvec, u = t - i * nvec;
+        const double2 q = Q[i * ldq_v + u];
+        WQ[i * ldq_v + u] = cplx ? make_double2(w[u] * q.x, w[u] * q.y) : make_double2(w[2 * u] * q.x, w[2 * u + 1] * q.y);
+    }
+}
+
+cudaError_t launch_weight_basis(double2 *WQ, const double2 *Q, long long k, long long ldq_v, long long nvec,
+                                const double *w, bool cplx, cudaStream_t s) {
+    k_weight_basis<<<148 * 4, 256, 0, s>>>(WQ, Q, k, ldq_v, nvec, w, cplx);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ maxloc / sqrt helpers
 // Used when columns are added to a context (enrichment): the pivot search over the whole
 // residual vector without a sweep.  One CTA, total order, exact.

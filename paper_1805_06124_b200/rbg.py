@@ -97,6 +97,7 @@ SYMBOLS = {
     "rbg_add_columns": ([_P, _P, _I64, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_add_columns_ex": ([_P, _P, _I64, _I64, ctypes.c_int, _I64, _I64], ctypes.c_int),
     "rbg_gram": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "rbg_restore": ([_P, _I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, ctypes.c_int], ctypes.c_int),
     "rbg_reconstruct": ([_P, ctypes.c_double, _I64, ctypes.POINTER(_I64), _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_eim": ([_P, _P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "rbg_gram_fold": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
@@ -401,6 +402,24 @@ class Context:
         self.M_global = int(M_global) if M_global is not None else self.M_global + mf
         del keep
 
+    def restore(self, state: "Result"):
+        """rbg_restore: continue a checkpointed greedy (a Result from result(full=True) of a
+        stopped context over the same S and w) in this fresh context; the next run() begins at
+        the decision for state.k."""
+        k = int(state.k)
+        dt = np.complex128 if self.cplx else np.float64
+        piv = np.ascontiguousarray(state.pivots[:k], dtype=np.int64)
+        err = np.ascontiguousarray(np.asarray(state.errors)[:k], dtype=np.float64)
+        nu = np.ascontiguousarray(state.nu[:k], dtype=np.int32)
+        rd = np.ascontiguousarray(state.rdiag[:k], dtype=np.float64)
+        Q = np.ascontiguousarray(state.Q[:k], dtype=dt)
+        R = np.ascontiguousarray(state.R[:k], dtype=dt)
+        r2 = np.ascontiguousarray(state.r2, dtype=np.float64)
+        if Q.shape != (k, self.N) or R.shape != (k, self.M) or r2.shape != (self.M,):
+            raise ValueError("checkpoint shapes do not match this context")
+        _check(lib().rbg_restore(self.h, k, piv.ctypes.data, err.ctypes.data, nu.ctypes.data, rd.ctypes.data,
+                                 Q.ctypes.data, self.N, R.ctypes.data, self.M, r2.ctypes.data, MEM_HOST))
+
     def gram(self) -> np.ndarray:
         """G = R R^H of the current coefficient block (k x k complex), rbg_gram."""
         k = self.info()[0]
@@ -651,6 +670,22 @@ def add_columns_ex(ctx: Context, F, first_gid: int, M_global: int):
 
 def gram(ctx: Context) -> np.ndarray:
     return ctx.gram()
+
+
+def restore(ctx: Context, state: Result):
+    ctx.restore(state)
+
+
+def save_checkpoint(ctx: Context, path: str):
+    """The stopped greedy's state (the getters' outputs) as an .npz file."""
+    r = ctx.result(full=True)
+    np.savez(path, k=r.k, stop=r.stop, pivots=r.pivots, errors=r.errors, nu=r.nu, rdiag=r.rdiag, Q=r.Q, R=r.R, r2=r.r2)
+
+
+def load_checkpoint(path: str) -> Result:
+    z = np.load(path)
+    return Result(k=int(z["k"]), stop=str(z["stop"]), pivots=z["pivots"], errors=z["errors"], nu=z["nu"],
+                  rdiag=z["rdiag"], Q=z["Q"], R=z["R"], r2=z["r2"])
 
 
 def gram_fold(ctx: Context, G=None) -> np.ndarray:

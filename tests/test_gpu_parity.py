@@ -446,3 +446,36 @@ def test_peer_tiny_shards_until_all_selected(rbg, orc, world, M, N, cplx):
         np.testing.assert_array_equal(r.errors, o.errors)
         np.testing.assert_array_equal(r.Q, o.Q)
         c.close()
+
+
+@pytest.mark.parametrize("case", ["cplx", "real"])
+def test_checkpoint_restore_continues_bit_for_bit(rbg, orc, tmp_path, case):
+    """Checkpoint / resume (rbg_restore): a greedy stopped at k_max = 30 is saved, loaded into a
+    fresh context with a larger k_max and continued; the result equals an uninterrupted run and
+    the oracle bit for bit (pivots, errors, Q, R, r2, nu, rdiag, stop)."""
+    if case == "cplx":
+        S, w, tol, k_max = inputs.config1(M=3000, N=2000)
+        k_max = 80
+    else:
+        S, w, tol, k_max = inputs.config0()
+    full = rbg.greedy(S, w, tol, k_max)
+    with rbg.Context(S, w, tol, 30) as ctx:
+        ctx.run()
+        assert ctx.info()[::2] == (30, "KMAX")
+        rbg.save_checkpoint(ctx, str(tmp_path / "ck.npz"))
+    state = rbg.load_checkpoint(str(tmp_path / "ck.npz"))
+    with rbg.Context(S, w, tol, k_max) as ctx:
+        import dataclasses
+        with pytest.raises((rbg.RbgError, ValueError)):        # k >= k_max is refused
+            ctx.restore(dataclasses.replace(state, k=k_max))
+        ctx.restore(state)
+        ctx.run()
+        g = ctx.result()
+        with pytest.raises(rbg.RbgError) as e:
+            ctx.restore(state)                                # not a fresh context any more
+        assert e.value.status == rbg.ESTATE
+    o = orc.greedy(S, w, tol, k_max, lanes=orc.CANONICAL)
+    for ref in (full, o):
+        assert (g.k, g.stop) == (ref.k, ref.stop)
+        for key in ("pivots", "errors", "Q", "R", "r2", "nu", "rdiag"):
+            np.testing.assert_array_equal(getattr(g, key), getattr(ref, key))
