@@ -222,9 +222,10 @@ def config_dict(a, world):
 
 def run_reference(a):
     """The CPU oracle (oracle/, as it stands) on the box's host cores, on this arm's workload:
-    at N = 1 all 409,600 columns (generated on the host with every core), iterations 0..W+K-1
-    actually run and iterations W..W+K-1 timed.  At N > 1 the whole job (N x 65.5 GB) does not
-    fit host RAM: one GPU's 409,600 columns are timed and the column sweep scaled by N."""
+    all M_global columns (generated on the host with every core) when they fit host RAM (always
+    at N = 1), iterations 0..W+K-1 actually run and iterations W..W+K-1 timed.  Otherwise (e.g.
+    N x 65.5 GB at N = 4, 8) one GPU's 409,600 columns are timed and the column sweep scaled by
+    M_global / 409,600."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -233,7 +234,9 @@ def run_reference(a):
     world = a.gpus
     W, K = a.warmup, a.steps
     M_glob = a.cols_per_gpu * world
-    cols = min(M_glob, a.cols_per_gpu)
+    # all columns when the job fits host RAM (S plus the oracle's R and headroom), else one GPU's
+    need = M_glob * a.rows * 16 + (W + K) * M_glob * 16
+    cols = M_glob if need * 1.1 < host_mem_available() or world == 1 else a.cols_per_gpu
     cfg = 2 if world == 1 else 3
     t0 = time.perf_counter()
     t = inputs.chirp_grid(a.rows)
