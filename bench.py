@@ -244,7 +244,8 @@ def run_reference(a):
     q, chi, psi = inputs.chirp_params(M_glob, cfg, spin=True)
     S = inputs.chirp_columns_host(t, w, q[:cols], chi[:cols], psi[:cols], spin=True)
     t_gen = time.perf_counter() - t0
-    r = O.greedy(S, w, 0.0, W + K, lanes=O.CANONICAL, max_iters=W + K)
+    # all host cores explicitly: torchrun starts its workers with OMP_NUM_THREADS=1
+    r = O.greedy(S, w, 0.0, W + K, lanes=O.CANONICAL, max_iters=W + K, threads=oracle_cores())
     if r.k != W + K:
         raise SystemExit(f"oracle stopped early ({r.stop} at k={r.k})")
     t_it = np.asarray(r.t_iter[W:W + K])
@@ -545,7 +546,7 @@ def run_ours(a):
         lo = min(W, n_it - 1)
         Sh = host.numpy()
         t0 = time.perf_counter()
-        r = O.greedy(Sh, w, 0.0, n_it, lanes=O.CANONICAL, max_iters=n_it)
+        r = O.greedy(Sh, w, 0.0, n_it, lanes=O.CANONICAL, max_iters=n_it, threads=oracle_cores())
         wall = time.perf_counter() - t0
         t_it = np.asarray(r.t_iter[lo:n_it])
         t_im = np.asarray(r.t_imgs[lo:n_it])

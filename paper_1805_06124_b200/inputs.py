@@ -89,7 +89,7 @@ def build_host(force: bool = False) -> str:
     return HOST_LIB
 
 
-def chirp_columns_host(t: np.ndarray, w: np.ndarray, q, chi, psi, spin: bool, out=None) -> np.ndarray:
+def chirp_columns_host(t: np.ndarray, w: np.ndarray, q, chi, psi, spin: bool, out=None, threads: int = 0) -> np.ndarray:
     """chirp_columns with every host core (inputs_host.c, OpenMP over columns): the full
     409,600-column matrix in seconds instead of minutes.  Equal to chirp_columns to rounding
     (another libm); used where only the workload's shape and values matter (the reference
@@ -100,7 +100,7 @@ def chirp_columns_host(t: np.ndarray, w: np.ndarray, q, chi, psi, spin: bool, ou
         _host_lib = ctypes.CDLL(build_host())
         dp = ctypes.POINTER(ctypes.c_double)
         _host_lib.rbg_inputs_chirp.argtypes = [dp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp, dp, dp,
-                                               ctypes.c_int]
+                                               ctypes.c_int, ctypes.c_int]
         _host_lib.rbg_inputs_chirp.restype = None
     x = (-np.asarray(t, dtype=np.float64) + CHIRP_EPS)
     A = np.ascontiguousarray(x ** -0.25)
@@ -114,8 +114,11 @@ def chirp_columns_host(t: np.ndarray, w: np.ndarray, q, chi, psi, spin: bool, ou
 
     def p(a):
         return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    if threads <= 0:
+        import os
+        threads = len(os.sched_getaffinity(0))        # every core (torchrun workers default to 1)
     _host_lib.rbg_inputs_chirp(p(out.view(np.float64)), N, M, p(A), p(base), p(wv), p(qv), p(cv), p(pv),
-                               1 if spin else 0)
+                               1 if spin else 0, threads)
     return out
 
 

@@ -11,11 +11,14 @@
  * im), column j at S + 2 j N.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 
+/* nthreads > 0: that many OpenMP threads (torchrun sets OMP_NUM_THREADS=1 for its workers) */
 void rbg_inputs_chirp(double *S, int64_t N, int64_t M, const double *A, const double *base, const double *w,
-                      const double *q, const double *chi, const double *psi, int spin)
+                      const double *q, const double *chi, const double *psi, int spin, int nthreads)
 {
+    if (nthreads > 0) omp_set_num_threads(nthreads);
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t j = 0; j < M; j++) {
         double *col = S + 2 * j * N;
