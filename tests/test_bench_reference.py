@@ -74,3 +74,19 @@ def test_dry_run_eight_ranks_bookkeeping():
         off += p["cols"]
     assert off == 3_276_800
     assert d["e2e_runs"] == all(p["e2e_guard"]["run"] for p in plans)
+
+
+def test_reference_arm_two_ranks_all_columns():
+    """Under torchrun with 2 ranks the reference arm runs on rank 0 alone, on all columns of the
+    job when they fit host RAM (not extrapolated), with every host core (torchrun workers start
+    with OMP_NUM_THREADS=1: the arm sets its thread count explicitly)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29573", os.path.join(ROOT, "bench.py"), "--impl",
+           "reference", "--gpus", "2", "--steps", "2", "--warmup", "1", "--cols-per-gpu", "1500", "--rows", "1000"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["extrapolated"] is False
+    assert "all 3000 columns" in d["cpu_baseline"]["sample"] and d["cpu_baseline"]["cores"] >= 1
