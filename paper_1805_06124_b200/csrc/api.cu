@@ -205,7 +205,7 @@ SweepArgs sweep_args(const rbg_ctx *c) {
     a.WQ = c->WQ;
     a.ldq_v = c->ldq_v;
     a.R = c->R;
-    a.ldr = c->M;
+    a.ldr = c->ldr;
     a.qi = -1;
     a.V = c->xmode ? c->S : nullptr;
     a.r2 = c->r2;
@@ -779,6 +779,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(cudaMemsetAsync(c->Q, 0, qbytes, c->stream));
     CUB(cudaMemsetAsync(c->WQ, 0, qbytes, c->stream));
     c->imgs_tm_ok = make_imgs_maps(c->WQ, c->Q, nvec, c->ldq_v, c->k_max, c->imgs_tm);
+    c->ldr = c->M;
     CUB(dmalloc(&c->R, (size_t)c->k_max * c->M * c->se));
     CUB(cudaMemsetAsync(c->R, 0, (size_t)c->k_max * c->M * c->se, c->stream));
     CUB(dmalloc(&c->r2, sizeof(double) * c->M));
@@ -996,7 +997,7 @@ rbg_status rbg_get_R(rbg_ctx *c, void *out, int64_t ldr, int on_device) {
     DevState h;
     TRY(read_state(c, &h));
     if (h.k)
-        CU(cudaMemcpy2D(out, (size_t)ldr * c->se, c->R, (size_t)c->M * c->se, (size_t)c->M * c->se, h.k,
+        CU(cudaMemcpy2D(out, (size_t)ldr * c->se, c->R, (size_t)c->ldr * c->se, (size_t)c->M * c->se, h.k,
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
     return RBG_OK;
 }

@@ -80,20 +80,26 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     double2 *S1n = c->S1;
     double *R1 = c->R, *r21 = c->r2;
     long long *gid1 = c->gid;
+    // R keeps a row stride with room for appended columns: an append within it writes the new
+    // columns' rows in place; beyond it R is reallocated with 1/8 (>= 4,096 columns) of slack
+    // and rows 0..k-1 copied (rows >= k are written by later sweeps before anything reads them)
+    const bool grow_r = M1 > c->ldr;
+    const long long ldr1 = grow_r ? M1 + std::max<long long>(M1 / 8, 4096) : c->ldr;
     cudaError_t e = cudaSuccess;
     if (M_f > 0) {
         S1n = nullptr;
-        R1 = nullptr;
         r21 = nullptr;
         e = dmalloc(&S1n, pitch * (ext0 + M_f));
         if (e == cudaSuccess && ext0) e = cudaMemcpyAsync(S1n, c->S1, pitch * ext0, cudaMemcpyDeviceToDevice, c->stream);
         if (e == cudaSuccess) e = cudaMemcpyAsync(S1n + ext0 * c->nvec, Fd, pitch * M_f, cudaMemcpyDeviceToDevice, c->stream);
-        if (e == cudaSuccess) e = dmalloc(&R1, (size_t)c->k_max * M1 * c->se);
+        if (grow_r) {
+            R1 = nullptr;
+            if (e == cudaSuccess) e = dmalloc(&R1, (size_t)c->k_max * ldr1 * c->se);
+            if (e == cudaSuccess && h.k)
+                e = cudaMemcpy2DAsync(R1, (size_t)ldr1 * c->se, c->R, (size_t)c->ldr * c->se, (size_t)M0 * c->se, h.k,
+                                      cudaMemcpyDeviceToDevice, c->stream);
+        }
         if (e == cudaSuccess) e = dmalloc(&r21, sizeof(double) * M1);
-        if (e == cudaSuccess) e = cudaMemsetAsync(R1, 0, (size_t)c->k_max * M1 * c->se, c->stream);
-        if (e == cudaSuccess && h.k)
-            e = cudaMemcpy2DAsync(R1, (size_t)M1 * c->se, c->R, (size_t)M0 * c->se, (size_t)M0 * c->se, h.k,
-                                  cudaMemcpyDeviceToDevice, c->stream);
         if (e == cudaSuccess) e = cudaMemcpyAsync(r21, c->r2, sizeof(double) * M0, cudaMemcpyDeviceToDevice, c->stream);
         if (e == cudaSuccess && sharded) {
             // global indices: the rank's original block, earlier appends, then these columns
@@ -112,7 +118,7 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     auto drop_new = [&]() {
         if (M_f > 0) {
             dfree(S1n);
-            dfree(R1);
+            if (R1 != c->R) dfree(R1);
             dfree(r21);
             if (gid1 != c->gid) dfree(gid1);
         }
@@ -124,7 +130,7 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     if (c->started && M_f > 0) {
         // the new columns get R rows 0..k-1 and the recurrence residual, then the pivot
         // search restarts over all columns and the next iteration begins at the decision
-        rbg_status st = coeff_passes(c, S1n + ext0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), M1, r21 + M0, h.k);
+        rbg_status st = coeff_passes(c, S1n + ext0 * c->nvec, M_f, R1 + (size_t)M0 * (c->se / 8), ldr1, r21 + M0, h.k);
         if (st != RBG_OK) {
             drop_new();
             return st;
@@ -132,11 +138,12 @@ rbg_status rbg_add_columns_ex(rbg_ctx *c, const void *F, int64_t M_f, int64_t ld
     }
     if (M_f > 0) {
         dfree(c->S1);
-        dfree(c->R);
+        if (R1 != c->R) dfree(c->R);
         dfree(c->r2);
         if (gid1 != c->gid) dfree(c->gid);
         c->S1 = S1n;
         c->R = R1;
+        c->ldr = ldr1;
         c->r2 = r21;
         c->gid = gid1;
         c->M = M1;
@@ -196,7 +203,7 @@ rbg_status rbg_restore(rbg_ctx *c, int64_t k, const int64_t *pivots, const doubl
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(c->Q, pitch, Q, (size_t)ldq * c->se, col, k, kind, c->stream);
     if (e == cudaSuccess) e = launch_weight_basis(c->WQ, c->Q, k, c->ldq_v, c->nvec, c->w, c->cplx, c->stream);
     if (e == cudaSuccess)
-        e = cudaMemcpy2DAsync(c->R, (size_t)c->M * c->se, R, (size_t)ldr * c->se, (size_t)c->M * c->se, k, kind, c->stream);
+        e = cudaMemcpy2DAsync(c->R, (size_t)c->ldr * c->se, R, (size_t)ldr * c->se, (size_t)c->M * c->se, k, kind, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->r2, r2, sizeof(double) * c->M, kind, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->piv, pivots, sizeof(long long) * k, kind, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->errors, errors, sizeof(double) * k, kind, c->stream);
@@ -239,7 +246,7 @@ rbg_status gram_device(rbg_ctx *c, int k, int kp, const double2 *G0, double2 *G)
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(tiles_d, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess)
-        e = launch_gram(c->R, c->M, k, c->M, c->cplx, P, kGramChunk, nchunks, tiles_d, (int)tiles.size(), c->stream);
+        e = launch_gram(c->R, c->ldr, k, c->M, c->cplx, P, kGramChunk, nchunks, tiles_d, (int)tiles.size(), c->stream);
     if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G0, G, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     dfree(tiles_d);

@@ -62,6 +62,7 @@ struct rbg_ctx {
     double *w = nullptr;
     double2 *Q = nullptr, *WQ = nullptr;
     double *R = nullptr, *r2 = nullptr;
+    long long ldr = 0;  // R row stride in elements (>= M: room for appended columns, rbg_add_columns)
     DevState *st = nullptr;
     double *errors = nullptr, *rdiag = nullptr;
     long long *piv = nullptr;
