@@ -199,7 +199,9 @@ def test_gpu_enrichment_device_v_borrowed_s_not_copied(orc):
         ctx.run()
         hist, ok = rbg.enrich(ctx, Vt, tol, rounds=4)
         g = ctx.result()
+        G = ctx.gram()                       # R now has a row stride with slack (ldr > M)
     assert ok == ok_o and hist == hist_o
+    np.testing.assert_array_equal(G, orc.gram(res.R))
     assert (g.k, g.stop) == (res.k, res.stop)
     for key in ("pivots", "errors", "nu", "Q", "R", "r2"):
         np.testing.assert_array_equal(getattr(g, key), getattr(res, key))
