@@ -778,7 +778,7 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     CUB(dmalloc(&c->WQ, qbytes));
     CUB(cudaMemsetAsync(c->Q, 0, qbytes, c->stream));
     CUB(cudaMemsetAsync(c->WQ, 0, qbytes, c->stream));
-    c->imgs_tm_ok = make_imgs_maps(c->WQ, c->Q, nvec, c->ldq_v, c->k_max, c->imgs_tm);
+    c->imgs_tm_ok = make_imgs_maps(c->Q, nvec, c->ldq_v, c->k_max, c->imgs_tm);
     c->ldr = c->M;
     CUB(dmalloc(&c->R, (size_t)c->k_max * c->M * c->se));
     CUB(cudaMemsetAsync(c->R, 0, (size_t)c->k_max * c->M * c->se, c->stream));

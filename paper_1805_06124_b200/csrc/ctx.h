@@ -102,7 +102,7 @@ struct rbg_ctx {
     cudaStream_t poll_stream = nullptr;  // polled rbg_run: reads the stop flag between batches
     int *poll_h = nullptr;               // pinned host word for that read
     rbg_ortho ortho = RBG_ORTHO_MGS;
-    alignas(64) unsigned char imgs_tm[256] = {};  // tensor maps of WQ and Q (k_imgs' basis pipe)
+    alignas(64) unsigned char imgs_tm[128] = {};  // tensor map of Q (k_imgs' basis pipe)
     bool imgs_tm_ok = false;
     bool xmode = false;          // explicit residuals (Algorithm 2 updates)
     double *w_true = nullptr;    // explicit mode: the caller's weights (w holds ones)

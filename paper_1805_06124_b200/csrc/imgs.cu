@@ -208,30 +208,6 @@ __device__ __forceinline__ ClusterReducerPre<16> make_reducer(double2 (*slots)[6
 }
 
 template <bool CPLX, int MAXV>
-__device__ __forceinline__ double nrm_partial(const double2 (&v)[MAXV], const double *w, int u0, int nm) {
-    double acc = 0.0;
-#pragma unroll
-    for (int m = 0; m < MAXV; m++) {
-        if (m < nm) {  // CAC rule 4
-            const int u = u0 + m * kLaneImgs;
-            if (CPLX) {
-                const double wu = w[u];
-                double t = wu * v[m].x;
-                acc = fma(t, v[m].x, acc);
-                t = wu * v[m].y;
-                acc = fma(t, v[m].y, acc);
-            } else {
-                double t = w[2 * u] * v[m].x;
-                acc = fma(t, v[m].x, acc);
-                t = w[2 * u + 1] * v[m].y;
-                acc = fma(t, v[m].y, acc);
-            }
-        }
-    }
-    return acc;
-}
-
-template <bool CPLX, int MAXV>
 __device__ __forceinline__ void dot_partial(const double2 (&v)[MAXV], const double2 *wq, int stride, int nm,
                                             double &pr, double &pi) {
     pr = 0.0;
@@ -322,12 +298,50 @@ __device__ __forceinline__ void load_slice(double2 (&r)[MAXV], const double2 *p,
     for (int m = 0; m < MAXV; m++) r[m] = (m < nm) ? p[m * stride] : make_double2(0.0, 0.0);
 }
 
-// Basis-vector pipeline.  STAGED (D > 0): the CTA's slices of w o q_b and q_b (MAXV chunks of
-// 256 vectors: chunk m starts at vector 2048 m + 256 rank) are prefetched D MGS steps ahead
-// into shared memory by TMA bulk copies issued by a dedicated producer warp (warp 8), one
-// full-mbarrier (TMA bytes) and one empty-mbarrier (8 consumer warps) per stage, so issuing
-// copies never delays a warp on the reduction's critical path.  D = 0: the slices are loaded
-// straight from global memory one step ahead (large N only).
+// The weights of this lane's vectors, held in registers for the whole kernel: (w_u, w_u) for
+// complex data, (w_2u, w_2u+1) for real data packed in pairs -- so that w o q_b is formed from
+// the staged q_b alone.  wr.x * q.x is the same IEEE product the kernel stores into WQ (a1), so
+// the dot's operand has the same bits as the stored w o q_b and only Q needs staging.
+template <bool CPLX, int MAXV>
+__device__ __forceinline__ void load_weights(double2 (&wr)[MAXV], const double *w, int u0, int nm) {
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) {
+        const int u = u0 + m * kLaneImgs;
+        if (m < nm) wr[m] = CPLX ? make_double2(w[u], w[u]) : make_double2(w[2 * u], w[2 * u + 1]);
+        else wr[m] = make_double2(0.0, 0.0);
+    }
+}
+
+template <int MAXV>
+__device__ __forceinline__ void weigh(double2 (&e)[MAXV], const double2 (&wr)[MAXV], const double2 (&q)[MAXV]) {
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) e[m] = make_double2(wr[m].x * q[m].x, wr[m].y * q[m].y);
+}
+
+// the weighted squared norm's lane partial, CAC rule 4 (w_u v.x v.x + w_u v.y v.y in this order)
+template <int MAXV>
+__device__ __forceinline__ double nrm_regs(const double2 (&v)[MAXV], const double2 (&wr)[MAXV], int nm) {
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < MAXV; m++) {
+        if (m < nm) {
+            double t = wr[m].x * v[m].x;
+            acc = fma(t, v[m].x, acc);
+            t = wr[m].y * v[m].y;
+            acc = fma(t, v[m].y, acc);
+        }
+    }
+    return acc;
+}
+
+// Basis-vector pipeline.  STAGED (D > 0): the CTA's slice of q_b (MAXV chunks of THREADS
+// vectors: chunk m starts at vector 2048 m + THREADS rank) is prefetched up to D MGS steps
+// ahead into shared memory by TMA issued by a dedicated producer warp (the last warp), one
+// full-mbarrier (TMA bytes) and one empty-mbarrier (the consumer warps) per stage, so issuing
+// copies never delays a warp on the reduction's critical path.  w o q_b is formed in registers
+// (weigh), so only Q is staged: half the TMA bytes and half the shared-memory reads of staging
+// both arrays (round 2).  D = 0: the slices of WQ and Q are loaded straight from global memory
+// one step ahead (large N only).
 // 4D tensor-map TMA: (x, rank, chunk, basis index) -> one CTA's MAXV chunk slices in one copy.
 __device__ __forceinline__ void tma_4d_g2s(void *dst, const CUtensorMap *map, int x, int y, int z, int w, uint64_t *bar) {
     asm volatile(
@@ -341,29 +355,27 @@ template <int MAXV, int D, int THREADS>
 struct BasisPipe {
     unsigned char *smem;
     uint64_t *full, *empty;
-    const double2 *WQ, *Q;
+    const double2 *Q;
     long long ldq_v;
     int k, rank, nvec;
-    // 16 x 128 lanes: one tensor-map copy per array and stage (tmW / tmQ view the basis as
-    // [basis][chunk][rank][128 vectors]; the allocations are padded so that the box of the last
-    // chunk stays in bounds, its vectors past nvec are never read); else MAXV bulk copies each.
+    // 16 x 128 lanes: one tensor-map copy per stage (tmQ views the basis as
+    // [basis][chunk][rank][128 vectors]; the allocation is padded so that the box of the last
+    // chunk stays in bounds, its vectors past nvec are never read); else MAXV bulk copies.
     // Per-SM TMA work is what limits the prefetch: with 10 bulk copies per stage a stage was
     // issued only ~1.3 us (~1.6 MGS steps) before it was needed (RBG_DEBUG_IMGS).
-    const CUtensorMap *tmW, *tmQ;
+    const CUtensorMap *tmQ;
 
-    static constexpr int kStageBytes = 2 * MAXV * THREADS * 16;
+    static constexpr int kStageBytes = MAXV * THREADS * 16;
 
-    __device__ __forceinline__ double2 *wq_stage(long long s) const {
+    __device__ __forceinline__ double2 *q_stage(long long s) const {
         return reinterpret_cast<double2 *>(smem + (size_t)(s % D) * kStageBytes);
     }
-    __device__ __forceinline__ double2 *q_stage(long long s) const { return wq_stage(s) + MAXV * THREADS; }
 
     __device__ void issue(long long s) const {  // one producer thread
         const int b = (int)(s % k);
-        if (tmW) {
+        if (tmQ) {
             uint64_t *bar = &full[s % D];
             mbar_arrive_expect_tx(bar, (uint32_t)kStageBytes);
-            tma_4d_g2s(wq_stage(s), tmW, 0, rank, 0, b, bar);
             tma_4d_g2s(q_stage(s), tmQ, 0, rank, 0, b, bar);
             return;
         }
@@ -374,17 +386,16 @@ struct BasisPipe {
             const int u0 = m * kLaneImgs + rank * THREADS;
             const int l = nvec - u0;
             len[m] = l < 0 ? 0 : (l > THREADS ? THREADS : l);
-            bytes += 2u * (uint32_t)len[m] * 16u;
+            bytes += (uint32_t)len[m] * 16u;
         }
         uint64_t *bar = &full[s % D];
         mbar_arrive_expect_tx(bar, bytes);
-        const double2 *wq = WQ + (long long)b * ldq_v, *q = Q + (long long)b * ldq_v;
-        double2 *dw = wq_stage(s), *dq = q_stage(s);
+        const double2 *q = Q + (long long)b * ldq_v;
+        double2 *dq = q_stage(s);
 #pragma unroll
         for (int m = 0; m < MAXV; m++) {
             if (len[m] > 0) {
                 const int u0 = m * kLaneImgs + rank * THREADS;
-                bulk_g2s(dw + m * THREADS, wq + u0, (uint32_t)len[m] * 16u, bar);
                 bulk_g2s(dq + m * THREADS, q + u0, (uint32_t)len[m] * 16u, bar);
             }
         }
@@ -419,7 +430,7 @@ struct BasisPipe {
 
 template <bool CPLX, int MAXV, int D, int CTAS, bool PRE>
 __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
-    k_imgs(const ImgsArgs a, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmQ) {
+    k_imgs(const ImgsArgs a, const __grid_constant__ CUtensorMap tmQ) {
     constexpr int THREADS = kLaneImgs / CTAS;  // consumer threads per CTA (one lane each)
     constexpr int DD = D > 0 ? D : 1;
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -428,6 +439,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
     __shared__ __align__(8) uint64_t s_bars[2];
     __shared__ __align__(8) uint64_t s_full[DD], s_empty[DD];
     __shared__ long long s_done;
+    __shared__ long long s_sub[3];  // RBG_DEBUG_IMGS sub-phase clocks (CTA 0, thread 0)
 
     // state written by the previous decision kernel (stop, k) and the basis q_1..q_k are final
     // before this kernel starts even as a programmatic dependent of the sweep (the sweep waits
@@ -453,8 +465,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
     const int nm = (!producer && u0 < nvec) ? (nvec - u0 + kLaneImgs - 1) / kLaneImgs : 0;
     const bool odd_tail = !CPLX && (a.N & 1);
 
-    const BasisPipe<MAXV, DD, THREADS> pipe{dsm,       s_full, s_empty, a.WQ, a.Q, a.ldq_v, (int)k, (int)rank, nvec,
-                                            a.use_tm ? &tmW : nullptr, a.use_tm ? &tmQ : nullptr};
+    const BasisPipe<MAXV, DD, THREADS> pipe{dsm,       s_full, s_empty, a.Q, a.ldq_v, (int)k, (int)rank, nvec,
+                                            a.use_tm ? &tmQ : nullptr};
     const long long limit = (long long)kNuMax * k;  // MGS steps that can ever be needed
     // stages issued before the cluster barrier (the rest by the producer loop, off the
     // critical path: each stage is 2 MAXV bulk copies issued by one thread)
@@ -524,7 +536,9 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
     using Red = typename std::conditional<PRE, ClusterReducerPre<CTAS>, ClusterReducer<CTAS>>::type;
     Red red = make_reducer<Red>(s_slots, s_wp, s_bars, rank, warp, lane);
     const uint64_t keep = policy_evict_last();
-    const double n0 = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
+    double2 wr[MAXV];
+    load_weights<CPLX, MAXV>(wr, a.w, u0, nm);
+    const double n0 = sqrt(red.sum(nrm_regs<MAXV>(v, wr, nm), 0.0).x);
     if (ts) ts[3] = globaltimer_ns();
     double n_prev = n0, nn = 0.0;
     int nu = 0;
@@ -539,60 +553,82 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
             q[mm] = (mm < nm) ? ld_keep(a.Q + u0 + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
         }
     }
-    // staged path: the slice of w o q_s is in registers before step s begins (loaded while the
-    // partials of step s - 1 were in flight), q_s is loaded while those of step s travel
-    double2 wqr[MAXV];
+    // staged path: q_s and w o q_s are in registers before step s begins (stage s was read,
+    // and released, while the partials of step s - 1 were in flight)
+    double2 wqr[MAXV], qc[MAXV];
     if (D > 0 && k > 0) {
         mbar_wait(&s_full[0], 0u);
-        load_slice<MAXV>(wqr, pipe.wq_stage(0) + tid, THREADS, nm);
+        load_slice<MAXV>(qc, pipe.q_stage(0) + tid, THREADS, nm);
+        weigh<MAXV>(wqr, wr, qc);
+        __syncwarp();
+        if (lane == 31) mbar_arrive(&s_empty[0]);
     }
+    // one MGS step of the staged path: q_s in qcur (and w o q_s in wqr) on entry; stage s + 1
+    // lands in qnext (and w o q_{s+1} in wqr).  Slots past nm hold zeros in v, wr, wqr and the
+    // staged slices, so the dot / axpy run over all MAXV slots without predicates: the extra
+    // terms are fma(+-0, +-0, x) = x for x != 0 and +0 for x = +0, and no partial is ever -0
+    // (each starts at +0), so the bits are those of the nm-term chains (CAC rules 2, 9).
+    auto mgs_step = [&](double2 (&qcur)[MAXV], double2 (&qnext)[MAXV]) {
+        double pr, pi;
+        // RBG_DEBUG_IMGS: clock64 at the phase boundaries of steps 64..95 (CTA 0, tid 0)
+        const bool tr = a.trace && rank == 0 && tid == 0 && s >= 64 && s < 96;
+        // every CTA's %globaltimer at step start / partial sent / coefficient known for
+        // steps 64..71 (trace[512 + (rank*8 + step)*4 + p]; p = 3: the next stage is in
+        // shared memory): the cluster's critical path
+        unsigned long long *gt = (a.trace && tid == 0 && s >= 64 && s < 72)
+                                     ? reinterpret_cast<unsigned long long *>(a.trace) + 512 + (rank * 8 + (s - 64)) * 4
+                                     : nullptr;
+        if (gt) gt[0] = globaltimer_ns();
+        const long long c0 = tr ? clock64() : 0;
+        dot_regs<CPLX, MAXV>(v, wqr, MAXV, pr, pi);
+        const long long c1 = tr ? clock64() : 0;
+        // (shared, not a local array: a local array costs three stack stores per step)
+        long long *sb = s_sub;
+        if constexpr (PRE) red.sub = tr ? sb : nullptr;
+        red.start(pr, pi);
+        if (gt) gt[1] = globaltimer_ns();
+        const long long c2 = tr ? clock64() : 0;
+        // while the partials travel: stage s + 1 into registers, w o q_{s+1} formed, the
+        // stage released (lane 31 never issues st.async, so its release-arrive does not
+        // wait for a remote store)
+        if (s + 1 < limit) {
+            mbar_wait(&s_full[(s + 1) % DD], (uint32_t)(((s + 1) / DD) & 1));
+            load_slice<MAXV>(qnext, pipe.q_stage(s + 1) + tid, THREADS, nm);
+            weigh<MAXV>(wqr, wr, qnext);
+            __syncwarp();
+            if (lane == 31) mbar_arrive(&s_empty[(s + 1) % DD]);
+        }
+        if (gt) gt[3] = globaltimer_ns();
+        const long long c3 = tr ? clock64() : 0;
+        const double2 c = red.finish();
+        if (gt) gt[2] = globaltimer_ns();
+        const long long c4 = tr ? clock64() : 0;
+        axpy_regs<CPLX, MAXV>(v, qcur, MAXV, c);
+        if (tr) {
+            const long long c5 = clock64();
+            long long *t = a.trace + (s - 64) * 8;
+            t[0] = c0; t[1] = c1; t[2] = c2; t[3] = c3; t[4] = c4; t[5] = c5;
+            t[6] = sb[1]; t[7] = sb[2];
+        }
+        s++;
+    };
+    double2 qb[MAXV];  // the other register buffer of the staged path (q_{s+1})
     while (nu < kNuMax) {
         nu++;
-        for (long long i = 0; i < k; i++, s++) {
-            double pr, pi;
-            double2 c;
-            if (D > 0) {
-                // RBG_DEBUG_IMGS: clock64 at the phase boundaries of steps 64..95 (CTA 0, tid 0)
-                const bool tr = a.trace && rank == 0 && tid == 0 && s >= 64 && s < 96;
-                // every CTA's %globaltimer at step start / partial sent / coefficient known for
-                // steps 64..71 (trace[512 + (rank*8 + step)*4 + p]; p = 3: the next stage is in
-                // shared memory): the cluster's critical path
-                unsigned long long *gt = (a.trace && tid == 0 && s >= 64 && s < 72)
-                                             ? reinterpret_cast<unsigned long long *>(a.trace) + 512 + (rank * 8 + (s - 64)) * 4
-                                             : nullptr;
-                if (gt) gt[0] = globaltimer_ns();
-                const long long c0 = tr ? clock64() : 0;
-                dot_regs<CPLX, MAXV>(v, wqr, nm, pr, pi);
-                const long long c1 = tr ? clock64() : 0;
-                long long sb[3] = {0, 0, 0};
-                if constexpr (PRE) red.sub = tr ? sb : nullptr;
-                red.start(pr, pi);
-                if (gt) gt[1] = globaltimer_ns();
-                const long long c2 = tr ? clock64() : 0;
-                // while the partials travel: q_s and the next stage's w o q into registers
-                double2 qr[MAXV];
-                load_slice<MAXV>(qr, pipe.q_stage(s) + tid, THREADS, nm);
-                if (s + 1 < limit) {
-                    mbar_wait(&s_full[(s + 1) % DD], (uint32_t)(((s + 1) / DD) & 1));
-                    load_slice<MAXV>(wqr, pipe.wq_stage(s + 1) + tid, THREADS, nm);
+        if (D > 0) {
+            // two steps per trip with the buffers' roles swapped: no register copies
+            for (long long i = 0; i < k; i += 2) {
+                mgs_step(qc, qb);
+                if (i + 1 == k) {
+#pragma unroll
+                    for (int mm = 0; mm < MAXV; mm++) qc[mm] = qb[mm];  // odd k: once per pass
+                    break;
                 }
-                if (gt) gt[3] = globaltimer_ns();
-                const long long c3 = tr ? clock64() : 0;
-                c = red.finish();
-                if (gt) gt[2] = globaltimer_ns();
-                const long long c4 = tr ? clock64() : 0;
-                axpy_regs<CPLX, MAXV>(v, qr, nm, c);
-                // stage s consumed (the axpy used q_s); lane 31 never issues st.async, so its
-                // release-arrive does not wait for a remote store
-                __syncwarp();
-                if (lane == 31) mbar_arrive(&s_empty[s % DD]);
-                if (tr) {
-                    const long long c5 = clock64();
-                    long long *t = a.trace + (s - 64) * 8;
-                    t[0] = c0; t[1] = c1; t[2] = c2; t[3] = c3; t[4] = c4; t[5] = c5;
-                    t[6] = sb[1]; t[7] = sb[2];
-                }
-            } else {
+                mgs_step(qb, qc);
+            }
+        } else {
+            for (long long i = 0; i < k; i++, s++) {
+                double pr, pi;
                 dot_partial<CPLX, MAXV>(v, wq, 1, nm, pr, pi);
                 double2 wq_n[MAXV], q_n[MAXV];
                 const long long bn = (i + 1 < k) ? i + 1 : 0;
@@ -602,7 +638,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
                     wq_n[mm] = (mm < nm) ? ld_keep(wqp + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
                     q_n[mm] = (mm < nm) ? ld_keep(qp + mm * kLaneImgs, keep) : make_double2(0.0, 0.0);
                 }
-                c = red.sum(pr, pi);
+                const double2 c = red.sum(pr, pi);
                 axpy<CPLX, MAXV>(v, q, 1, nm, c);
 #pragma unroll
                 for (int mm = 0; mm < MAXV; mm++) {
@@ -611,14 +647,17 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
                 }
             }
         }
-        nn = sqrt(red.sum(nrm_partial<CPLX, MAXV>(v, a.w, u0, nm), 0.0).x);
+        nn = sqrt(red.sum(nrm_regs<MAXV>(v, wr, nm), 0.0).x);
         if (nn > n_prev / 2.0) {  // Hoffmann's test with kappa = 2
             accepted = true;
             break;
         }
         n_prev = nn;
     }
-    if (tid == 0) s_done = s;  // release the producer: it drains the copies it issued
+    // release the producer: it drains the copies it issued past the stages the consumers read
+    // (stages 0 .. s, or 0 .. limit - 1: stage s + 1 is read during step s, and once released the
+    // producer may already have reused its slot, so those slots must not be waited on again)
+    if (tid == 0) s_done = (k > 0 && s < limit) ? s + 1 : s;
     if (ts) ts[4] = globaltimer_ns();
     // the next sweep may now take the SMs this cluster does not use (earlier, its first loads
     // would compete with the latency-bound reductions for the memory system)
@@ -642,12 +681,7 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
         if (mm < nm) {
             const double2 qq = make_double2(v[mm].x / nn, v[mm].y / nn);
             st_keep(qo + u, qq, keep);
-            if (CPLX) {
-                const double wu = a.w[u];
-                st_keep(wqo + u, make_double2(wu * qq.x, wu * qq.y), keep);
-            } else {
-                st_keep(wqo + u, make_double2(a.w[2 * u] * qq.x, a.w[2 * u + 1] * qq.y), keep);
-            }
+            st_keep(wqo + u, make_double2(wr[mm].x * qq.x, wr[mm].y * qq.y), keep);
         }
     }
     if (leader) {
@@ -662,8 +696,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
 }
 
 // (MAXV, D): vectors per lane and prefetch depth, D * MAXV * 32 KB / CTAS of shared memory.
-// Tensor maps of WQ and Q for the 16 x 128 staged path (BasisPipe); false if not applicable.
-bool make_imgs_maps(const double2 *WQ, const double2 *Q, long long nvec, long long ldq_v, long long k_max, void *maps) {
+// The tensor map of Q for the 16 x 128 staged path (BasisPipe); false if not applicable.
+bool make_imgs_maps(const double2 *Q, long long nvec, long long ldq_v, long long k_max, void *map) {
     const int maxv = imgs_maxv(nvec);
     if (maxv == 0 || maxv > 8 || getenv("RBG_IMGS_BULK")) return false;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -675,20 +709,14 @@ bool make_imgs_maps(const double2 *WQ, const double2 *Q, long long nvec, long lo
             return false;
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    CUtensorMap *tm = static_cast<CUtensorMap *>(maps);
-    const void *base[2] = {WQ, Q};
-    for (int i = 0; i < 2; i++) {
-        // (256 doubles = 128 vectors) x 16 ranks x maxv chunks (2,048 vectors apart) x k_max
-        const cuuint64_t dims[4] = {256, 16, (cuuint64_t)maxv, (cuuint64_t)k_max};
-        const cuuint64_t strides[3] = {2048, 32768, (cuuint64_t)ldq_v * 16};
-        const cuuint32_t box[4] = {256, 1, (cuuint32_t)maxv, 1};
-        const cuuint32_t estr[4] = {1, 1, 1, 1};
-        if (encode(&tm[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void *>(base[i]), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return false;
-    }
-    return true;
+    // (256 doubles = 128 vectors) x 16 ranks x maxv chunks (2,048 vectors apart) x k_max
+    const cuuint64_t dims[4] = {256, 16, (cuuint64_t)maxv, (cuuint64_t)k_max};
+    const cuuint64_t strides[3] = {2048, 32768, (cuuint64_t)ldq_v * 16};
+    const cuuint32_t box[4] = {256, 1, (cuuint32_t)maxv, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return encode(static_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2 *>(Q), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int imgs_maxv(long long nvec) {
@@ -729,9 +757,9 @@ template <bool CPLX, int MAXV, int D, int CTAS>
 static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
     auto kern = imgs_pre() ? k_imgs<CPLX, MAXV, D, CTAS, true> : k_imgs<CPLX, MAXV, D, CTAS, false>;
     constexpr int THREADS = kLaneImgs / CTAS;
-    const size_t smem = D > 0 ? (size_t)D * 2 * MAXV * THREADS * 16 : 0;
+    const size_t smem = D > 0 ? (size_t)D * MAXV * THREADS * 16 : 0;
     cudaError_t e;
-    if (smem > 48 * 1024) {
+    if (smem > 0) {  // dynamic + static may pass 48 KB even when the dynamic part alone does not
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
@@ -756,12 +784,12 @@ static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.pdl ? 2 : 1;
-    // the tensor maps cut 128-vector slices: the 16 x 128 staged path only
+    // the tensor map cuts 128-vector slices: the 16 x 128 staged path only
     ImgsArgs b = a;
     b.use_tm = (a.use_tm && a.tm && CTAS == 16 && D > 0) ? 1 : 0;
     const CUtensorMap *tm = static_cast<const CUtensorMap *>(a.tm);
     static const CUtensorMap zero{};
-    e = cudaLaunchKernelEx(&cfg, kern, b, tm ? tm[0] : zero, tm ? tm[1] : zero);
+    e = cudaLaunchKernelEx(&cfg, kern, b, tm ? *tm : zero);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

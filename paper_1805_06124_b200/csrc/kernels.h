@@ -100,7 +100,7 @@ struct ImgsArgs {
     cudaGraphConditionalHandle cond;  // rbg_run's device loop (loop_exit), valid when use_cond
     int use_cond;
     int pdl;  // launch as a programmatic dependent of the preceding sweep (MGS kernel)
-    const void *tm;  // host copy of 2 CUtensorMap (WQ, Q) for the staged basis pipe, or NULL
+    const void *tm;  // host copy of the CUtensorMap of Q for the staged basis pipe, or NULL
     int use_tm;
 };
 
@@ -180,9 +180,9 @@ SweepConfig sweep_config(bool cplx, bool init, long long nvec, int num_sms, int 
 cudaError_t launch_sweep(const SweepArgs &a, bool cplx, bool init, const SweepConfig &cfg,
                          cudaStream_t s);
 int imgs_maxv(long long nvec);  // 0 if unsupported
-// Tensor maps (2 x CUtensorMap, 64-byte aligned) of WQ and Q for k_imgs' staged basis pipe;
+// The tensor map (one CUtensorMap, 64-byte aligned) of Q for k_imgs' staged basis pipe;
 // the basis allocations must extend imgs_basis_pad(nvec) vectors past k_max * ldq_v.
-bool make_imgs_maps(const double2 *WQ, const double2 *Q, long long nvec, long long ldq_v, long long k_max, void *maps);
+bool make_imgs_maps(const double2 *Q, long long nvec, long long ldq_v, long long k_max, void *map);
 inline long long imgs_basis_pad(long long nvec) { return (long long)imgs_maxv(nvec) * kLaneImgs; }
 // Hoffmann CGSCI variant (imgs_cgs.cu): cooperative grid, vbuf nvec vectors, cbuf k_max.
 int cgs_grid(int num_sms);
