@@ -357,20 +357,32 @@ rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_d
         if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, 3 * sizeof(unsigned long long), c->stream);
         if (e == cudaSuccess) {
             unsigned long long *trace = nullptr;  // RBG_DEBUG_JACOBI: phase timestamps of 8 rounds
-            if (block && getenv("RBG_DEBUG_JACOBI") && dmalloc(&trace, 32 * sizeof(unsigned long long)) != cudaSuccess)
+            if (block && getenv("RBG_DEBUG_JACOBI") && dmalloc(&trace, 128 * sizeof(unsigned long long)) != cudaSuccess)
                 trace = nullptr;
+            if (trace) cudaMemsetAsync(trace, 0, 128 * sizeof(unsigned long long), c->stream);
             if (e == cudaSuccess)
                 e = block ? launch_bjacobi(G, V, kp, reinterpret_cast<double2 *>(rots), flags, sweeps, c->num_sms,
                                            c->stream, trace)
                           : launch_jacobi(G, V, kp, rots, flags, sweeps, c->num_sms, c->stream);
             if (trace) {
-                unsigned long long tt[32];
+                unsigned long long tt[128];
                 cudaMemcpyAsync(tt, trace, sizeof tt, cudaMemcpyDeviceToHost, c->stream);
                 cudaStreamSynchronize(c->stream);
                 for (int r = 1; r < 8; r++)
                     fprintf(stderr, "rbg: bjacobi round %d: P1+bar %.1f us, P2+bar %.1f us, P3+bar %.1f us\n", r,
                             (tt[r * 4 + 1] - tt[r * 4]) * 1e-3, (tt[r * 4 + 2] - tt[r * 4 + 1]) * 1e-3,
                             (tt[r * 4 + 3] - tt[r * 4 + 2]) * 1e-3);
+                for (int r = 1; r < 8; r++)
+                    fprintf(stderr, "rbg: bjacobi round %d P1 (CTA 0): load+measure %.2f us, %d local rounds %.2f us, U store %.2f us\n",
+                            r, (tt[64 + r * 4] - tt[r * 4]) * 1e-3, 31, (tt[64 + r * 4 + 1] - tt[64 + r * 4]) * 1e-3,
+                            (tt[64 + r * 4 + 2] - tt[64 + r * 4 + 1]) * 1e-3);
+                fprintf(stderr, "rbg: bjacobi max off-diagonal ratio per sweep:");
+                for (int sw = 0; sw < 32 && tt[32 + sw]; sw++) {
+                    double v;
+                    std::memcpy(&v, &tt[32 + sw], sizeof v);
+                    fprintf(stderr, " %.2e", v);
+                }
+                fprintf(stderr, "\n");
                 dfree(trace);
             }
         }

@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
     for (; sweep < 40; sweep++) {
         unsigned long long *flag = &flags[sweep & 1];
         for (int r = 0; r < nb - 1; r++) {
-            const bool tr = trace && sweep == 0 && r < 8 && blockIdx.x == 0 && tid == 0;
+            const bool trc = trace && sweep == 0 && r < 8 && blockIdx.x == 0;  // CTA 0 (uniform)
+            const bool tr = trc && tid == 0;
             if (tr) trace[r * 4 + 0] = globaltimer_ns();
             // ---- P1: local problems
             for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
@@ -455,19 +456,29 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
                     U[a][b] = make_double2(a == b ? 1.0 : 0.0, 0.0);
                 }
                 __syncthreads();
-                for (int e = tid; e < kJL * kJL; e += blockDim.x) {  // convergence measure
-                    const int a = e % kJL, b = e / kJL;
-                    if (a < b) {
-                        const double2 c = A[a][b];
-                        const double ac = sqrt(c.x * c.x + c.y * c.y);
-                        if (ac > 0.0) {
-                            const double den = sqrt(fabs(A[a][a].x * A[b][b].x));
-                            atomicMax(flag, dbits(den > 0.0 ? ac / den : 1.0));
+                {  // convergence measure: the CTA's largest ratio, one atomic per CTA
+                    double mx = 0.0;   // ratios are >= 0: their bit patterns order as the values
+                    for (int e = tid; e < kJL * kJL; e += blockDim.x) {
+                        const int a = e % kJL, b = e / kJL;
+                        if (a < b) {
+                            const double2 c = A[a][b];
+                            const double ac = sqrt(c.x * c.x + c.y * c.y);
+                            if (ac > 0.0) {
+                                const double den = sqrt(fabs(A[a][a].x * A[b][b].x));
+                                mx = fmax(mx, den > 0.0 ? ac / den : 1.0);
+                            }
                         }
                     }
+#pragma unroll
+                    for (int h = 16; h > 0; h >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, h));
+                    if (lane == 0 && mx > 0.0) atomicMax(flag, dbits(mx));
                 }
                 // the local rounds run on the first 256 threads only (one per 2 x 2 block of the
                 // update), synchronised by a named barrier: cheaper than a 1,024-thread barrier
+                if (trc && pr == 0) {
+                    __syncthreads();
+                    if (tid == 0) trace[64 + r * 4] = globaltimer_ns();
+                }
                 if (tid < kJLoc)
                 for (int lr = 0; lr < kJL - 1; lr++) {
                     if (tid < kJL / 2) {
@@ -514,9 +525,11 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
                     asm volatile("bar.sync 1, %0;" ::"r"(kJLoc) : "memory");
                 }
                 __syncthreads();
+                if (tr && pr == 0) trace[64 + r * 4 + 1] = globaltimer_ns();
                 double2 *Up = Us + (size_t)pr * kJL * kJL;   // column-major 32 x 32
                 for (int e = tid; e < kJL * kJL; e += blockDim.x) Up[e] = U[e % kJL][e / kJL];
                 __syncthreads();
+                if (tr && pr == 0) trace[64 + r * 4 + 2] = globaltimer_ns();
             }
             grid_barrier(bar, bar + 1, nblocks);
             if (tr) trace[r * 4 + 1] = globaltimer_ns();
@@ -589,6 +602,7 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
             if (tr) trace[r * 4 + 3] = globaltimer_ns();
         }
         const double off = __longlong_as_double((long long)*(volatile unsigned long long *)flag);
+        if (trace && blockIdx.x == 0 && tid == 0 && sweep < 32) trace[32 + sweep] = dbits(off);
         grid_barrier(bar, bar + 1, nblocks);
         if (blockIdx.x == 0 && tid == 0) flags[(sweep + 1) & 1] = 0ull;
         grid_barrier(bar, bar + 1, nblocks);
