@@ -236,20 +236,39 @@ namespace {
 rbg_status gram_device(rbg_ctx *c, int k, int kp, const double2 *G0, double2 *G) {
     const long long nchunks = std::max<long long>(1, (c->M + kGramChunk - 1) / kGramChunk);
     const int nt = (k + gram_tile() - 1) / gram_tile();
-    std::vector<int2> tiles;
+    // work items {tile a, tile b, chunk}, heaviest tiles first (FMA count of the tile's 16-row
+    // groups below k, the diagonal tiles' lower groups skipped), chunk-major within a class
+    const int gs = gram_tile() / 16;
+    auto groups = [&](int t) { return std::min(gs, (k - t * gram_tile() + 15) / 16); };
+    std::vector<std::pair<int, int2>> tiles;  // (cost, tile)
     for (int a = 0; a < nt; a++)
-        for (int b = a; b < nt; b++) tiles.push_back(make_int2(a, b));
-    int2 *tiles_d = nullptr;
+        for (int b = a; b < nt; b++) {
+            const int nu = groups(a), nv = groups(b);
+            int cost = 0;
+            for (int u = 0; u < nu; u++)
+                for (int v = 0; v < nv; v++) cost += (a != b || v >= u) ? 1 : 0;
+            tiles.push_back({cost, make_int2(a, b)});
+        }
+    std::stable_sort(tiles.begin(), tiles.end(), [](const auto &x, const auto &y) { return x.first > y.first; });
+    std::vector<int4> items;
+    for (size_t i = 0; i < tiles.size();) {
+        size_t j = i;
+        while (j < tiles.size() && tiles[j].first == tiles[i].first) j++;
+        for (long long ch = 0; ch < nchunks; ch++)
+            for (size_t t = i; t < j; t++) items.push_back(make_int4(tiles[t].second.x, tiles[t].second.y, (int)ch, 0));
+        i = j;
+    }
+    int4 *items_d = nullptr;
     double2 *P = nullptr;
-    cudaError_t e = dmalloc(&tiles_d, sizeof(int2) * tiles.size());
+    cudaError_t e = dmalloc(&items_d, sizeof(int4) * items.size());
     if (e == cudaSuccess) e = dmalloc(&P, sizeof(double2) * (size_t)nchunks * k * k);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(tiles_d, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c->stream);
+        e = cudaMemcpyAsync(items_d, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess)
-        e = launch_gram(c->R, c->ldr, k, c->M, c->cplx, P, kGramChunk, nchunks, tiles_d, (int)tiles.size(), c->stream);
+        e = launch_gram(c->R, c->ldr, k, c->M, c->cplx, P, kGramChunk, items_d, (int)items.size(), c->stream);
     if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G0, G, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    dfree(tiles_d);
+    dfree(items_d);
     dfree(P);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "gram: %s", cudaGetErrorString(e));
     return RBG_OK;

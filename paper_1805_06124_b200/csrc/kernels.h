@@ -206,7 +206,7 @@ struct Rot;
 constexpr long long kGramChunk = 4096;  // columns per Gram chunk (R30)
 int gram_tile();  // pairs per k_gram tile side
 cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool cplx, double2 *P, long long chunk,
-                        long long nchunks, int2 *tiles_d, int ntiles, cudaStream_t s);
+                        const int4 *items_d, int nitems, cudaStream_t s);
 cudaError_t launch_gram_reduce(const double2 *P, long long nchunks, int k, int kp, const double2 *G0, double2 *G,
                                cudaStream_t s);
 cudaError_t launch_jacobi(double2 *G, double2 *V, int kp, Rot *rots, unsigned long long *flags, int *sweeps,

@@ -120,17 +120,21 @@ __device__ __forceinline__ void gram_tile_nv(int nv, bool diag, unsigned char *s
 #undef RBG_GRAM_CASE
 }
 
+// One CTA per work item {tile a, tile b, chunk}: the host orders the items by decreasing
+// work (full off-diagonal tiles, edge tiles, diagonal tiles) and, within a class, chunk-major
+// (the tiles of one chunk run together and share R's slices in L2), so the block scheduler's
+// last wave is made of the cheapest items (round 2: 1,500 items over 296 slots = 5.07 waves).
 template <bool CPLX>
 __global__ void __launch_bounds__(256 + 32, 2) k_gram(const __grid_constant__ CUtensorMap tmR, int k, long long M,
-                                                      long long chunk, const int2 *tiles, double2 *P) {
+                                                      long long chunk, const int4 *items, double2 *P) {
     extern __shared__ __align__(1024) unsigned char gsm_raw[];
     unsigned char *stg = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);  // swizzle needs 1024-B tiles
     __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages];
     constexpr int kOpBytes = (CPLX ? 2 : 1) * kGBox;
-    const int2 t = tiles[blockIdx.x];
+    const int4 t = items[blockIdx.x];
     const int a0 = t.x * kGramTile, b0 = t.y * kGramTile;
     const bool diag = t.x == t.y;
-    const long long c = blockIdx.y;
+    const long long c = t.z;
     const long long j0 = c * chunk, j1 = (j0 + chunk < M) ? j0 + chunk : M;
     const long long nst = (j1 - j0 + kGramSub - 1) / kGramSub;
     const int tid = threadIdx.x;
@@ -694,7 +698,7 @@ cudaError_t launch_eig_sort(const double2 *G, int k, int kp, double tau2, int kr
 
 // ------------------------------------------------------------------ host launchers
 cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool cplx, double2 *P, long long chunk,
-                        long long nchunks, int2 *tiles_d, int ntiles, cudaStream_t s) {
+                        const int4 *items_d, int nitems, cudaStream_t s) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void *fn = nullptr;
@@ -734,8 +738,7 @@ cudaError_t launch_gram(const double *R, long long ldr, int k, long long M, bool
     const size_t smem = (size_t)kGStages * 2 * xs * kGBox + 1024;
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
-        dim3 grid(ntiles, (unsigned)nchunks);
-        kern<<<grid, 256 + 32, smem, s>>>(tm, k, M, chunk, tiles_d, P);
+        kern<<<nitems, 256 + 32, smem, s>>>(tm, k, M, chunk, items_d, P);
         e = cudaGetLastError();
     }
     if (Rp) {  // the caller synchronises before freeing its own buffers; so do we here
