@@ -118,9 +118,9 @@ struct ClusterReducer {
 // mbarriers double-buffered by parity as in ClusterReducer (a CTA's warp 0 sends reduction
 // n + 1 only after all its warps passed the named barrier of n + 1, i.e. after they read the
 // slots of reduction n).
-template <int CTAS>
+template <int CTAS, int THREADS = kLaneImgs / CTAS>
 struct ClusterReducerPre {
-    static constexpr int WPC = kLaneImgs / CTAS / 32;
+    static constexpr int WPC = THREADS / 32;
     double2 (*slots)[64];   // [parity][CTA]
     double2 (*wp)[32];      // [parity][warp]
     uint64_t *bars;
@@ -128,6 +128,7 @@ struct ClusterReducerPre {
     int warp, lane, par;
     uint32_t phase;
     long long *sub = nullptr;  // RBG_DEBUG_IMGS: clocks after butterfly / CTA tree / remote wait
+    double2 own{};             // CTAS == 1: the CTA partial is the sum (no exchange)
 
     __device__ __forceinline__ double2 sum(double re, double im) {
         start(re, im);
@@ -154,6 +155,10 @@ struct ClusterReducerPre {
 #pragma unroll
             for (int w = 0; w < WPC; w += 2 * h) t[w] = make_double2(t[w].x + t[w + h].x, t[w].y + t[w + h].y);
         if (sub) sub[1] = clock64();
+        if constexpr (CTAS == 1) {
+            own = t[0];  // every thread evaluated the CTA tree: nothing to exchange
+            return;
+        }
         if (warp == 0 && lane < CTAS) {
             const uint32_t dst = map_dsmem(smem_u32(&slots[par][rank]), (uint32_t)lane);
             const uint32_t bar = map_dsmem(smem_u32(&bars[par]), (uint32_t)lane);
@@ -162,6 +167,10 @@ struct ClusterReducerPre {
     }
 
     __device__ __forceinline__ double2 finish() {
+        if constexpr (CTAS == 1) {
+            par ^= 1;
+            return own;
+        }
         mbar_wait(&bars[par], (phase >> par) & 1u);
         if (sub) sub[2] = clock64();
         phase ^= 1u << par;
@@ -183,28 +192,17 @@ struct ClusterReducerPre {
     }
 };
 
-template <class Red>
-__device__ __forceinline__ Red make_reducer(double2 (*slots)[64], double2 (*wp)[32], uint64_t *bars, uint32_t rank,
-                                            int warp, int lane);
-template <>
-__device__ __forceinline__ ClusterReducer<8> make_reducer(double2 (*slots)[64], double2 (*)[32], uint64_t *bars,
-                                                          uint32_t rank, int warp, int lane) {
-    return ClusterReducer<8>{slots, bars, rank, warp, lane, 0, 0u};
+template <int CTAS, int T>
+__device__ __forceinline__ ClusterReducerPre<CTAS, T> make_reducer(ClusterReducerPre<CTAS, T> *, double2 (*slots)[64],
+                                                                 double2 (*wp)[32], uint64_t *bars, uint32_t rank,
+                                                                 int warp, int lane) {
+    return ClusterReducerPre<CTAS, T>{slots, wp, bars, rank, warp, lane, 0, 0u};
 }
-template <>
-__device__ __forceinline__ ClusterReducer<16> make_reducer(double2 (*slots)[64], double2 (*)[32], uint64_t *bars,
-                                                           uint32_t rank, int warp, int lane) {
-    return ClusterReducer<16>{slots, bars, rank, warp, lane, 0, 0u};
-}
-template <>
-__device__ __forceinline__ ClusterReducerPre<8> make_reducer(double2 (*slots)[64], double2 (*wp)[32], uint64_t *bars,
-                                                             uint32_t rank, int warp, int lane) {
-    return ClusterReducerPre<8>{slots, wp, bars, rank, warp, lane, 0, 0u};
-}
-template <>
-__device__ __forceinline__ ClusterReducerPre<16> make_reducer(double2 (*slots)[64], double2 (*wp)[32], uint64_t *bars,
-                                                              uint32_t rank, int warp, int lane) {
-    return ClusterReducerPre<16>{slots, wp, bars, rank, warp, lane, 0, 0u};
+template <int CTAS>
+__device__ __forceinline__ ClusterReducer<CTAS> make_reducer(ClusterReducer<CTAS> *, double2 (*slots)[64],
+                                                             double2 (*)[32], uint64_t *bars, uint32_t rank, int warp,
+                                                             int lane) {
+    return ClusterReducer<CTAS>{slots, bars, rank, warp, lane, 0, 0u};
 }
 
 template <bool CPLX, int MAXV>
@@ -428,10 +426,14 @@ struct BasisPipe {
     }
 };
 
-template <bool CPLX, int MAXV, int D, int CTAS, bool PRE>
-__global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
+// THREADS: consumer lanes per CTA, kLaneImgs / CTAS -- or 128 with CTAS in {1, 2, 4} when all
+// vectors sit in the first CTAS x 128 lanes (nvec <= 512, see launch_imgs): the lanes of the
+// other CTAs of the 16 x 128 layout would hold only zeros, their CTA partials are +0 and the
+// cross-CTA tree's nodes over them add +0 (x + 0 = x; no partial is ever -0), so the fewer-CTA
+// tree gives the 2,048-lane tree's bits (CAC rule 3) with fewer DSMEM messages.
+template <bool CPLX, int MAXV, int D, int CTAS, bool PRE, int THREADS = kLaneImgs / CTAS>
+__global__ void __launch_bounds__(THREADS + 32, 1)
     k_imgs(const ImgsArgs a, const __grid_constant__ CUtensorMap tmQ) {
-    constexpr int THREADS = kLaneImgs / CTAS;  // consumer threads per CTA (one lane each)
     constexpr int DD = D > 0 ? D : 1;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ double2 s_slots[2][64];
@@ -533,8 +535,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
     }
 
     const int warp = tid >> 5, lane = tid & 31;
-    using Red = typename std::conditional<PRE, ClusterReducerPre<CTAS>, ClusterReducer<CTAS>>::type;
-    Red red = make_reducer<Red>(s_slots, s_wp, s_bars, rank, warp, lane);
+    using Red = typename std::conditional<PRE, ClusterReducerPre<CTAS, THREADS>, ClusterReducer<CTAS>>::type;
+    Red red = make_reducer(static_cast<Red *>(nullptr), s_slots, s_wp, s_bars, rank, warp, lane);
     const uint64_t keep = policy_evict_last();
     double2 wr[MAXV];
     load_weights<CPLX, MAXV>(wr, a.w, u0, nm);
@@ -590,7 +592,8 @@ __global__ void __launch_bounds__(kLaneImgs / CTAS + 32, 1)
         const long long c2 = tr ? clock64() : 0;
         // while the partials travel: stage s + 1 into registers, w o q_{s+1} formed, the
         // stage released (lane 31 never issues st.async, so its release-arrive does not
-        // wait for a remote store)
+        // wait for a remote store).  (Loading the stage before the reduction instead: k = 299
+        // IMGS 369 -> 387 us, no gain on the one-CTA path either.)
         if (s + 1 < limit) {
             mbar_wait(&s_full[(s + 1) % DD], (uint32_t)(((s + 1) / DD) & 1));
             load_slice<MAXV>(qnext, pipe.q_stage(s + 1) + tid, THREADS, nm);
@@ -794,6 +797,47 @@ static cudaError_t launch_md(const ImgsArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Small N (nvec <= 512, one vector per lane): a cluster of CTAS in {1, 2, 4} CTAs x 128 lanes
+// (the occupied lanes of the 16 x 128 layout; same tree, same bits), CTA pre-reduction,
+// 16 basis stages of one bulk copy each.  RBG_IMGS_SMALL=0 keeps the 16-CTA cluster.
+template <bool CPLX, int CTAS>
+static cudaError_t launch_small(const ImgsArgs &a, cudaStream_t s) {
+    constexpr int THREADS = 128, D = 16;
+    auto kern = k_imgs<CPLX, 1, D, CTAS, true, THREADS>;
+    const size_t smem = (size_t)D * THREADS * 16;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CTAS, 1, 1);
+    cfg.blockDim = dim3(THREADS + 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CTAS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.pdl ? 2 : 1;
+    ImgsArgs b = a;
+    b.use_tm = 0;
+    static const CUtensorMap zero{};
+    e = cudaLaunchKernelEx(&cfg, kern, b, zero);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+static bool imgs_small() {
+    static int v = -1;
+    if (v < 0) {
+        v = 1;
+        if (const char *e = getenv("RBG_IMGS_SMALL")) v = atoi(e) != 0;
+    }
+    return v != 0;
+}
+
 template <bool CPLX, int CTAS>
 static cudaError_t launch_c(const ImgsArgs &a, cudaStream_t s) {
     // prefetch depth: the same shared-memory budget per CTA at either cluster size
@@ -813,6 +857,12 @@ static cudaError_t launch_c(const ImgsArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_imgs(const ImgsArgs &a, bool cplx, cudaStream_t s) {
+    if (a.nvec <= 512 && imgs_ctas() == 16 && imgs_small()) {
+        const int c = a.nvec <= 128 ? 1 : (a.nvec <= 256 ? 2 : 4);
+        if (c == 1) return cplx ? launch_small<true, 1>(a, s) : launch_small<false, 1>(a, s);
+        if (c == 2) return cplx ? launch_small<true, 2>(a, s) : launch_small<false, 2>(a, s);
+        return cplx ? launch_small<true, 4>(a, s) : launch_small<false, 4>(a, s);
+    }
     if (imgs_ctas() == 16) return cplx ? launch_c<true, 16>(a, s) : launch_c<false, 16>(a, s);
     return cplx ? launch_c<true, 8>(a, s) : launch_c<false, 8>(a, s);
 }
