@@ -101,6 +101,22 @@ def test_ragged_shapes(rbg, orc, N, M, cplx):
     compare(g, o)
 
 
+@pytest.mark.parametrize("N,cplx", [(128, True), (129, True), (256, True), (257, True), (512, True), (513, True),
+                                     (255, False), (257, False), (1023, False), (1025, False), (2048, True),
+                                     (2049, True)])
+def test_imgs_cluster_size_boundaries(rbg, orc, N, cplx):
+    """nvec around the IMGS layout switches (1, 2, 4 CTAs of 128 lanes up to 512 vectors, then the
+    16-CTA cluster; one vector per lane up to 2,048): same bits on both sides of each boundary,
+    with enough iterations for two MGS passes per pivot and an odd and even basis size."""
+    rng = np.random.default_rng(N * 131 + cplx)
+    M = 300
+    S = rng.standard_normal((M, N)) + (1j * rng.standard_normal((M, N)) if cplx else 0)
+    w = rng.uniform(0.5, 1.5, N)
+    for k_max in (37, 40):
+        g, o = both(rbg, orc, S, w, 0.0, k_max)
+        compare(g, o)
+
+
 def test_degenerate_inputs(rbg, orc):
     g = rbg.greedy(np.zeros((5, 4)), None, 0.0, 3)
     assert (g.k, g.stop, list(g.errors)) == (0, "RANK", [0.0])
