@@ -720,11 +720,28 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     c->col_offset = d->col_offset;
     c->M_global = Mg;
 
-    // snapshot matrix
+    // snapshot matrix.  A private copy is uploaded in chunks of ~1 GB on the context's stream;
+    // the finiteness scan of each chunk runs on a second stream as soon as the chunk has landed
+    // (it overlaps the next chunk's copy), and the verdict is read only at the end of create, so
+    // the host-side allocations below overlap the upload too (the e2e bench's create is bounded
+    // by the PCIe copy).
     const size_t col_bytes = (size_t)d->N * c->se;
+    unsigned long long *bad = nullptr, hbad = ~0ull;
+    struct FreeOnExit {  // the flag of a create that fails before the verdict is read
+        unsigned long long *&p;
+        ~FreeOnExit() {
+            if (p) dfree(p);
+        }
+    } bad_guard{bad};
+    if (d->check_finite) {  // first non-finite entry in column-major order, on the device
+        CUB(dmalloc(&bad, sizeof *bad));
+        CUB(cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream));
+    }
+    CUB(cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking));
     if (d->S_mem == RBG_MEM_DEVICE && d->borrow) {
         c->S = const_cast<double2 *>(static_cast<const double2 *>(d->S));
         c->ldv = cplx ? ld : ld / 2;
+        if (bad) CUB(launch_check_finite(c->S, c->ldv, c->M, c->N, nvec, cplx, bad, c->stream));
     } else {
         c->ldv = nvec;
         const size_t dst_pitch = (size_t)nvec * 16;
@@ -732,23 +749,42 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         c->own_S = true;
         if (dst_pitch != col_bytes) CUB(cudaMemsetAsync(c->S, 0, dst_pitch * d->M, c->stream));
         const cudaMemcpyKind kind = d->S_mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        if (dst_pitch == col_bytes && (size_t)ld * c->se == col_bytes)
-            CUB(cudaMemcpyAsync(c->S, d->S, col_bytes * d->M, kind, c->stream));
-        else
-            CUB(cudaMemcpy2DAsync(c->S, dst_pitch, d->S, (size_t)ld * c->se, col_bytes, d->M, kind, c->stream));
+        const bool flat = dst_pitch == col_bytes && (size_t)ld * c->se == col_bytes;
+        const long long per = std::max<long long>(1, (1LL << 30) / (long long)dst_pitch);   // columns per chunk
+        cudaEvent_t ev = nullptr;
+        if (bad) CUB(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        for (long long c0 = 0; c0 < d->M; c0 += per) {
+            const long long mc = std::min<long long>(per, d->M - c0);
+            const char *src = static_cast<const char *>(d->S) + (size_t)c0 * ld * c->se;
+            double2 *dst = c->S + (size_t)c0 * nvec;
+            cudaError_t e = flat ? cudaMemcpyAsync(dst, src, col_bytes * mc, kind, c->stream)
+                                 : cudaMemcpy2DAsync(dst, dst_pitch, src, (size_t)ld * c->se, col_bytes, mc, kind, c->stream);
+            if (e == cudaSuccess && bad) e = cudaEventRecord(ev, c->stream);
+            if (e == cudaSuccess && bad) e = cudaStreamWaitEvent(c->poll_stream, ev, 0);
+            if (e == cudaSuccess && bad) e = launch_check_finite(dst, nvec, mc, c->N, nvec, cplx, bad, c->poll_stream, c0);
+            if (e != cudaSuccess) {
+                if (ev) cudaEventDestroy(ev);
+                CUB(e);
+            }
+        }
+        if (bad) {  // the context's stream continues after every chunk's scan
+            cudaError_t e = cudaEventRecord(ev, c->poll_stream);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, ev, 0);
+            cudaEventDestroy(ev);
+            CUB(e);
+        }
     }
-    if (d->check_finite) {  // first non-finite entry in column-major order, on the device
-        unsigned long long *bad = nullptr, hbad = ~0ull;
-        CUB(dmalloc(&bad, sizeof *bad));
-        CUB(cudaMemcpyAsync(bad, &hbad, sizeof hbad, cudaMemcpyHostToDevice, c->stream));
-        CUB(launch_check_finite(c->S, c->ldv, c->M, c->N, nvec, cplx, bad, c->stream));
-        CUB(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, c->stream));
-        CUB(cudaStreamSynchronize(c->stream));
+    if (bad) CUB(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, c->stream));
+    auto nonfinite = [&]() -> bool {  // after a synchronisation of c->stream
+        if (!bad) return false;
         dfree(bad);
-        if (hbad != ~0ull)
-            return bail(fail(RBG_ENONFINITE, "non-finite S entry at (row %lld, col %lld)", (long long)(hbad % d->N),
-                             (long long)(hbad / d->N) + d->col_offset));
-    }
+        bad = nullptr;
+        return hbad != ~0ull;
+    };
+    auto nonfinite_fail = [&]() {
+        return bail(fail(RBG_ENONFINITE, "non-finite S entry at (row %lld, col %lld)", (long long)(hbad % d->N),
+                         (long long)(hbad / d->N) + d->col_offset));
+    };
 
     // weights (zero padded), basis, coefficients, state
     std::vector<double> wpad(2 * nvec + 2, 0.0);
@@ -761,6 +797,8 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         double2 *V = nullptr;
         if (c->own_S) V = c->S;                               // scale the private copy in place
         else CUB(dmalloc(&V, (size_t)nvec * 16 * c->M));
+        CUB(cudaStreamSynchronize(c->stream));  // the scan's verdict before S is scaled
+        if (nonfinite()) return nonfinite_fail();
         CUB(launch_scale_sqrtw(V, nvec, c->S, c->ldv, c->M, nvec, c->N, c->w_true, cplx, c->stream));
         c->S = V;
         c->own_S = true;
@@ -835,10 +873,10 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
     }
     // rbg_run's helpers, allocated here so that no run pays cudaHostAlloc / stream creation
     // (both synchronise with the device) between its iterations
-    CUB(cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking));
     CUB(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     CUB(cudaHostAlloc(&c->poll_h, sizeof(int), cudaHostAllocDefault));
     CUB(cudaStreamSynchronize(c->stream));
+    if (nonfinite()) return nonfinite_fail();
 #undef CUB
     *out = c;
     return RBG_OK;

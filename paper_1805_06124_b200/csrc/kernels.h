@@ -244,9 +244,10 @@ inline cudaError_t dmalloc(T **p, size_t bytes) {
 void debug_set_canary(bool on);
 long long debug_canary_violations(std::string *msg);
 
-// First non-finite entry of a device block: writes min(col * N + row) (or -1) to *out.
+// First non-finite entry of a device block: atomicMin of (col0 + col) * N + row into *out
+// (which the caller sets to ~0 first).
 cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
                                 long long nvec, bool cplx, unsigned long long *out,
-                                cudaStream_t s);
+                                cudaStream_t s, long long col0 = 0);
 
 }  // namespace rbg

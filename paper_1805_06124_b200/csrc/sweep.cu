@@ -767,7 +767,7 @@ cudaError_t launch_sqrt_clamp(const double *in, double *out, long long M, cudaSt
 
 // ------------------------------------------------------------------ finiteness scan
 __global__ void k_check_finite(const double2 *S, long long ldv, long long M, long long N,
-                               long long nvec, bool cplx, unsigned long long *out) {
+                               long long nvec, bool cplx, unsigned long long *out, long long col0) {
     const long long total = M * nvec;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
@@ -778,15 +778,15 @@ __global__ void k_check_finite(const double2 *S, long long ldv, long long M, lon
         if (!cplx && row0 + 1 >= N) bad1 = false;  // padding row
         if (bad0 || bad1) {
             const long long row = cplx ? u : (bad0 ? row0 : row0 + 1);
-            atomicMin(out, (unsigned long long)(c * N + row));
+            atomicMin(out, (unsigned long long)((c + col0) * N + row));
         }
     }
 }
 
 cudaError_t launch_check_finite(const double2 *S, long long ldv, long long M, long long N,
                                 long long nvec, bool cplx, unsigned long long *out,
-                                cudaStream_t s) {
-    k_check_finite<<<148 * 8, 256, 0, s>>>(S, ldv, M, N, nvec, cplx, out);
+                                cudaStream_t s, long long col0) {
+    k_check_finite<<<148 * 8, 256, 0, s>>>(S, ldv, M, N, nvec, cplx, out, col0);
     return cudaGetLastError();
 }
 
