@@ -750,7 +750,8 @@ rbg_status rbg_create_ex(rbg_ctx **out, const rbg_desc *d) {
         if (dst_pitch != col_bytes) CUB(cudaMemsetAsync(c->S, 0, dst_pitch * d->M, c->stream));
         const cudaMemcpyKind kind = d->S_mem == RBG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         const bool flat = dst_pitch == col_bytes && (size_t)ld * c->se == col_bytes;
-        const long long per = std::max<long long>(1, (1LL << 30) / (long long)dst_pitch);   // columns per chunk
+        long long per = std::max<long long>(1, (1LL << 30) / (long long)dst_pitch);   // columns per chunk
+        if (const char *e = getenv("RBG_UPLOAD_CHUNK_COLS")) per = std::max<long long>(1, atoll(e));   // tests
         cudaEvent_t ev = nullptr;
         if (bad) CUB(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         for (long long c0 = 0; c0 < d->M; c0 += per) {
