@@ -13,8 +13,10 @@
 // all-to-all of the CTA partials through distributed shared memory (st.async + mbarrier
 // transaction counts, no cluster barrier) and the cross-CTA tree evaluated by every thread,
 // after which every CTA holds the bit-identical coefficient and updates its slice of v.  The
-// basis slices are prefetched several steps ahead by TMA bulk copies from a producer warp.
-// The kernel is replicated on every GPU of a sharded run (no broadcast of q needed).
+// slices of q_b are prefetched several steps ahead by TMA from a producer warp (one 4D
+// tensor-map copy per stage) and w o q_b is formed in registers; for nvec <= 512 only the 1, 2
+// or 4 CTAs that hold vectors run (same tree, same bits).  The kernel is replicated on every
+// GPU of a sharded run (no broadcast of q needed).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -26,10 +28,12 @@
 
 namespace rbg {
 
-// Sum over the 2048 lanes with the balanced pairwise tree of CAC rule 3.
+// Sum over the 2048 lanes with the balanced pairwise tree of CAC rule 3 (ClusterReducer, the
+// RBG_IMGS_PRE=0 variant; the default ClusterReducerPre below adds a CTA pre-reduction).
 //  1. xor-butterfly in the warp (offsets 1..16): every lane holds its warp's partial;
-//  2. lanes 0..7 of warp w of CTA r st.async the partial into slot 8r+w of CTA 0..7's
-//     shared memory, each store counted (16 B) on the receiving CTA's mbarrier;
+//  2. lanes 0..CTAS-1 of warp w of CTA r st.async the partial into slot WPC r + w of every
+//     CTA's shared memory (WPC warps per CTA), each store counted (16 B) on the receiving
+//     CTA's mbarrier;
 //  3. every warp waits for its CTA's 64 slots (1024 B), then lane l adds slots 2l, 2l+1 and
 //     an xor-butterfly over the lanes finishes the tree over the 64 (CTA, warp) leaves.
 // No CTA or cluster barrier is needed; every warp of every CTA ends with the same bits.
