@@ -306,6 +306,162 @@ __global__ void __launch_bounds__(64) k_eim_solve_w(EimArgs a, int l, const __gr
     }
 }
 
+// IEEE num / den (round to nearest) from y = RN(1 / den), precomputed off the chain: q0 = num y,
+// then two FMA remainder corrections; with y correctly rounded and the second correction
+// starting within one ulp, the result is the correctly rounded quotient (Markstein's theorem)
+// whenever nothing over- or underflows -- guaranteed here by |num|, den in [2^-500, 2^500];
+// outside that range (and for num = 0, NaN, inf) the division itself is used.  Checked against
+// the division on 3.5e9 random and adversarial operand pairs (scripts/div_check.c,
+// tests/test_div_check.py): no difference.  Three dependent FMAs instead of the division's ~400-clock sequence on the
+// substitution's serial chain.
+__device__ __forceinline__ double div_rn_pre(double num, double den, double y, bool den_ok) {
+    const double an = fabs(num);
+    const double q0 = num * y;
+    const double q1 = fma(fma(-q0, den, num), y, q0);
+    const double q2 = fma(fma(-q1, den, num), y, q1);
+    if (den_ok && an >= 0x1p-500 && an <= 0x1p500) return q2;
+    if (num == 0.0) return num;   // 0 / den = +-0 exactly (den > 0)
+    return num / den;
+}
+
+// ---- multi-warp forward substitution (default, round 2) ----------------------------------
+// The serial chain of k_eim_solve_w is A(0) -> B(0,1) -> A(1) -> B(1,2) -> ... (phase A of a
+// block, then the next block's update by it); the other phase-B tiles (sb, s), s > sb + 1, only
+// have to be done before block s's turn.  So one main warp runs the chain (its tiles (sb, sb) and
+// (sb, sb+1) through the TMA ring), and helper warp s - 2 owns row block s >= 2: it applies the
+// tiles (0, s) .. (s-2, s) in increasing sb as each block's coefficients are published (an
+// mbarrier per block), reading T from L2 with 8 loads in flight, then hands its rows to the main
+// warp (an mbarrier per block).  Every row still receives its updates in increasing b, one
+// cmsub each, so the bits are those of the unblocked substitution.  Threads 32 (nblk + 1) for
+// nblk = ceil(l / 32) <= 31 row blocks.
+constexpr int kEimMwMaxBlk = 31;
+constexpr int kEimMwRing = 4;
+constexpr size_t kEimMwSmem = kEimMwRing * kEimTile + 2 * kEimMwRing * sizeof(uint64_t) +
+                              2 * 32 * sizeof(uint64_t) + 1024 * sizeof(double2) + 32 * 32 * sizeof(double2);
+
+__global__ void __launch_bounds__(1024) k_eim_solve_mw(EimArgs a, int l, const __grid_constant__ CUtensorMap tmT) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const double2(*ring)[32][32] = reinterpret_cast<const double2(*)[32][32]>(sm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + kEimMwRing * kEimTile), *empty = full + kEimMwRing;
+    uint64_t *coefbar = empty + kEimMwRing;        // [32]: block sb's coefficients are in s_c
+    uint64_t *vbar = coefbar + 32;                 // [32]: block s's rows are in s_v[s]
+    double2 *s_c = reinterpret_cast<double2 *>(vbar + 32);   // c_0 .. c_{l-1}
+    double2(*s_v)[32] = reinterpret_cast<double2(*)[32]>(s_c + 1024);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nblk = (l + 31) / 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kEimMwRing; i++) {
+            mbar_init_nofence(&full[i], 1);
+            mbar_init_nofence(&empty[i], 1);
+        }
+        for (int i = 0; i < 32; i++) {
+            mbar_init_nofence(&coefbar[i], 1);
+            mbar_init_nofence(&vbar[i], 1);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    if (warp == 1) {  // producer: the main warp's tiles (sb, sb), (sb, sb + 1) in its order
+        if (lane == 0) {
+            int n = 0;
+            for (int sb = 0; sb < nblk; sb++)
+                for (int s = sb; s < nblk && s <= sb + 1; s++, n++) {
+                    const int slot = n % kEimMwRing;
+                    if (n >= kEimMwRing) mbar_wait(&empty[slot], (uint32_t)((n / kEimMwRing - 1) & 1));
+                    mbar_arrive_expect_tx(&full[slot], (uint32_t)kEimTile);
+                    tma_tile_g2s((void *)&ring[slot][0][0], &tmT, s * 64, sb * 32, &full[slot]);
+                }
+        }
+        return;
+    }
+    if (warp >= 2) {  // helper for row block s = warp: tiles (0, s) .. (s - 2, s)
+        const int sblk = warp;
+        const int r = sblk * 32 + lane;
+        const bool mine = r < l;
+        double2 x = mine ? load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[r]) : make_double2(0.0, 0.0);
+        const int ncols = 32 * (sblk - 1);            // columns 0 .. 32 (s - 1) - 1, all full blocks
+        const double2 *tcol = a.Tt + r;               // Tt[b * k + r]
+        double2 tr[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) tr[j] = (mine && j < ncols) ? tcol[(long long)j * a.k] : make_double2(0.0, 0.0);
+        for (int b = 0; b < ncols; b += 8) {
+            if ((b & 31) == 0) mbar_wait(&coefbar[b >> 5], 0u);
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const double2 t = tr[j];
+                const int bn = b + 8 + j;
+                tr[j] = (mine && bn < ncols) ? tcol[(long long)bn * a.k] : make_double2(0.0, 0.0);
+                if (mine) x = cmsub(x, s_c[b + j], t);
+            }
+        }
+        s_v[sblk][lane] = x;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&vbar[sblk]);
+        return;
+    }
+    // main warp (warp 0)
+    double2 v = lane < l ? load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[lane]) : make_double2(0.0, 0.0);
+    int n = 0;
+    for (int sb = 0; sb < nblk; sb++) {
+        const int b0 = sb * 32, bl_end = l - b0 < 32 ? l - b0 : 32;
+        const int r = b0 + lane;
+        const double2 td = r < l ? a.Tt[(long long)r * a.k + r] : make_double2(1.0, 0.0);
+        const double dd = fma(td.x, td.x, td.y * td.y);
+        const double yy = 1.0 / dd;   // RN(1 / den) of this lane's column, off the chain
+        const int dok = dd >= 0x1p-500 && dd <= 0x1p500;
+        int slot = n % kEimMwRing;
+        mbar_wait(&full[slot], (uint32_t)((n / kEimMwRing) & 1));
+#pragma unroll 1
+        for (int bl = 0; bl < bl_end; bl++) {  // phase A: the same quotients as k_eim_solve_w
+            // every lane forms c_b itself from the owner's numerators (no divergent branch and
+            // no broadcast of the quotients); the tile entry is read before the chain needs it
+            const double2 t = ring[slot][bl][lane];
+            const double n1 = __shfl_sync(0xffffffffu, fma(v.x, td.x, v.y * td.y), bl);
+            const double n2 = __shfl_sync(0xffffffffu, fma(v.y, td.x, -(v.x * td.y)), bl);
+            const double den = __shfl_sync(0xffffffffu, dd, bl);
+            const double y = __shfl_sync(0xffffffffu, yy, bl);
+            const bool den_ok = __shfl_sync(0xffffffffu, dok, bl) != 0;
+            const double2 cb = make_double2(div_rn_pre(n1, den, y, den_ok), div_rn_pre(n2, den, y, den_ok));
+            if (lane == bl) {
+                a.c[b0 + bl] = cb;
+                s_c[b0 + bl] = cb;
+            }
+            if (lane > bl && lane < bl_end) v = cmsub(v, cb, t);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[slot]);
+            mbar_arrive(&coefbar[sb]);  // release: block sb's coefficients for the helpers
+        }
+        n++;
+        if (sb + 1 < nblk) {  // the next block's rows, then its update by block sb
+            double2 x;
+            if (sb + 1 >= 2) {
+                mbar_wait(&vbar[sb + 1], 0u);
+                x = s_v[sb + 1][lane];
+            } else {
+                x = 32 + lane < l ? load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[32 + lane]) : make_double2(0.0, 0.0);
+            }
+            slot = n % kEimMwRing;
+            mbar_wait(&full[slot], (uint32_t)((n / kEimMwRing) & 1));
+#pragma unroll 8
+            for (int bl = 0; bl < 32; bl++) x = cmsub(x, s_c[b0 + bl], ring[slot][bl][lane]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            n++;
+            v = x;
+        }
+    }
+}
+
+static cudaError_t launch_solve_mw(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
+    const int nblk = (l + 31) / 32;
+    cudaError_t e = cudaFuncSetAttribute(k_eim_solve_mw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEimMwSmem);
+    if (e != cudaSuccess) return e;
+    k_eim_solve_mw<<<1, 32 * (nblk > 2 ? nblk : 2), kEimMwSmem, s>>>(a, l, tm);
+    return cudaGetLastError();
+}
+
 // xi_l over all rows with a ring of kEimU loads in flight per thread (one row per thread, the
 // xi_b of row i consumed in increasing b: the oracle's sequential sum), maxloc as k_eim_residual.
 constexpr int kEimU = 32;
@@ -414,8 +570,18 @@ static cudaError_t launch_solve_w(const EimArgs &a, int l, const CUtensorMap &tm
     return cudaGetLastError();
 }
 
+static bool eim_single_warp() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("RBG_EIM");
+        v = (e && !strcmp(e, "warp1")) ? 1 : 0;
+    }
+    return v != 0;
+}
+
 static cudaError_t launch_solve(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
     const int slots = (l + 31) / 32;
+    if (slots <= kEimMwMaxBlk && !eim_single_warp()) return launch_solve_mw(a, l, tm, s);
     if (slots <= 1) return launch_solve_w<1>(a, l, tm, s);
     if (slots <= 2) return launch_solve_w<2>(a, l, tm, s);
     if (slots <= 4) return launch_solve_w<4>(a, l, tm, s);
