@@ -1,6 +1,6 @@
 #!/bin/bash
 # L2-resident prefix A/B (scripts/l2keep_probe.py) + config-2 bench with and without it.
-python scripts/l2keep_probe.py 0 32 64 96 > gpurun_out/l2keep_small.jsonl 2> gpurun_out/l2keep_small.err; echo small rc=$?
+python scripts/env_ab_probe.py RBG_L2_KEEP_MB 0 32 64 96 > gpurun_out/l2keep_small.jsonl 2> gpurun_out/l2keep_small.err; echo small rc=$?
 for rep in 1 2; do for mb in 0 48; do
 RBG_L2_KEEP_MB=$mb python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu > gpurun_out/l2keep_bench_$mb.$rep.json 2>/dev/null; echo bench $mb rc=$?
 python - <<PY
