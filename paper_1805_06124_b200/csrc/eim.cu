@@ -467,28 +467,14 @@ static cudaError_t launch_solve_mw(const EimArgs &a, int l, const CUtensorMap &t
 constexpr int kEimU = 32;
 constexpr int kEimThreadsW = 64;
 
-__global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int l) {
-    __shared__ double s_m[kEimThreadsW / 32];
-    __shared__ long long s_j[kEimThreadsW / 32];
+// The end of a residual step (every thread of the block): xi_l(i) stored, |xi_l(i)|^2 into the
+// block's maxloc, the last block to finish reduces the per-block records (ties: lowest row),
+// records the node p_l and gathers row l of T (T[l][b] = xi_b(p_l), b <= l).
+template <int WARPS>
+__device__ __forceinline__ void eim_residual_finish(const EimArgs &a, int l, double2 x, bool mine, long long i) {
+    __shared__ double s_m[WARPS];
+    __shared__ long long s_j[WARPS];
     __shared__ int s_last;
-    extern __shared__ double2 s_c[];  // c_0 .. c_{l-1}
-    for (int b = threadIdx.x; b < l; b += blockDim.x) s_c[b] = a.c[b];
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const bool mine = i < a.N;
-    double2 xr[kEimU];
-#pragma unroll
-    for (int t = 0; t < kEimU; t++) xr[t] = (mine && t < l) ? a.Xi[(long long)t * a.N + i] : make_double2(0.0, 0.0);
-    double2 x = mine ? load_q(a.Q, a.ldq_v, a.cplx, l, i) : make_double2(0.0, 0.0);
-    __syncthreads();
-    for (int b0 = 0; b0 < l; b0 += kEimU) {
-#pragma unroll
-        for (int t = 0; t < kEimU; t++) {
-            const int b = b0 + t, bn = b + kEimU;
-            const double2 xi = xr[t];
-            xr[t] = (mine && bn < l) ? a.Xi[(long long)bn * a.N + i] : make_double2(0.0, 0.0);
-            if (b < l) x = cmsub(x, s_c[b], xi);
-        }
-    }
     double bm = -1.0;
     long long bj = 0x7fffffffffffffffLL;
     if (mine) {
@@ -510,7 +496,7 @@ __global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < kEimThreadsW / 32; w++)
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++)  // WARPS >= the block's warps
             if (rec_better(s_m[w], s_j[w], bm, bj)) {
                 bm = s_m[w];
                 bj = s_j[w];
@@ -561,6 +547,114 @@ __global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int 
     }
 }
 
+__global__ void __launch_bounds__(kEimThreadsW) k_eim_residual_w(EimArgs a, int l) {
+    extern __shared__ double2 s_c[];  // c_0 .. c_{l-1}
+    for (int b = threadIdx.x; b < l; b += blockDim.x) s_c[b] = a.c[b];
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const bool mine = i < a.N;
+    double2 xr[kEimU];
+#pragma unroll
+    for (int t = 0; t < kEimU; t++) xr[t] = (mine && t < l) ? a.Xi[(long long)t * a.N + i] : make_double2(0.0, 0.0);
+    double2 x = mine ? load_q(a.Q, a.ldq_v, a.cplx, l, i) : make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int b0 = 0; b0 < l; b0 += kEimU) {
+#pragma unroll
+        for (int t = 0; t < kEimU; t++) {
+            const int b = b0 + t, bn = b + kEimU;
+            const double2 xi = xr[t];
+            xr[t] = (mine && bn < l) ? a.Xi[(long long)bn * a.N + i] : make_double2(0.0, 0.0);
+            if (b < l) x = cmsub(x, s_c[b], xi);
+        }
+    }
+    eim_residual_finish<kEimThreadsW / 32>(a, l, x, mine, i);
+}
+
+// The same step with the xi_b staged through shared memory by a 2D tensor-map TMA (round 2):
+// one CTA per SM owns `rows` consecutive rows (ceil(N / SMs), at most 128); a producer warp
+// streams the (rows x kEimSb) tiles of Xi -- rows r0.., basis columns b0.. -- into `nst`
+// shared-memory stages (full / empty mbarriers, as many stages as fit: 6 at N = 10,000), and
+// each compute thread consumes its row's xi_b from shared memory in increasing b (the same
+// cmsub chain as k_eim_residual_w, so the same bits).  k_eim_residual_w keeps 32 loads in
+// flight per row thread (5 MB over the device), which holds a step at ~1.3 TB/s from L2.
+constexpr int kEimSb = 32;        // basis columns per stage
+constexpr int kEimMaxRows = 128;  // box inner dimension 2 * rows <= 256 doubles
+constexpr int kEimMaxStages = 8;
+
+struct EimTiles {
+    int rows;     // rows per CTA (a multiple of 4)
+    int nst;      // stages
+    size_t smem;  // dynamic shared memory
+};
+
+static EimTiles eim_tiles(long long N, int k, int num_sms) {
+    EimTiles t;
+    long long r = (N + num_sms - 1) / num_sms;
+    r = (r + 3) / 4 * 4;
+    t.rows = (int)(r < 4 ? 4 : (r > kEimMaxRows ? kEimMaxRows : r));
+    const size_t stage = (size_t)t.rows * kEimSb * 16;
+    const size_t fixed = 2 * kEimMaxStages * sizeof(uint64_t) + sizeof(double2) * (size_t)k;
+    const size_t budget = 220 * 1024;
+    int n = (int)((budget - fixed) / stage);
+    t.nst = n < 2 ? 2 : (n > kEimMaxStages ? kEimMaxStages : n);
+    t.smem = (size_t)t.nst * stage + fixed;
+    return t;
+}
+
+__global__ void __launch_bounds__(kEimMaxRows + 32, 1) k_eim_residual_t(EimArgs a, int l, int rows, int nst,
+                                                                       const __grid_constant__ CUtensorMap tmXi) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const double2 *stage = reinterpret_cast<const double2 *>(sm);       // [nst][kEimSb][rows]
+    const size_t stage_elems = (size_t)kEimSb * rows;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + nst * stage_elems * 16), *empty = full + kEimMaxStages;
+    double2 *s_c = reinterpret_cast<double2 *>(empty + kEimMaxStages);   // c_0 .. c_{l-1}
+    const int tid = threadIdx.x;
+    const int cthreads = (rows + 31) / 32 * 32;   // compute warps; the producer warp follows
+    const long long r0 = (long long)blockIdx.x * rows;
+    const int nt = (l + kEimSb - 1) / kEimSb;
+    if (tid == 0) {
+        for (int i = 0; i < nst; i++) {
+            mbar_init_nofence(&full[i], 1);
+            mbar_init_nofence(&empty[i], cthreads / 32);
+        }
+        fence_mbarrier_init();
+    }
+    for (int b = tid; b < l; b += blockDim.x) s_c[b] = a.c[b];
+    __syncthreads();
+    double2 x = make_double2(0.0, 0.0);
+    bool mine = false;
+    long long i = 0;
+    if (tid >= cthreads) {  // producer warp
+        if (tid == cthreads) {
+            for (int st = 0; st < nt; st++) {
+                const int slot = st % nst;
+                if (st >= nst) mbar_wait(&empty[slot], (uint32_t)((st / nst - 1) & 1));
+                mbar_arrive_expect_tx(&full[slot], (uint32_t)(stage_elems * 16));
+                tma_tile_g2s((void *)(stage + slot * stage_elems), &tmXi, (int)(2 * r0), st * kEimSb, &full[slot]);
+            }
+        }
+    } else {
+        i = r0 + tid;
+        mine = tid < rows && i < a.N;
+        x = mine ? load_q(a.Q, a.ldq_v, a.cplx, l, i) : make_double2(0.0, 0.0);
+        const int col = tid < rows ? tid : 0;
+        for (int st = 0; st < nt; st++) {
+            const int slot = st % nst;
+            mbar_wait(&full[slot], (uint32_t)((st / nst) & 1));
+            const int b0 = st * kEimSb, bend = l - b0 < kEimSb ? l - b0 : kEimSb;
+            const double2 *tile = stage + slot * stage_elems + col;
+            if (bend == kEimSb) {
+#pragma unroll 8
+                for (int bb = 0; bb < kEimSb; bb++) x = cmsub(x, s_c[b0 + bb], tile[bb * rows]);
+            } else {
+                for (int bb = 0; bb < bend; bb++) x = cmsub(x, s_c[b0 + bb], tile[bb * rows]);
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+        }
+    }
+    eim_residual_finish<kEimMaxRows / 32 + 1>(a, l, x, mine, i);
+}
+
 template <int SLOTS>
 static cudaError_t launch_solve_w(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
     // set on every call: the attribute is per device, and a process may drive several
@@ -594,16 +688,37 @@ static cudaError_t launch_solve(const EimArgs &a, int l, const CUtensorMap &tm, 
     return launch_solve_w<32>(a, l, tm, s);
 }
 
-// 2D view of Tt for the solver's tiles: inner dimension 2k doubles (rows a), outer k columns b.
-static cudaError_t make_tt_map(const EimArgs &a, CUtensorMap *tm) {
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult q;
-        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
+    return encode;
+}
+
+// 2D view of Xi for k_eim_residual_t: inner dimension 2N doubles (rows), outer k columns b;
+// rows past N in the last CTA's box are zero-filled.
+static cudaError_t make_xi_map(const EimArgs &a, int rows, CUtensorMap *tm) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * a.N), (cuuint64_t)a.k};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.N * 16};
+    const cuuint32_t box[2] = {(cuuint32_t)(2 * rows), kEimSb};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.Xi, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// 2D view of Tt for the solver's tiles: inner dimension 2k doubles (rows a), outer k columns b.
+static cudaError_t make_tt_map(const EimArgs &a, CUtensorMap *tm) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode) return cudaErrorNotSupported;
     const cuuint64_t dims[2] = {(cuuint64_t)(2 * a.k), (cuuint64_t)a.k};
     const cuuint64_t strides[1] = {(cuuint64_t)a.k * 16};
     const cuuint32_t box[2] = {64, 32};
@@ -627,7 +742,7 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
                     int *status_d, cudaStream_t s) {
     if (k < 1 || k > 1024) return cudaErrorInvalidValue;
     const int blocks = (int)((N + kEimThreads - 1) / kEimThreads < 296 ? (N + kEimThreads - 1) / kEimThreads : 296);
-    const long long nrec = std::max<long long>(blocks, (N + 63) / 64);   // per-block maxloc records
+    const long long nrec = std::max<long long>(blocks, (N + 3) / 4);   // per-block maxloc records (>= 4 rows per block)
     EimArgs a{};
     a.Q = Q;
     a.ldq_v = ldq_v;
@@ -640,7 +755,7 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     if (e == cudaSuccess) e = dmalloc(&a.T, sizeof(double2) * (size_t)k * k);
     if (e == cudaSuccess) e = dmalloc(&a.Tt, sizeof(double2) * (size_t)k * k);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.Tt, 0, sizeof(double2) * (size_t)k * k, s);
-    CUtensorMap tmT;
+    CUtensorMap tmT, tmXi;
     if (e == cudaSuccess) e = make_tt_map(a, &tmT);
     if (e == cudaSuccess) e = dmalloc(&a.c, sizeof(double2) * k);
     if (e == cudaSuccess) e = dmalloc(&a.bm, sizeof(double) * nrec);
@@ -654,6 +769,18 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     const char *ev = getenv("RBG_EIM");
     const bool v1 = ev && !strcmp(ev, "block");
     const int blocks_w = (int)((N + kEimThreadsW - 1) / kEimThreadsW);
+    // RBG_EIM_RESID=w: the residual with per-thread load rings (round 1-2), same bits
+    const char *rv = getenv("RBG_EIM_RESID");
+    const bool resid_w = rv && !strcmp(rv, "w");
+    int dev = 0, sms = 148;
+    if (e == cudaSuccess) cudaGetDevice(&dev);
+    if (e == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const EimTiles tl = eim_tiles(N, k, sms);
+    const int blocks_t = (int)((N + tl.rows - 1) / tl.rows);
+    const size_t t_smem = tl.smem;
+    if (e == cudaSuccess && !v1 && !resid_w) e = make_xi_map(a, tl.rows, &tmXi);
+    if (e == cudaSuccess && !v1 && !resid_w)
+        e = cudaFuncSetAttribute(k_eim_residual_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t_smem);
     for (int l = 0; l < k && e == cudaSuccess; l++) {
         if (l > 0) {
             if (v1) {
@@ -666,7 +793,8 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
         if (e == cudaSuccess) {
             const size_t sh = sizeof(double2) * (size_t)(l > 0 ? l : 1);
             if (v1) k_eim_residual<<<blocks, kEimThreads, sh, s>>>(a, l);
-            else k_eim_residual_w<<<blocks_w, kEimThreadsW, sh, s>>>(a, l);
+            else if (resid_w) k_eim_residual_w<<<blocks_w, kEimThreadsW, sh, s>>>(a, l);
+            else k_eim_residual_t<<<blocks_t, (tl.rows + 31) / 32 * 32 + 32, t_smem, s>>>(a, l, tl.rows, tl.nst, tmXi);
             e = cudaGetLastError();
         }
     }
