@@ -324,6 +324,19 @@ __device__ __forceinline__ double div_rn_pre(double num, double den, double y, b
     return num / den;
 }
 
+// Both components of a complex quotient (n1 + i n2) / den with one range test: when both
+// numerators are in range (and den is) each component is div_rn_pre's fast path, so the two
+// three-FMA chains interleave instead of running one after the other behind their branches;
+// otherwise each component goes through div_rn_pre itself.  Same bits either way.
+__device__ __forceinline__ double2 div2_rn_pre(double n1, double n2, double den, double y, bool den_ok) {
+    const double q01 = n1 * y, q02 = n2 * y;
+    const double q11 = fma(fma(-q01, den, n1), y, q01), q12 = fma(fma(-q02, den, n2), y, q02);
+    const double q21 = fma(fma(-q11, den, n1), y, q11), q22 = fma(fma(-q12, den, n2), y, q12);
+    const double a1 = fabs(n1), a2 = fabs(n2);
+    if (den_ok && a1 >= 0x1p-500 && a1 <= 0x1p500 && a2 >= 0x1p-500 && a2 <= 0x1p500) return make_double2(q21, q22);
+    return make_double2(div_rn_pre(n1, den, y, den_ok), div_rn_pre(n2, den, y, den_ok));
+}
+
 // ---- multi-warp forward substitution (default, round 2) ----------------------------------
 // The serial chain of k_eim_solve_w is A(0) -> B(0,1) -> A(1) -> B(1,2) -> ... (phase A of a
 // block, then the next block's update by it); the other phase-B tiles (sb, s), s > sb + 1, only
@@ -400,6 +413,8 @@ __global__ void __launch_bounds__(1024) k_eim_solve_mw(EimArgs a, int l, const _
         return;
     }
     // main warp (warp 0)
+    __shared__ double s_den[32], s_y[32];
+    __shared__ int s_ok[32];
     double2 v = lane < l ? load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[lane]) : make_double2(0.0, 0.0);
     int n = 0;
     for (int sb = 0; sb < nblk; sb++) {
@@ -409,26 +424,39 @@ __global__ void __launch_bounds__(1024) k_eim_solve_mw(EimArgs a, int l, const _
         const double dd = fma(td.x, td.x, td.y * td.y);
         const double yy = 1.0 / dd;   // RN(1 / den) of this lane's column, off the chain
         const int dok = dd >= 0x1p-500 && dd <= 0x1p500;
+        // the block's per-column constants go to shared memory: broadcast reads off the chain
+        // instead of three more shuffles per column in the MIO queue ahead of the numerators'
+        s_den[lane] = dd;
+        s_y[lane] = yy;
+        s_ok[lane] = dok;
+        __syncwarp();
         int slot = n % kEimMwRing;
         mbar_wait(&full[slot], (uint32_t)((n / kEimMwRing) & 1));
+        // lane predicates as loop-carried bit masks shifted once per column (bit 0: this column),
+        // so the compiler cannot re-derive them from the lane id on the chain
+        unsigned updb = (lane < bl_end) ? ((1u << lane) - 1u) : 0u;   // bit bl set iff bl < lane
+        unsigned meb = 1u << lane;                                      // bit bl set iff bl == lane
+        double2 mycb = make_double2(0.0, 0.0);
 #pragma unroll 1
         for (int bl = 0; bl < bl_end; bl++) {  // phase A: the same quotients as k_eim_solve_w
             // every lane forms c_b itself from the owner's numerators (no divergent branch and
             // no broadcast of the quotients); the tile entry is read before the chain needs it
             const double2 t = ring[slot][bl][lane];
+            const double den = s_den[bl], y = s_y[bl];
+            const bool den_ok = s_ok[bl] != 0;
             const double n1 = __shfl_sync(0xffffffffu, fma(v.x, td.x, v.y * td.y), bl);
             const double n2 = __shfl_sync(0xffffffffu, fma(v.y, td.x, -(v.x * td.y)), bl);
-            const double den = __shfl_sync(0xffffffffu, dd, bl);
-            const double y = __shfl_sync(0xffffffffu, yy, bl);
-            const bool den_ok = __shfl_sync(0xffffffffu, dok, bl) != 0;
-            const double2 cb = make_double2(div_rn_pre(n1, den, y, den_ok), div_rn_pre(n2, den, y, den_ok));
-            if (lane == bl) {
-                a.c[b0 + bl] = cb;
-                s_c[b0 + bl] = cb;
-            }
-            if (lane > bl && lane < bl_end) v = cmsub(v, cb, t);
+            const double2 cb = div2_rn_pre(n1, n2, den, y, den_ok);
+            if (meb & 1u) mycb = cb;   // this lane's coefficient, stored after the loop
+            if (updb & 1u) v = cmsub(v, cb, t);
+            updb >>= 1;
+            meb >>= 1;
         }
-        __syncwarp();
+        if (lane < bl_end) {
+            a.c[b0 + lane] = mycb;
+            s_c[b0 + lane] = mycb;
+        }
+        __syncwarp();   // the coefficients are in place; s_den / s_y / s_ok are rewritten next block
         if (lane == 0) {
             mbar_arrive(&empty[slot]);
             mbar_arrive(&coefbar[sb]);  // release: block sb's coefficients for the helpers
