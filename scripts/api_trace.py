@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Where the wall time of rbg_eim goes: torch.profiler (CUPTI) trace of one ctx.eim() call on a
-k-vector config-2-shaped basis -- GPU kernel time, the gaps between kernels, and the runtime
-API calls on the host (cudaLaunchKernel, cudaFuncSetAttribute, cudaMalloc, ...)."""
+"""Where the wall time of a NEXT-row call goes: torch.profiler (CUPTI) trace of one ctx.eim() /
+ctx.reconstruct() / ctx.gram() call (--call) on a k-vector config-2-shaped basis -- GPU kernel
+time, the gaps between kernels, and the runtime API calls on the host (cudaLaunchKernel,
+cudaMalloc, cudaMemcpy, ...)."""
 import argparse
 import json
 import os
@@ -20,6 +21,7 @@ def main():
     p.add_argument("--cols", type=int, default=20480)
     p.add_argument("--k", type=int, default=300)
     p.add_argument("--out", default="gpurun_out/eim_trace.json")
+    p.add_argument("--call", default="eim", choices=["eim", "reconstruct", "gram"])
     a = p.parse_args()
     N = 10000
     t = inputs.chirp_grid(N)
@@ -29,17 +31,18 @@ def main():
     rbg.gen_chirp(S, t, w, q, chi, psi, spin=True)
     with rbg.Context(S, w, 0.0, a.k) as ctx:
         ctx.run()
-        ctx.eim()
+        call = {"eim": ctx.eim, "reconstruct": lambda: ctx.reconstruct(1e-3), "gram": ctx.gram}[a.call]
+        call()
         torch.cuda.synchronize()
         walls = []
         for _ in range(2):
             t0 = time.perf_counter()
-            ctx.eim()
+            call()
             walls.append(time.perf_counter() - t0)
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
             t0 = time.perf_counter()
-            ctx.eim()
+            call()
             wall = time.perf_counter() - t0
     prof.export_chrome_trace(a.out)
     ev = json.load(open(a.out))["traceEvents"]

@@ -2,8 +2,8 @@
 # EIM residual: TMA-staged tiles (default) vs per-thread load rings (RBG_EIM_RESID=w), parity + A/B.
 timeout 900 python -m pytest tests/test_eim.py tests/test_gpu_canary.py -q -x > gpurun_out/eim_parity.log 2>&1; echo parity rc=$?; tail -1 gpurun_out/eim_parity.log
 for rep in 1 2; do
-  python scripts/eim_trace.py --out /tmp/t.json > gpurun_out/eim_trace_t.$rep.json 2>/dev/null; echo t rc=$?
-  RBG_EIM_RESID=w python scripts/eim_trace.py --out /tmp/w.json > gpurun_out/eim_trace_w.$rep.json 2>/dev/null; echo w rc=$?
+  python scripts/api_trace.py --out /tmp/t.json > gpurun_out/eim_trace_t.$rep.json 2>/dev/null; echo t rc=$?
+  RBG_EIM_RESID=w python scripts/api_trace.py --out /tmp/w.json > gpurun_out/eim_trace_w.$rep.json 2>/dev/null; echo w rc=$?
 done
 for f in gpurun_out/eim_trace_[tw].*.json; do python -c "
 import json,sys; d=json.load(open('$f')); print('$f', 'wall_ms', round(min(d['walls_s'])*1e3,2), 'gpu_busy_ms', round(d['gpu_busy_us']/1e3,2), 'span_ms', round(d['gpu_span_us']/1e3,2))"; done

@@ -10,5 +10,5 @@ python bench.py > gpurun_out/bench_final_b_default.json 2> gpurun_out/bench_fina
 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_final_b_20.json 2> gpurun_out/bench_final_b_20.err; echo bench20 rc=$?
 C1="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu"
 $C1 > gpurun_out/plain1_b.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final_b.csv $C1 > gpurun_out/ncu1_b.log 2>&1; echo ncu1 rc=$?
-python scripts/eim_trace.py --out /tmp/e.json > gpurun_out/eim_trace_final_b.json 2>/dev/null; echo eim rc=$?
+python scripts/api_trace.py --out /tmp/e.json > gpurun_out/eim_trace_final_b.json 2>/dev/null; echo eim rc=$?
 python scripts/bench_next.py > gpurun_out/bench_next_final_b.json 2> gpurun_out/bench_next_final_b.err; echo next rc=$?
