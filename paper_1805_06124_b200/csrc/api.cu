@@ -180,6 +180,7 @@ void free_ctx(rbg_ctx *c) {
     dfree(c->cgs_v);
     dfree(c->w_true);
     dfree(c->cgs_c);
+    c->scratch.release();
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

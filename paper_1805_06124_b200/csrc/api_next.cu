@@ -27,9 +27,9 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
     TRY(upload_block(c, V, M_v, ldv, V_mem, &Vd, &v_owned));
     const long long k = h.k;
     double *Rv = nullptr, *e2 = nullptr, *ed = nullptr;
-    cudaError_t e = dmalloc(&Rv, (size_t)std::max<long long>(k, 1) * M_v * c->se);
-    if (e == cudaSuccess) e = dmalloc(&e2, sizeof(double) * M_v);
-    if (e == cudaSuccess) e = dmalloc(&ed, sizeof(double) * M_v);
+    cudaError_t e = salloc(&c->scratch, kScValR, &Rv, (size_t)std::max<long long>(k, 1) * M_v * c->se);
+    if (e == cudaSuccess) e = salloc(&c->scratch, kScValE2, &e2, sizeof(double) * M_v);
+    if (e == cudaSuccess) e = salloc(&c->scratch, kScValE, &ed, sizeof(double) * M_v);
     rbg_status st = e == cudaSuccess ? coeff_passes(c, Vd, M_v, Rv, M_v, e2, k)
                                      : fail(RBG_ENOMEM, "validation buffers: %s", cudaGetErrorString(e));
     const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -44,9 +44,9 @@ rbg_status rbg_validate(rbg_ctx *c, const void *V, int64_t M_v, int64_t ldv, rbg
     }
     cudaStreamSynchronize(c->stream);
     if (v_owned) dfree(Vd);
-    dfree(Rv);
-    dfree(e2);
-    dfree(ed);
+    sfree(&c->scratch, Rv);
+    sfree(&c->scratch, e2);
+    sfree(&c->scratch, ed);
     return st;
 }
 
@@ -260,16 +260,16 @@ rbg_status gram_device(rbg_ctx *c, int k, int kp, const double2 *G0, double2 *G)
     }
     int4 *items_d = nullptr;
     double2 *P = nullptr;
-    cudaError_t e = dmalloc(&items_d, sizeof(int4) * items.size());
-    if (e == cudaSuccess) e = dmalloc(&P, sizeof(double2) * (size_t)nchunks * k * k);
+    cudaError_t e = salloc(&c->scratch, kScGramItems, &items_d, sizeof(int4) * items.size());
+    if (e == cudaSuccess) e = salloc(&c->scratch, kScGramP, &P, sizeof(double2) * (size_t)nchunks * k * k);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(items_d, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess)
         e = launch_gram(c->R, c->ldr, k, c->M, c->cplx, P, kGramChunk, items_d, (int)items.size(), c->stream);
     if (e == cudaSuccess) e = launch_gram_reduce(P, nchunks, k, kp, G0, G, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    dfree(items_d);
-    dfree(P);
+    sfree(&c->scratch, items_d);
+    sfree(&c->scratch, P);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "gram: %s", cudaGetErrorString(e));
     return RBG_OK;
 }
@@ -287,14 +287,14 @@ rbg_status rbg_gram(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     if (k == 0) return RBG_OK;
     const int kp = k + (k & 1);
     double2 *Gd = nullptr;
-    CU(dmalloc(&Gd, sizeof(double2) * (size_t)kp * kp));
+    CU(salloc(&c->scratch, kScRecG, &Gd, sizeof(double2) * (size_t)kp * kp));
     rbg_status st = gram_device(c, k, kp, nullptr, Gd);
     if (st == RBG_OK) {
         cudaError_t e = cudaMemcpy2D(G, (size_t)ldg * 16, Gd, (size_t)kp * 16, (size_t)k * 16, k,
                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "gram copy: %s", cudaGetErrorString(e));
     }
-    dfree(Gd);
+    sfree(&c->scratch, Gd);
     return st;
 }
 
@@ -311,8 +311,8 @@ rbg_status rbg_gram_fold(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
     const cudaMemcpyKind in = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const cudaMemcpyKind out = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     double2 *G0 = nullptr, *G1 = nullptr;
-    cudaError_t e = dmalloc(&G0, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = dmalloc(&G1, sizeof(double2) * (size_t)kp * kp);
+    cudaError_t e = salloc(&c->scratch, kScRecG, &G0, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = salloc(&c->scratch, kScRecV, &G1, sizeof(double2) * (size_t)kp * kp);
     if (e == cudaSuccess) e = cudaMemsetAsync(G0, 0, sizeof(double2) * (size_t)kp * kp, c->stream);
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(G0, (size_t)kp * 16, G, (size_t)ldg * 16, (size_t)k * 16, k, in, c->stream);
     rbg_status st = e == cudaSuccess ? gram_device(c, k, kp, G0, G1) : fail(RBG_ECUDA, "gram_fold: %s", cudaGetErrorString(e));
@@ -320,8 +320,8 @@ rbg_status rbg_gram_fold(rbg_ctx *c, void *G, int64_t ldg, int on_device) {
         e = cudaMemcpy2D(G, (size_t)ldg * 16, G1, (size_t)kp * 16, (size_t)k * 16, k, out);
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "gram_fold copy: %s", cudaGetErrorString(e));
     }
-    dfree(G0);
-    dfree(G1);
+    sfree(&c->scratch, G0);
+    sfree(&c->scratch, G1);
     return st;
 }
 
@@ -351,14 +351,15 @@ rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_d
     unsigned long long *flags = nullptr;
     int *sweeps = nullptr, *order = nullptr, *krd = nullptr;
     double *sig = nullptr;
-    cudaError_t e = dmalloc(&G, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = dmalloc(&V, sizeof(double2) * (size_t)kp * kp);
-    if (e == cudaSuccess) e = dmalloc(&rots, block ? bjacobi_scratch_bytes(kp) : jacobi_scratch_bytes(kp));
-    if (e == cudaSuccess) e = dmalloc(&flags, 3 * sizeof(unsigned long long));  // ratios + barrier
-    if (e == cudaSuccess) e = dmalloc(&sweeps, sizeof(int));
-    if (e == cudaSuccess) e = dmalloc(&order, sizeof(int) * kp);
-    if (e == cudaSuccess) e = dmalloc(&krd, sizeof(int));
-    if (e == cudaSuccess) e = dmalloc(&sig, sizeof(double) * kp);
+    ScratchPool *sp = &c->scratch;
+    cudaError_t e = salloc(sp, kScRecG, &G, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = salloc(sp, kScRecV, &V, sizeof(double2) * (size_t)kp * kp);
+    if (e == cudaSuccess) e = salloc(sp, kScRecRots, &rots, block ? bjacobi_scratch_bytes(kp) : jacobi_scratch_bytes(kp));
+    if (e == cudaSuccess) e = salloc(sp, kScRecFlags, &flags, 3 * sizeof(unsigned long long));  // ratios + barrier
+    if (e == cudaSuccess) e = salloc(sp, kScRecSweeps, &sweeps, sizeof(int));
+    if (e == cudaSuccess) e = salloc(sp, kScRecOrder, &order, sizeof(int) * kp);
+    if (e == cudaSuccess) e = salloc(sp, kScRecKr, &krd, sizeof(int));
+    if (e == cudaSuccess) e = salloc(sp, kScRecSig, &sig, sizeof(double) * kp);
     rbg_status st = e == cudaSuccess ? RBG_OK : fail(RBG_ENOMEM, "reconstruct buffers: %s", cudaGetErrorString(e));
     if (st == RBG_OK && !Gin) st = gram_device(c, k, kp, nullptr, G);
     if (st == RBG_OK && Gin) {
@@ -419,7 +420,7 @@ rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_d
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && sigma) e = cudaMemcpy(sigma, sig, sizeof(double) * k, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && X && kr > 0) {
-            e = dmalloc(&Xd, (size_t)kr * c->nvec * 16);
+            e = salloc(sp, kScRecX, &Xd, (size_t)kr * c->nvec * 16);
             if (e == cudaSuccess)
                 e = launch_recon_x(c->Q, c->ldq_v, c->nvec, k, V, kp, order, kr, Xd, c->nvec, c->cplx, c->stream);
             if (e == cudaSuccess)
@@ -430,15 +431,9 @@ rbg_status reconstruct_impl(rbg_ctx *c, const void *Gin, int64_t ldg, int g_on_d
         if (e != cudaSuccess) st = fail(RBG_ECUDA, "reconstruct: %s", cudaGetErrorString(e));
         else if (kr_out) *kr_out = kr;
     }
-    dfree(G);
-    dfree(V);
-    dfree(Xd);
-    dfree(rots);
-    dfree(flags);
-    dfree(sweeps);
-    dfree(order);
-    dfree(krd);
-    dfree(sig);
+    for (void *q : {(void *)G, (void *)V, (void *)Xd, (void *)rots, (void *)flags, (void *)sweeps, (void *)order,
+                    (void *)krd, (void *)sig})
+        sfree(sp, q);   // no-ops for what the context's pool keeps
     return st;
 }
 
@@ -467,17 +462,17 @@ rbg_status rbg_eim(rbg_ctx *c, int64_t *nodes, void *B, int64_t ldb, int on_devi
     long long *nd = nullptr;
     double2 *Bd = nullptr;
     int *status = nullptr, hs = 0;
-    cudaError_t e = dmalloc(&nd, sizeof(long long) * k);
-    if (e == cudaSuccess) e = dmalloc(&Bd, sizeof(double2) * (size_t)k * k);
-    if (e == cudaSuccess) e = dmalloc(&status, sizeof(int));
-    if (e == cudaSuccess) e = run_eim(c->Q, c->ldq_v, c->N, c->cplx, k, nd, Bd, status, c->stream);
+    cudaError_t e = salloc(&c->scratch, kScEimNodes, &nd, sizeof(long long) * k);
+    if (e == cudaSuccess) e = salloc(&c->scratch, kScEimB, &Bd, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = salloc(&c->scratch, kScEimStatus, &status, sizeof(int));
+    if (e == cudaSuccess) e = run_eim(c->Q, c->ldq_v, c->N, c->cplx, k, nd, Bd, status, c->stream, &c->scratch);
     if (e == cudaSuccess) e = cudaMemcpy(&hs, status, sizeof(int), cudaMemcpyDeviceToHost);
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (e == cudaSuccess && nodes) e = cudaMemcpy(nodes, nd, sizeof(long long) * k, kind);
     if (e == cudaSuccess && B) e = cudaMemcpy2D(B, (size_t)ldb * 16, Bd, (size_t)k * 16, (size_t)k * 16, k, kind);
-    dfree(nd);
-    dfree(Bd);
-    dfree(status);
+    sfree(&c->scratch, nd);
+    sfree(&c->scratch, Bd);
+    sfree(&c->scratch, status);
     if (e != cudaSuccess) return fail(RBG_ECUDA, "eim: %s", cudaGetErrorString(e));
     if (hs) return fail(RBG_ESTATE, "EIM residual vanished: the basis is numerically degenerate");
     return RBG_OK;

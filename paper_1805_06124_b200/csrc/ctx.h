@@ -122,6 +122,7 @@ struct rbg_ctx {
     unsigned long long epoch = 0;
     long long *imgs_trace = nullptr;  // RBG_DEBUG_IMGS=<iteration>: phase clocks of that IMGS
     long long trace_iter = -1;
+    rbg::ScratchPool scratch;         // work buffers of the NEXT-row calls, kept between calls
 };
 
 namespace rbg_api {

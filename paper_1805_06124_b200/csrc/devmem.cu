@@ -1,3 +1,4 @@
+#include <cstdlib>
 // devmem.cu -- every device allocation of the library, with optional canaries.
 //
 // compute-sanitizer is closed on this GPU pool, so out-of-bounds WRITES are caught the cheap
@@ -98,6 +99,38 @@ long long debug_canary_violations(std::string *msg) {
         if (!intact(kv.first, kv.second)) note(r, kv.first, kv.second);
     if (msg) *msg = r.first;
     return r.violations;
+}
+
+bool scratch_disabled() {
+    static const bool off = getenv("RBG_NO_SCRATCH") != nullptr;
+    return off;
+}
+
+cudaError_t ScratchPool::get(int slot, size_t n, void **out) {
+    if (slot < 0 || slot >= kSlots) return cudaErrorInvalidValue;
+    if (n == 0) n = 1;
+    if (bytes[slot] < n) {
+        dfree(p[slot]);
+        p[slot] = nullptr;
+        bytes[slot] = 0;
+        const cudaError_t e = dmalloc(&p[slot], n);
+        if (e != cudaSuccess) {
+            p[slot] = nullptr;
+            *out = nullptr;
+            return e;
+        }
+        bytes[slot] = n;
+    }
+    *out = p[slot];
+    return cudaSuccess;
+}
+
+void ScratchPool::release() {
+    for (int i = 0; i < kSlots; i++) {
+        dfree(p[i]);
+        p[i] = nullptr;
+        bytes[i] = 0;
+    }
 }
 
 }  // namespace rbg

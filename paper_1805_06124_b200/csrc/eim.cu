@@ -346,13 +346,14 @@ __device__ __forceinline__ double2 div2_rn_pre(double n1, double n2, double den,
 // mbarrier per block), reading T from L2 with 8 loads in flight, then hands its rows to the main
 // warp (an mbarrier per block).  Every row still receives its updates in increasing b, one
 // cmsub each, so the bits are those of the unblocked substitution.  Threads 32 (nblk + 1) for
-// nblk = ceil(l / 32) <= 31 row blocks.
-constexpr int kEimMwMaxBlk = 31;
+// nblk = ceil(l / 32) <= 15 row blocks (512 threads, so 128 registers per thread and no spills
+// on the chain; longer solves, l > 480, take the single-warp solver -- same bits).
+constexpr int kEimMwMaxBlk = 15;
 constexpr int kEimMwRing = 4;
 constexpr size_t kEimMwSmem = kEimMwRing * kEimTile + 2 * kEimMwRing * sizeof(uint64_t) +
                               2 * 32 * sizeof(uint64_t) + 1024 * sizeof(double2) + 32 * 32 * sizeof(double2);
 
-__global__ void __launch_bounds__(1024) k_eim_solve_mw(EimArgs a, int l, const __grid_constant__ CUtensorMap tmT) {
+__global__ void __launch_bounds__(512) k_eim_solve_mw(EimArgs a, int l, const __grid_constant__ CUtensorMap tmT) {
     extern __shared__ __align__(1024) unsigned char sm[];
     const double2(*ring)[32][32] = reinterpret_cast<const double2(*)[32][32]>(sm);
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + kEimMwRing * kEimTile), *empty = full + kEimMwRing;
@@ -416,11 +417,13 @@ __global__ void __launch_bounds__(1024) k_eim_solve_mw(EimArgs a, int l, const _
     __shared__ double s_den[32], s_y[32];
     __shared__ int s_ok[32];
     double2 v = lane < l ? load_q(a.Q, a.ldq_v, a.cplx, l, a.nodes[lane]) : make_double2(0.0, 0.0);
+    double2 td = lane < l ? a.Tt[(long long)lane * a.k + lane] : make_double2(1.0, 0.0);   // T[r][r], r = lane
     int n = 0;
     for (int sb = 0; sb < nblk; sb++) {
         const int b0 = sb * 32, bl_end = l - b0 < 32 ? l - b0 : 32;
         const int r = b0 + lane;
-        const double2 td = r < l ? a.Tt[(long long)r * a.k + r] : make_double2(1.0, 0.0);
+        // the next block's diagonal, loaded a block ahead (its latency off the chain)
+        const double2 td_next = r + 32 < l ? a.Tt[(long long)(r + 32) * a.k + r + 32] : make_double2(1.0, 0.0);
         const double dd = fma(td.x, td.x, td.y * td.y);
         const double yy = 1.0 / dd;   // RN(1 / den) of this lane's column, off the chain
         const int dok = dd >= 0x1p-500 && dd <= 0x1p500;
@@ -479,6 +482,7 @@ __global__ void __launch_bounds__(1024) k_eim_solve_mw(EimArgs a, int l, const _
             n++;
             v = x;
         }
+        td = td_next;
     }
 }
 
@@ -767,7 +771,7 @@ __global__ void k_eim_nodes_matrix(EimArgs a, double2 *B) {
 }
 
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
-                    int *status_d, cudaStream_t s) {
+                    int *status_d, cudaStream_t s, ScratchPool *pool) {
     if (k < 1 || k > 1024) return cudaErrorInvalidValue;
     const int blocks = (int)((N + kEimThreads - 1) / kEimThreads < 296 ? (N + kEimThreads - 1) / kEimThreads : 296);
     const long long nrec = std::max<long long>(blocks, (N + 3) / 4);   // per-block maxloc records (>= 4 rows per block)
@@ -779,16 +783,16 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
     a.k = k;
     a.nodes = nodes_d;
     a.status = status_d;
-    cudaError_t e = dmalloc(&a.Xi, sizeof(double2) * (size_t)k * N);
-    if (e == cudaSuccess) e = dmalloc(&a.T, sizeof(double2) * (size_t)k * k);
-    if (e == cudaSuccess) e = dmalloc(&a.Tt, sizeof(double2) * (size_t)k * k);
+    cudaError_t e = salloc(pool, kScEimXi, &a.Xi, sizeof(double2) * (size_t)k * N);
+    if (e == cudaSuccess) e = salloc(pool, kScEimT, &a.T, sizeof(double2) * (size_t)k * k);
+    if (e == cudaSuccess) e = salloc(pool, kScEimTt, &a.Tt, sizeof(double2) * (size_t)k * k);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.Tt, 0, sizeof(double2) * (size_t)k * k, s);
     CUtensorMap tmT, tmXi;
     if (e == cudaSuccess) e = make_tt_map(a, &tmT);
-    if (e == cudaSuccess) e = dmalloc(&a.c, sizeof(double2) * k);
-    if (e == cudaSuccess) e = dmalloc(&a.bm, sizeof(double) * nrec);
-    if (e == cudaSuccess) e = dmalloc(&a.bj, sizeof(long long) * nrec);
-    if (e == cudaSuccess) e = dmalloc(&a.ticket, sizeof(unsigned));
+    if (e == cudaSuccess) e = salloc(pool, kScEimC, &a.c, sizeof(double2) * k);
+    if (e == cudaSuccess) e = salloc(pool, kScEimBm, &a.bm, sizeof(double) * nrec);
+    if (e == cudaSuccess) e = salloc(pool, kScEimBj, &a.bj, sizeof(long long) * nrec);
+    if (e == cudaSuccess) e = salloc(pool, kScEimTicket, &a.ticket, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(status_d, 0, sizeof(int), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.c, 0, sizeof(double2) * k, s);
@@ -831,13 +835,13 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    dfree(a.Xi);
-    dfree(a.T);
-    dfree(a.Tt);
-    dfree(a.c);
-    dfree(a.bm);
-    dfree(a.bj);
-    dfree(a.ticket);
+    sfree(pool, a.Xi);
+    sfree(pool, a.T);
+    sfree(pool, a.Tt);
+    sfree(pool, a.c);
+    sfree(pool, a.bm);
+    sfree(pool, a.bj);
+    sfree(pool, a.ticket);
     return e;
 }
 

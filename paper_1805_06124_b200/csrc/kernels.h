@@ -230,13 +230,52 @@ bool coeff_block_enabled();
 cudaError_t launch_coeff_block(const double2 *V, long long ldv, long long M, const double2 *WQ, long long ldq_v,
                                long long k, long long nvec, long long N, bool cplx, double *C, long long ldc,
                                double *r2, cudaStream_t s);
+struct ScratchPool;
 cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, int k, long long *nodes_d, double2 *B_d,
-                    int *status_d, cudaStream_t s);
+                    int *status_d, cudaStream_t s, ScratchPool *pool = nullptr);
 
 // Device allocations of the library (devmem.cu): cudaMalloc / cudaFree, with a checked
 // 256-byte canary tail per buffer while canaries are on (rbg_debug_set_canary).
 cudaError_t dmalloc(void **p, size_t bytes);
 cudaError_t dfree(void *p);
+
+// Reusable device work buffers of one context (devmem.cu): slot i is (re)allocated through
+// dmalloc only when a call needs more than it holds, and freed with the context -- the
+// NEXT-row calls (Gram, reconstruction, EIM) would otherwise cudaMalloc / cudaFree their
+// buffers on every call (~2 ms of host time per call at k = 300).  Contents are not kept
+// between calls; every user initialises what it reads, as with a fresh allocation.
+struct ScratchPool {
+    static constexpr int kSlots = 24;
+    static constexpr size_t kMaxKeep = size_t(1) << 30;   // larger requests are not retained
+    void *p[kSlots] = {};
+    size_t bytes[kSlots] = {};
+    cudaError_t get(int slot, size_t n, void **out);
+    bool owns(const void *q) const {
+        for (int i = 0; i < kSlots; i++)
+            if (q && p[i] == q) return true;
+        return false;
+    }
+    void release();
+};
+enum ScratchSlot {
+    kScGramItems = 0, kScGramP, kScRecG, kScRecV, kScRecRots, kScRecFlags, kScRecSweeps, kScRecOrder,
+    kScRecKr, kScRecSig, kScRecX, kScEimNodes, kScEimB, kScEimStatus, kScEimXi, kScEimT, kScEimTt,
+    kScEimC, kScEimBm, kScEimBj, kScEimTicket, kScValR, kScValE2, kScValE
+};
+bool scratch_disabled();   // RBG_NO_SCRATCH: every work buffer from dmalloc, freed per call (A/B)
+// The pool's slot, or a fresh dmalloc without a pool or above kMaxKeep; every salloc is paired
+// with an sfree, which frees only what the pool does not hold.
+template <class T>
+cudaError_t salloc(ScratchPool *pool, int slot, T **p, size_t bytes) {
+    void *q = nullptr;
+    cudaError_t e = (pool && bytes <= ScratchPool::kMaxKeep && !scratch_disabled()) ? pool->get(slot, bytes, &q)
+                                                                                     : dmalloc(&q, bytes);
+    *p = static_cast<T *>(q);
+    return e;
+}
+inline void sfree(ScratchPool *pool, void *p) {
+    if (!pool || !pool->owns(p)) dfree(p);
+}
 template <class T>
 inline cudaError_t dmalloc(T **p, size_t bytes) {
     return dmalloc(reinterpret_cast<void **>(p), bytes);

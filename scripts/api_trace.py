@@ -21,7 +21,8 @@ def main():
     p.add_argument("--cols", type=int, default=20480)
     p.add_argument("--k", type=int, default=300)
     p.add_argument("--out", default="gpurun_out/eim_trace.json")
-    p.add_argument("--call", default="eim", choices=["eim", "reconstruct", "gram"])
+    p.add_argument("--call", default="eim", choices=["eim", "reconstruct", "gram", "validate"])
+    p.add_argument("--val-cols", type=int, default=40960)
     a = p.parse_args()
     N = 10000
     t = inputs.chirp_grid(N)
@@ -31,7 +32,13 @@ def main():
     rbg.gen_chirp(S, t, w, q, chi, psi, spin=True)
     with rbg.Context(S, w, 0.0, a.k) as ctx:
         ctx.run()
-        call = {"eim": ctx.eim, "reconstruct": lambda: ctx.reconstruct(1e-3), "gram": ctx.gram}[a.call]
+        V = None
+        if a.call == "validate":
+            qv, cv, pv = inputs.chirp_params(a.val_cols, 12, spin=True)
+            V = torch.empty((a.val_cols, N), dtype=torch.complex128, device="cuda")
+            rbg.gen_chirp(V, t, w, qv, cv, pv, spin=True)
+        call = {"eim": ctx.eim, "reconstruct": lambda: ctx.reconstruct(1e-3), "gram": ctx.gram,
+                "validate": lambda: ctx.validate(V)}[a.call]
         call()
         torch.cuda.synchronize()
         walls = []
