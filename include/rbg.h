@@ -25,7 +25,9 @@
  *    S is N x M with column j at S + j*ld elements; ld >= N.
  *  - Ownership: the library owns the context and every buffer it allocates; outputs are
  *    copied into caller-owned buffers.  A borrowed device S (rbg_desc.borrow = 1) must
- *    stay alive and unmodified until rbg_destroy.
+ *    stay alive and unmodified until rbg_destroy.  The work buffers of rbg_validate,
+ *    rbg_gram(_fold), rbg_reconstruct(_gram) and rbg_eim (up to 1 GB each) stay allocated in
+ *    the context between calls and are released by rbg_destroy; a context is not thread-safe.
  *  - All GPU work is enqueued on one CUDA stream (rbg_desc.stream, or a stream the library
  *    creates).  Getters synchronise that stream.
  */
