@@ -374,6 +374,8 @@ __global__ void __launch_bounds__(512) k_eim_solve_mw(EimArgs a, int l, const __
         }
         fence_mbarrier_init();
     }
+    grid_dep_wait();     // programmatic dependent launch: T, the nodes and Q are the residual's
+    grid_dep_launch();
     __syncthreads();
     if (warp == 1) {  // producer: the main warp's tiles (sb, sb), (sb, sb + 1) in its order
         if (lane == 0) {
@@ -486,11 +488,36 @@ __global__ void __launch_bounds__(512) k_eim_solve_mw(EimArgs a, int l, const __
     }
 }
 
+// The EIM steps' kernels go out as programmatic dependents of their predecessor (each calls
+// grid_dep_wait before it reads anything): the launch latency between the ~600 short kernels
+// of an EIM run overlaps the predecessor's tail.  RBG_NO_PDL turns it off (same bits).
+static bool eim_pdl() {
+    static const bool off = getenv("RBG_NO_PDL") != nullptr;
+    return !off;
+}
+
+template <typename... Args>
+static cudaError_t launch_dep(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = eim_pdl() ? 1 : 0;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kern, args...);
+}
+
 static cudaError_t launch_solve_mw(const EimArgs &a, int l, const CUtensorMap &tm, cudaStream_t s) {
     const int nblk = (l + 31) / 32;
     cudaError_t e = cudaFuncSetAttribute(k_eim_solve_mw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEimMwSmem);
     if (e != cudaSuccess) return e;
-    k_eim_solve_mw<<<1, 32 * (nblk > 2 ? nblk : 2), kEimMwSmem, s>>>(a, l, tm);
+    e = launch_dep(k_eim_solve_mw, dim3(1), dim3(32 * (nblk > 2 ? nblk : 2)), kEimMwSmem, s, a, l, tm);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -650,6 +677,10 @@ __global__ void __launch_bounds__(kEimMaxRows + 32, 1) k_eim_residual_t(EimArgs 
         }
         fence_mbarrier_init();
     }
+    // programmatic dependent launch (run_eim): everything below reads the solve's and the
+    // previous steps' outputs; the next solve may be launched now (it waits the same way)
+    grid_dep_wait();
+    grid_dep_launch();
     for (int b = tid; b < l; b += blockDim.x) s_c[b] = a.c[b];
     __syncthreads();
     double2 x = make_double2(0.0, 0.0);
@@ -826,8 +857,9 @@ cudaError_t run_eim(const double2 *Q, long long ldq_v, long long N, bool cplx, i
             const size_t sh = sizeof(double2) * (size_t)(l > 0 ? l : 1);
             if (v1) k_eim_residual<<<blocks, kEimThreads, sh, s>>>(a, l);
             else if (resid_w) k_eim_residual_w<<<blocks_w, kEimThreadsW, sh, s>>>(a, l);
-            else k_eim_residual_t<<<blocks_t, (tl.rows + 31) / 32 * 32 + 32, t_smem, s>>>(a, l, tl.rows, tl.nst, tmXi);
-            e = cudaGetLastError();
+            else e = launch_dep(k_eim_residual_t, dim3(blocks_t), dim3((tl.rows + 31) / 32 * 32 + 32), t_smem, s, a, l,
+                                tl.rows, tl.nst, tmXi);
+            if (e == cudaSuccess) e = cudaGetLastError();
         }
     }
     if (e == cudaSuccess) {
