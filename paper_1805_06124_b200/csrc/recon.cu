@@ -435,7 +435,8 @@ __device__ __forceinline__ Rot rot_params(double a, double b, double2 c, int p, 
 
 __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, int kp, double2 *Us,
                                                  unsigned long long *flags, int *sweeps_out,
-                                                 unsigned long long *trace) {
+                                                 unsigned long long *trace, int merged) {
+    extern __shared__ double2 bj_dyn[];   // merged phase: V, U_p and T tiles (3 x 32 x 33)
     __shared__ double2 A[kJL][kJL + 1];   // A[row][col]
     __shared__ double2 U[kJL][kJL + 1];
     __shared__ Rot srot[kJL / 2];
@@ -537,6 +538,66 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
             }
             grid_barrier(bar, bar + 1, nblocks);
             if (tr) trace[r * 4 + 1] = globaltimer_ns();
+            if (merged) {
+                // ---- P2+P3 merged: every 32 x 32 tile (rows of pair p, columns of pair q) of the
+                // two-sided update depends only on its own old entries and two local rotations,
+                // G_pq <- U_p^H (G_pq U_q) and V_pq <- V_pq U_q, so one grid phase and one barrier
+                // replace the column pass, its barrier and the row pass (the products associate
+                // differently: tolerance parity, as the rest of the eigen-step)
+                double2(*Vt)[kJL + 1] = reinterpret_cast<double2(*)[kJL + 1]>(bj_dyn);
+                double2(*Up)[kJL + 1] = Vt + kJL;
+                double2(*Tt)[kJL + 1] = Up + kJL;
+                const int ta = tid >> 5, tb = tid & 31;   // output element (ta, tb) of the tile
+                const int ea = tid & 31, eb = tid >> 5;   // staging element (ea, eb): rows contiguous
+                for (int t = blockIdx.x; t < npairs * npairs; t += gridDim.x) {
+                    const int p = t / npairs, q = t % npairs;
+                    int I, J, K, L;
+                    round_pair(r, p, nb, I, J);
+                    round_pair(r, q, nb, K, L);
+                    // coalesced staging: consecutive threads take consecutive rows of a column
+                    const long long sa = blk_idx(I, J, ea), sb = blk_idx(K, L, eb);
+                    A[ea][eb] = G[sa + sb * kp];
+                    Vt[ea][eb] = V[sa + sb * kp];
+                    U[ea][eb] = Us[(size_t)q * kJL * kJL + tid];      // column-major: U_q[ea][eb]
+                    Up[ea][eb] = Us[(size_t)p * kJL * kJL + tid];     // U_p[ea][eb]
+                    __syncthreads();
+                    double2 tg = make_double2(0.0, 0.0), tv = make_double2(0.0, 0.0);
+#pragma unroll 8
+                    for (int m = 0; m < kJL; m++) {   // (G U_q)[ta][tb], (V U_q)[ta][tb]
+                        const double2 uu = U[m][tb], g = A[ta][m], v = Vt[ta][m];
+                        tg.x = fma(g.x, uu.x, tg.x);
+                        tg.x = fma(-g.y, uu.y, tg.x);
+                        tg.y = fma(g.x, uu.y, tg.y);
+                        tg.y = fma(g.y, uu.x, tg.y);
+                        tv.x = fma(v.x, uu.x, tv.x);
+                        tv.x = fma(-v.y, uu.y, tv.x);
+                        tv.y = fma(v.x, uu.y, tv.y);
+                        tv.y = fma(v.y, uu.x, tv.y);
+                    }
+                    __syncthreads();   // A and Vt fully read
+                    Tt[ta][tb] = tg;
+                    Vt[ta][tb] = tv;
+                    __syncthreads();
+                    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+                    for (int m = 0; m < kJL; m++) {   // (U_p^H T)[ta][tb] = sum_m conj(U_p[m][ta]) T[m][tb]
+                        const double2 uu = Up[m][ta], y = Tt[m][tb];
+                        acc.x = fma(uu.x, y.x, acc.x);
+                        acc.x = fma(uu.y, y.y, acc.x);
+                        acc.y = fma(uu.x, y.y, acc.y);
+                        acc.y = fma(-uu.y, y.x, acc.y);
+                    }
+                    if (blk_idx(I, J, ta) == blk_idx(K, L, tb)) acc.y = 0.0;  // Hermitian: real diagonal
+                    A[ta][tb] = acc;
+                    __syncthreads();
+                    G[sa + sb * kp] = A[ea][eb];   // coalesced write-back
+                    V[sa + sb * kp] = Vt[ea][eb];
+                    __syncthreads();   // the tile arrays are refilled for the next tile
+                }
+                grid_barrier(bar, bar + 1, nblocks);
+                if (tr) trace[r * 4 + 2] = trace[r * 4 + 3] = globaltimer_ns();
+                continue;
+            }
             // ---- P2: columns: M[row, I u J] <- M[row, I u J] U.  The grid is cut into npairs
             // groups of CTAs, each group owns one block pair; a CTA stages that pair's U in
             // shared memory (conflict-free U[m][lane] reads) and its warps take rows.
@@ -631,8 +692,20 @@ cudaError_t launch_bjacobi(double2 *G, double2 *V, int kp, double2 *Us, unsigned
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     int grid = num_sms;
-    void *args[] = {&G, &V, &kp, &Us, &flags, &sweeps, &trace};
-    return cudaLaunchCooperativeKernel((void *)k_bjacobi, grid, kBjThreads, args, 0, s);
+    // RBG_JACOBI_SPLIT=1: the separate column and row passes (two barriers) instead of the
+    // merged tile update (one)
+    static const bool split = getenv("RBG_JACOBI_SPLIT") != nullptr;
+    int merged = split ? 0 : 1;
+    const size_t dyn = merged ? (size_t)3 * kJL * (kJL + 1) * sizeof(double2) : 0;
+    if (dyn) {
+        e = cudaFuncSetAttribute(k_bjacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bjacobi, kBjThreads, dyn);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    }
+    void *args[] = {&G, &V, &kp, &Us, &flags, &sweeps, &trace, &merged};
+    return cudaLaunchCooperativeKernel((void *)k_bjacobi, grid, kBjThreads, args, dyn, s);
 }
 
 // X(:, r) = Q V(:, order[r]) for r < kr: X is N_v x kr vectors (column stride ldx_v), Q is
