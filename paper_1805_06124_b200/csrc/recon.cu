@@ -549,50 +549,90 @@ __global__ void __launch_bounds__(kBjThreads) k_bjacobi(double2 *G, double2 *V, 
                 double2(*Tt)[kJL + 1] = Up + kJL;
                 const int ta = tid >> 5, tb = tid & 31;   // output element (ta, tb) of the tile
                 const int ea = tid & 31, eb = tid >> 5;   // staging element (ea, eb): rows contiguous
-                for (int t = blockIdx.x; t < npairs * npairs; t += gridDim.x) {
-                    const int p = t / npairs, q = t % npairs;
+                // work items: the nG tiles p <= q of the Hermitian G (two products each; the (q, p)
+                // tile is written as the conjugate transpose, so G stays exactly Hermitian) and
+                // the nV tiles of V (one product each).  With more CTAs than G tiles, CTA b < nG
+                // takes G tile b and the others share the V tiles, so no CTA does more than two
+                // products (three when every CTA did G_pq and V_pq of one tile)
+                const int nG = npairs * (npairs + 1) / 2, nV = npairs * npairs;
+                const int G_ctas = (int)gridDim.x > nG ? nG : 0;   // 0: one grid-stride list
+                auto tile_pq = [&](int g, int &p, int &q) {          // g-th pair p <= q, row-major
+                    p = 0;
+                    while (g >= npairs - p) {
+                        g -= npairs - p;
+                        p++;
+                    }
+                    q = p + g;
+                };
+                const int first = G_ctas ? ((int)blockIdx.x < nG ? (int)blockIdx.x : nG + (int)blockIdx.x - nG)
+                                         : (int)blockIdx.x;
+                const int stride = G_ctas ? ((int)blockIdx.x < nG ? nG + nV : (int)gridDim.x - nG) : (int)gridDim.x;
+                for (int t = first; t < nG + nV; t += stride) {
+                    const bool gtile = t < nG;
+                    int p, q;
+                    if (gtile) tile_pq(t, p, q);
+                    else {
+                        p = (t - nG) / npairs;
+                        q = (t - nG) % npairs;
+                    }
                     int I, J, K, L;
                     round_pair(r, p, nb, I, J);
                     round_pair(r, q, nb, K, L);
                     // coalesced staging: consecutive threads take consecutive rows of a column
                     const long long sa = blk_idx(I, J, ea), sb = blk_idx(K, L, eb);
-                    A[ea][eb] = G[sa + sb * kp];
-                    Vt[ea][eb] = V[sa + sb * kp];
-                    U[ea][eb] = Us[(size_t)q * kJL * kJL + tid];      // column-major: U_q[ea][eb]
-                    Up[ea][eb] = Us[(size_t)p * kJL * kJL + tid];     // U_p[ea][eb]
-                    __syncthreads();
-                    double2 tg = make_double2(0.0, 0.0), tv = make_double2(0.0, 0.0);
-#pragma unroll 8
-                    for (int m = 0; m < kJL; m++) {   // (G U_q)[ta][tb], (V U_q)[ta][tb]
-                        const double2 uu = U[m][tb], g = A[ta][m], v = Vt[ta][m];
-                        tg.x = fma(g.x, uu.x, tg.x);
-                        tg.x = fma(-g.y, uu.y, tg.x);
-                        tg.y = fma(g.x, uu.y, tg.y);
-                        tg.y = fma(g.y, uu.x, tg.y);
-                        tv.x = fma(v.x, uu.x, tv.x);
-                        tv.x = fma(-v.y, uu.y, tv.x);
-                        tv.y = fma(v.x, uu.y, tv.y);
-                        tv.y = fma(v.y, uu.x, tv.y);
+                    if (gtile) {
+                        A[ea][eb] = G[sa + sb * kp];
+                        Up[ea][eb] = Us[(size_t)p * kJL * kJL + tid];     // U_p[ea][eb] (column-major)
+                    } else {
+                        Vt[ea][eb] = V[sa + sb * kp];
                     }
-                    __syncthreads();   // A and Vt fully read
-                    Tt[ta][tb] = tg;
-                    Vt[ta][tb] = tv;
+                    U[ea][eb] = Us[(size_t)q * kJL * kJL + tid];          // U_q[ea][eb]
                     __syncthreads();
                     double2 acc = make_double2(0.0, 0.0);
+                    if (gtile) {
 #pragma unroll 8
-                    for (int m = 0; m < kJL; m++) {   // (U_p^H T)[ta][tb] = sum_m conj(U_p[m][ta]) T[m][tb]
-                        const double2 uu = Up[m][ta], y = Tt[m][tb];
-                        acc.x = fma(uu.x, y.x, acc.x);
-                        acc.x = fma(uu.y, y.y, acc.x);
-                        acc.y = fma(uu.x, y.y, acc.y);
-                        acc.y = fma(-uu.y, y.x, acc.y);
+                        for (int m = 0; m < kJL; m++) {   // (G U_q)[ta][tb]
+                            const double2 uu = U[m][tb], g = A[ta][m];
+                            acc.x = fma(g.x, uu.x, acc.x);
+                            acc.x = fma(-g.y, uu.y, acc.x);
+                            acc.y = fma(g.x, uu.y, acc.y);
+                            acc.y = fma(g.y, uu.x, acc.y);
+                        }
+                        Tt[ta][tb] = acc;
+                        __syncthreads();
+                        acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+                        for (int m = 0; m < kJL; m++) {   // (U_p^H T)[ta][tb] = sum_m conj(U_p[m][ta]) T[m][tb]
+                            const double2 uu = Up[m][ta], y = Tt[m][tb];
+                            acc.x = fma(uu.x, y.x, acc.x);
+                            acc.x = fma(uu.y, y.y, acc.x);
+                            acc.y = fma(uu.x, y.y, acc.y);
+                            acc.y = fma(-uu.y, y.x, acc.y);
+                        }
+                        if (blk_idx(I, J, ta) == blk_idx(K, L, tb)) acc.y = 0.0;  // Hermitian: real diagonal
+                        __syncthreads();   // A fully read before it is overwritten
+                        A[ta][tb] = acc;
+                        __syncthreads();
+                        G[sa + sb * kp] = A[ea][eb];   // coalesced write-back
+                        if (p != q) {                  // G_qp = G_pq^H
+                            const double2 x = A[eb][ea];
+                            G[blk_idx(K, L, ea) + blk_idx(I, J, eb) * kp] = make_double2(x.x, -x.y);
+                        }
+                    } else {
+#pragma unroll 8
+                        for (int m = 0; m < kJL; m++) {   // (V U_q)[ta][tb]
+                            const double2 uu = U[m][tb], v = Vt[ta][m];
+                            acc.x = fma(v.x, uu.x, acc.x);
+                            acc.x = fma(-v.y, uu.y, acc.x);
+                            acc.y = fma(v.x, uu.y, acc.y);
+                            acc.y = fma(v.y, uu.x, acc.y);
+                        }
+                        __syncthreads();
+                        Vt[ta][tb] = acc;
+                        __syncthreads();
+                        V[sa + sb * kp] = Vt[ea][eb];
                     }
-                    if (blk_idx(I, J, ta) == blk_idx(K, L, tb)) acc.y = 0.0;  // Hermitian: real diagonal
-                    A[ta][tb] = acc;
-                    __syncthreads();
-                    G[sa + sb * kp] = A[ea][eb];   // coalesced write-back
-                    V[sa + sb * kp] = Vt[ea][eb];
-                    __syncthreads();   // the tile arrays are refilled for the next tile
+                    __syncthreads();   // the tile arrays are refilled for the next item
                 }
                 grid_barrier(bar, bar + 1, nblocks);
                 if (tr) trace[r * 4 + 2] = trace[r * 4 + 3] = globaltimer_ns();
